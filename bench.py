@@ -1,0 +1,336 @@
+#!/usr/bin/env python3
+"""Benchmark: job-mix instances optimized/sec (BASELINE.json metric) on B200.
+
+Default workload = BASELINE.json configs[1] (config 2): 1M random job mixes per GPU (1-7 jobs
+each, acceptance_test.cpp:72-85 distribution), full search over the 36-entry MIG catalog and
+every distinct job-to-slice assignment (111 candidates). One step = one pass of the partition-
+search kernel over the 1M-instance batch resident in HBM.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N>1 runs under torchrun, one rank per GPU; every rank owns an independent 1M-instance shard
+(weak scaling, no data-path collective); timings are device-side (CUDA events) and the max over
+ranks is reported. `e2e` measures the same metric through the C-ABI host-pointer call
+(pinned host buffers; H2D, search, D2H inside the timed region). `cpu_baseline` times the
+reference's own optimize_partition (oracle/_ref, the unmodified reference headers) on a bounded
+sample with every host thread. `--impl reference` times only that reference CPU path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+METRIC = "job-mix instances optimized/sec (and configs scored/sec) at 1/2/4/8 B200 vs CPU"
+UNIT = "instances/s"
+N_PER_GPU = 1_000_000
+CANDS_PER_M = {1: 5, 2: 13, 3: 29, 4: 35, 5: 21, 6: 7, 7: 1}
+WORKLOAD = ("config2: 1M random job mixes per GPU (m~U{1..7}, acceptance_test.cpp:72-85 "
+            "distribution), exhaustive search over 36 MIG partitions x distinct assignments "
+            "(111 candidates), FP64 objective, reference tie-break")
+
+
+def gen_mixes(seed: int, n: int):
+    """Synthetic config-2 input (same distribution as the reference generator; numpy stream)."""
+    rng = np.random.default_rng(seed)
+    m = rng.integers(1, 8, n)
+    offs = np.zeros(n + 1, np.int64)
+    np.cumsum(m, out=offs[1:])
+    J = int(offs[-1])
+    u = rng.random((J, 5))
+    f4 = 0.2 + 0.8 * u[:, 0]
+    f3 = 0.15 + (f4 - 0.15) * u[:, 1]
+    f2 = 0.1 + (f3 - 0.1) * u[:, 2]
+    f1 = 0.05 + (f2 - 0.05) * u[:, 3]
+    f1[u[:, 4] < 0.25] = 0.0
+    speeds = np.empty((J, 5), np.float64)
+    speeds[:, 0], speeds[:, 1], speeds[:, 2], speeds[:, 3], speeds[:, 4] = f1, f2, f3, f4, 1.0
+    return speeds.reshape(-1), offs.astype(np.uint32), m
+
+
+def candidates_of(m: np.ndarray) -> int:
+    return int(sum(CANDS_PER_M[k] * int((m == k).sum()) for k in CANDS_PER_M))
+
+
+def algorithmic_bytes(m: np.ndarray) -> int:
+    """Per launch: 40 B speeds per job + 4 B offset + 1 B decision + 8 B objective per
+    instance (+ the closing offset). SURVEY.md 8(d) / DESIGN.md."""
+    return int(40 * int(m.sum()) + 13 * len(m) + 4)
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the search kernel from the committed ncu --set full capture."""
+    p = ROOT / "profiles" / "search_kernel_ncu.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed regions run."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+
+    def stop(self):
+        if self._th:
+            self._stop.set()
+            self._th.join()
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+            "source": "nvml" if self.nv else "unavailable",
+        }
+
+
+def cpu_reference_rate(speeds, offs, m, target_s: float = 12.0):
+    """Reference optimize_partition (oracle/_ref) on every host thread over a bounded sample of
+    the same workload. Falls back to the C restatement (kind "port") if _ref is absent."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    threads = oracle_lib.host_threads()
+    if oracle_lib.have_ref():
+        impl, kind = oracle_lib.Ref(), "reference"
+        run = lambda s, f: impl.optimize_batch(s, f, threads=threads)  # noqa: E731
+    else:
+        impl, kind, threads = oracle_lib.Oracle(), "port", 1
+        run = lambda s, f: impl.optimize_batch(s, f)  # noqa: E731
+
+    def sample(n):
+        f = offs[: n + 1]
+        return speeds[: int(f[-1]) * 5], f
+
+    n = min(100_000, len(m))
+    t0 = time.perf_counter(); run(*sample(n)); dt = time.perf_counter() - t0
+    n = int(min(len(m), max(n, n * target_s / max(dt, 1e-6))))
+    t0 = time.perf_counter(); run(*sample(n)); dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"first {n} instances of the rank-0 config-2 batch, one pass, "
+                      f"{threads} host threads, {dt:.2f} s",
+            "candidates_per_s": candidates_of(m[:n]) / dt}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    speeds, offs, m = gen_mixes(12345, N_PER_GPU)
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    threads = oracle_lib.host_threads()
+    if oracle_lib.have_ref():
+        impl, kind = oracle_lib.Ref(), "reference"
+        run = lambda s, f: impl.optimize_batch(s, f, threads=threads)  # noqa: E731
+    else:
+        impl, kind, threads = oracle_lib.Oracle(), "port", 1
+        run = lambda s, f: impl.optimize_batch(s, f)  # noqa: E731
+    per_step = 250_000
+    f = offs[: per_step + 1]
+    s = speeds[: int(f[-1]) * 5]
+    for _ in range(args.warmup):
+        run(s, f)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run(s, f)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "instances_per_step": per_step,
+                   "sample": "bounded sample of the config-2 batch per step"},
+        "configs_scored_per_s": candidates_of(m[:per_step]) * args.steps / dt,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{per_step} instances per step, {threads} host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    import paper_2207_11428_b200 as miso
+    from paper_2207_11428_b200._native import host_alloc, host_free
+    ctx = miso.Context(local)
+
+    speeds, offs, m = gen_mixes(1000 + rank, N_PER_GPU)
+    n = len(m)
+    d_speeds = torch.from_numpy(speeds).cuda()
+    d_offs = torch.from_numpy(offs.view(np.int32)).cuda()
+    d_cand = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d_obj = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        ctx.optimize_batch(d_speeds, d_offs, d_cand, d_obj)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(); torch.cuda.synchronize()
+    t_start.record(stream)
+    for i in range(K):
+        ev[i][0].record(stream)
+        ctx.optimize_batch(d_speeds, d_offs, d_cand, d_obj)
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize(); barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+
+    # --- e2e: the C-ABI host-pointer call, pinned buffers, H2D + search + D2H timed ---
+    import ctypes as C
+    nb_s, nb_o = speeds.nbytes, offs.nbytes
+    p_s, p_o, p_c, p_b = host_alloc(nb_s), host_alloc(nb_o), host_alloc(n), host_alloc(8 * n)
+    C.memmove(p_s, speeds.ctypes.data, nb_s)
+    C.memmove(p_o, offs.ctypes.data, nb_o)
+    lib = miso.lib
+    for _ in range(2):
+        lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
+    E = max(3, min(K, 20))
+    barrier(); torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for _ in range(E):
+        rc = lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
+        assert rc == 0, lib.miso_b200_last_error()
+    e2e_s = time.perf_counter() - w0
+    barrier()
+    clk = clocks.stop()
+    h_c = np.ctypeslib.as_array((C.c_uint8 * n).from_address(p_c)).copy()
+    h_b = np.ctypeslib.as_array((C.c_double * n).from_address(p_b)).copy()
+    d_c = d_cand.cpu().numpy()
+    assert np.array_equal(h_c, d_c) and np.array_equal(h_b.view(np.uint64), d_obj.cpu().numpy().view(np.uint64))
+    for p in (p_s, p_o, p_c, p_b):
+        host_free(p)
+
+    # max over ranks
+    t = torch.tensor([total_ms, kern_ms, e2e_s], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        stats = torch.tensor([float((d_c < 111).sum()), float(d_obj.sum().item())],
+                             dtype=torch.float64, device="cuda")
+        dist.all_reduce(stats)  # final statistics gather (feasible count, objective checksum)
+    total_ms, kern_ms, e2e_s = t.tolist()
+
+    if rank == 0:
+        value = world * n * K / (total_ms / 1e3)
+        cands = candidates_of(m)
+        alg = algorithmic_bytes(m)
+        achieved = alg / (kern_ms / 1e3) / 1e9
+        peak, peak_src = measured_peak()
+        traffic = ncu_traffic()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "instances_per_gpu": n, "jobs_per_gpu": int(m.sum()),
+                       "candidates_per_gpu_step": cands,
+                       "l2": "inputs %.0f MB per GPU > 126 MB L2; no flush" % ((speeds.nbytes + offs.nbytes) / 1e6),
+                       "parallelism": f"{world} independent shards"},
+            "configs_scored_per_s": world * cands * K / (total_ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "optimize_tile_kernel", "kernel_ms": kern_ms,
+                         "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+            "e2e": {"value": world * n * E / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": nb_s + nb_o, "d2h_bytes_per_step": n * 9,
+                    "api": "miso_b200_optimize_batch_host (pinned host buffers)", "steps": E},
+            "clocks": clk,
+            "gpu_launches": K,
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference_rate(speeds, offs, m)
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,95 @@
+/*
+ * miso_b200.h -- C ABI of the B200-native MISO decision core.
+ *
+ * Plain pointers and sizes, no C++ or torch types. Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj/include/miso/). Status
+ * codes mirror the reference CLI's exit codes (tools/miso_cli.cpp:4-5) as negatives:
+ *   0 ok, -1 unexpected/CUDA error, -2 invalid argument, -3 malformed input, -4 infeasible.
+ * Per-item outcomes of batch calls are reported in-band (see MISO_B200_CAND_*), never by
+ * aborting the batch: the reference throws per call, a batch reports per instance.
+ *
+ * Threading: one context per device; a context may be used from one host thread at a time.
+ * Device-pointer calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy default
+ * stream) and do not synchronize. Host-pointer calls (`*_host`) are synchronous and overlap
+ * H2D, compute and D2H internally; pass pinned memory (miso_b200_host_alloc) for full speed.
+ */
+#ifndef MISO_B200_H
+#define MISO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MISO_B200_OK 0
+#define MISO_B200_E_UNEXPECTED (-1)
+#define MISO_B200_E_INVALID (-2)
+#define MISO_B200_E_MALFORMED (-3)
+#define MISO_B200_E_INFEASIBLE (-4)
+
+/* Per-instance decision byte written by the optimize calls:
+ *   0..110  winning candidate id (decode with miso_b200_candidate)
+ *   0xFF    no valid assignment       == optimize_partition returning std::nullopt
+ *                                        (optimizer.hpp:102)
+ *   0xFE    job count m outside 1..7  == optimize_partition throwing invalid_argument
+ *                                        (optimizer.hpp:65-66)                          */
+#define MISO_B200_CAND_INFEASIBLE 0xFF
+#define MISO_B200_CAND_BAD_M 0xFE
+#define MISO_B200_NUM_CANDIDATES 111
+#define MISO_B200_NUM_KINDS 5 /* slice kinds 1g,2g,3g,4g,7g = 0..4 (topology.hpp:27-45) */
+
+typedef struct miso_b200_ctx miso_b200_ctx;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int miso_b200_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* miso_b200_last_error(void);
+
+/* Create/destroy a context on a CUDA device. Owns the candidate table for its catalog and
+ * scratch buffers for the host-pointer paths. */
+int miso_b200_create(int device, miso_b200_ctx** out);
+void miso_b200_destroy(miso_b200_ctx* ctx);
+
+/* Replaces PartitionCatalog (topology.hpp:184-208, load_catalog :276-326): `counts` holds
+ * n_entries rows of per-kind counts [1g,2g,3g,4g,7g] in the catalog's own order (the order
+ * entry indices refer to). Rows must be feasible partitions (PartitionConfig::violation,
+ * topology.hpp:84-101) and distinct; else -2. A new context uses default_catalog()
+ * (topology.hpp:205-208). */
+int miso_b200_set_catalog(miso_b200_ctx* ctx, const uint8_t* counts, int n_entries);
+/* Copies the active catalog (<= 36 rows of 5 counts) into `counts`; returns n_entries. */
+int miso_b200_get_catalog(const miso_b200_ctx* ctx, uint8_t* counts);
+
+/* Decodes a candidate id: its index in the ACTIVE catalog (-1 if the entry is not in it),
+ * its job count m and the slice kind of each job (place[0..m-1]). */
+int miso_b200_candidate(const miso_b200_ctx* ctx, int cand, int* entry, int* m, uint8_t place[7]);
+
+/* Batched optimize_partition (optimizer.hpp:62-115) over independent job mixes, DEVICE
+ * pointers. speeds: packed rows of 5 FP64 effective speeds (kind order 1g..7g, already zeroed
+ * by effective_speed, profiles.hpp:60-65) for sum(m) jobs; offsets: n+1 job offsets (instance
+ * i owns rows offsets[i]..offsets[i+1]-1). Writes cand[i] (see MISO_B200_CAND_*) and obj[i]
+ * (the FP64 objective, bit-exact with the reference; 0 when no decision). */
+int miso_b200_optimize_batch(miso_b200_ctx* ctx, const double* speeds, const uint32_t* offsets,
+                             uint64_t n, uint8_t* cand, double* obj, void* stream);
+
+/* Same contract with HOST pointers: chunked H2D -> search -> D2H pipeline over two streams.
+ * Synchronous. */
+int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
+                                  const uint32_t* offsets, uint64_t n, uint8_t* cand,
+                                  double* obj);
+
+/* One-instance drop-in for optimize_partition (optimizer.hpp:62-63), host pointers.
+ * Returns 1 (decision written: entry index in the active catalog, place[m], *obj),
+ * 0 (std::nullopt) or -2 (m outside 1..7, invalid_argument). */
+int miso_b200_optimize(miso_b200_ctx* ctx, const double* speeds, int m, int* entry,
+                       uint8_t* place, double* obj);
+
+/* Pinned host memory for the *_host paths. */
+int miso_b200_host_alloc(size_t bytes, void** out);
+void miso_b200_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MISO_B200_H */

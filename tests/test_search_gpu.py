@@ -1,0 +1,183 @@
+"""GPU parity tests for kernel (b), the batched partition search, through the C ABI.
+
+Bar: bit-exact candidate, placement and FP64 objective versus the oracle (oracle/, itself
+pinned to the reference's golden vectors in test_oracle.py) and the golden fixtures.
+"""
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.asarray(a, np.float64).view(np.uint64)
+
+
+def check_against(ctx, speeds, offsets, entry, place, obj, cand=None, got_obj=None):
+    if cand is None:
+        cand, got_obj = ctx.optimize_batch(speeds, offsets)
+    e, p = ctx.decode(cand, offsets)
+    assert np.array_equal(e, entry.astype(np.int32)), np.nonzero(e != entry)[0][:10]
+    feas = np.repeat(entry >= 0, np.diff(offsets.astype(np.int64)))
+    assert np.array_equal(p[feas], place[: len(feas)][feas])
+    assert np.array_equal(bits(got_obj), bits(obj))
+
+
+@pytest.mark.parametrize("name", ["opt_random_0b5e55ed", "opt_accept_acce91", "opt_ties_71e5"])
+def test_golden_host_path(ctx, golden, name):
+    g = np.load(golden / f"{name}.npz")
+    check_against(ctx, g["speeds"], g["offsets"], g["entry"], g["place"], g["obj"])
+
+
+@pytest.mark.parametrize("name", ["opt_random_0b5e55ed", "opt_ties_71e5"])
+def test_golden_device_path(ctx, golden, name):
+    import torch
+    g = np.load(golden / f"{name}.npz")
+    s = torch.from_numpy(g["speeds"]).cuda()
+    o = torch.from_numpy(g["offsets"].astype(np.int32)).cuda()
+    cand, obj = ctx.optimize_batch(s, o)
+    torch.cuda.synchronize()
+    check_against(ctx, g["speeds"], g["offsets"], g["entry"], g["place"], g["obj"],
+                  cand.cpu().numpy(), obj.cpu().numpy())
+
+
+def test_literal_cases_dropin(ctx, golden):
+    """optimizer_test.cpp:29-106 through the reference-shaped single-instance API."""
+    lit = json.loads((golden / "opt_literal.json").read_text())
+    for name, case in lit.items():
+        sp = np.array(case["speeds"]).reshape(-1, 5)
+        jobs = [(f"j{i}", sp[i]) for i in range(len(sp))]
+        r = ctx.optimize_partition(jobs)
+        if case["entry"] < 0:
+            assert r is None, name
+            continue
+        assert r.entry == case["entry"], name
+        assert [a.slice for a in r.assignments] == case["place"], name
+        assert float(r.objective).hex() == case["obj_hex"], name
+        for i, a in enumerate(r.assignments):
+            assert a.job_id == f"j{i}" and a.speed == sp[i, a.slice]
+    r = ctx.optimize_partition([("j1", [0.3, 0.5, 0.85, 0.9, 1.0]), ("j2", [0.35, 0.4, 0.5, 0.6, 1.0])])
+    assert r.partition_name == "3g+3g" and abs(r.objective - 1.35) < 1e-12
+
+
+def test_job_count_out_of_range(ctx):
+    with pytest.raises(ValueError):
+        ctx.optimize_partition([])
+    with pytest.raises(ValueError):
+        ctx.optimize_partition([("x", [1, 1, 1, 1, 1])] * 8)
+    cand, obj = ctx.optimize_batch(np.ones(8 * 5), np.array([0, 0, 8, 8], np.uint32))
+    assert list(cand) == [0xFE, 0xFE, 0xFE] and list(obj) == [0, 0, 0]
+
+
+def test_empty_batch(ctx):
+    cand, obj = ctx.optimize_batch(np.zeros(0), np.array([0], np.uint32))
+    assert len(cand) == 0 and len(obj) == 0
+
+
+def test_config2_million_vs_oracle(ctx, oracle):
+    """Config 2 (1M acceptance-generator mixes) bit-exact against the oracle."""
+    s, f = oracle.gen_mixes(0xACCE91, 1_000_000)
+    e, p, o = oracle.optimize_batch(s, f)
+    check_against(ctx, s, f, e, p, o)
+
+
+def test_special_values(ctx, oracle):
+    """NaN, +-inf, -0.0, subnormals, negatives: validity is exactly `v > 0`."""
+    rng = np.random.default_rng(3)
+    vals = np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, 5e-324, -1.0, 0.5, 1.0, 1e308, 0.25])
+    sizes = rng.integers(1, 8, 20000)
+    f = np.concatenate([[0], np.cumsum(sizes)]).astype(np.uint32)
+    s = vals[rng.integers(0, len(vals), int(f[-1]) * 5)]
+    e, p, o = oracle.optimize_batch(s, f)
+    check_against(ctx, s, f, e, p, o)
+
+
+def test_all_m7_and_all_m1_tiles(ctx, oracle):
+    """Tiles at the maximum staged size (every instance m=7) and the minimum."""
+    rng = np.random.default_rng(5)
+    for m in (7, 1, 4):
+        n = 3000
+        f = (np.arange(n + 1) * m).astype(np.uint32)
+        s = rng.uniform(0.01, 1.0, n * m * 5)
+        e, p, o = oracle.optimize_batch(s, f)
+        check_against(ctx, s, f, e, p, o)
+
+
+def test_misaligned_device_base(ctx, oracle):
+    """Speeds base pointer only 8-byte aligned (a view one row-element in)."""
+    import torch
+    s, f = oracle.gen_mixes(99, 5000)
+    e, p, o = oracle.optimize_batch(s, f)
+    buf = torch.zeros(len(s) + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = torch.from_numpy(s).cuda()
+    cand, obj = ctx.optimize_batch(buf[1:], torch.from_numpy(f.astype(np.int32)).cuda())
+    torch.cuda.synchronize()
+    check_against(ctx, s, f, e, p, o, cand.cpu().numpy(), obj.cpu().numpy())
+
+
+def test_catalog_subset(ctx, oracle):
+    """A file-loaded catalog (topology.hpp:276-326) is any subset of the 36 entries."""
+    from oracle_lib import OrcCatalog
+    import ctypes as C
+    rng = np.random.default_rng(11)
+    full = oracle.catalog_counts()
+    s, f = oracle.gen_mixes(4242, 20000)
+    try:
+        for trial in range(4):
+            keep = np.sort(rng.choice(36, size=int(rng.integers(3, 30)), replace=False))
+            sub = full[keep]
+            ctx.set_catalog(sub)
+            cat = OrcCatalog()
+            cat.n_entries = len(sub)
+            for i, row in enumerate(sub):
+                for k in range(5):
+                    cat.counts[i][k] = int(row[k])
+            n = len(f) - 1
+            e = np.zeros(n, np.int16); p = np.zeros(int(f[-1]), np.uint8); o = np.zeros(n)
+            oracle.lib.orc_optimize_batch(C.byref(cat), s, f, n, e, p, o)
+            check_against(ctx, s, f, e, p, o)
+    finally:
+        ctx.set_catalog(full)
+
+
+def test_invalid_catalog_rejected(ctx):
+    import paper_2207_11428_b200 as m
+    with pytest.raises(m.MisoError) as ei:
+        ctx.set_catalog([[0, 0, 1, 1, 0]])  # 4g + 3g cannot co-exist
+    assert ei.value.code == -2
+    with pytest.raises(m.MisoError):
+        ctx.set_catalog([[1, 0, 0, 0, 0], [1, 0, 0, 0, 0]])  # duplicate
+
+
+def test_full_size_properties(ctx, oracle):
+    """At 8M instances: every decision is consistent with its own inputs (placement speeds
+    > 0, objective == job-order sum, partition size == m), and a sampled slice matches the
+    oracle exactly."""
+    import torch
+    s, f = oracle.gen_mixes(0xB200, 8_000_000)
+    ds = torch.from_numpy(s).cuda()
+    df = torch.from_numpy(f.astype(np.int32)).cuda()
+    cand, obj = ctx.optimize_batch(ds, df)
+    cand = cand.cpu().numpy(); obj = obj.cpu().numpy()
+    ent, ms, pl = ctx.candidate_table()
+    m = np.diff(f.astype(np.int64))
+    ok = cand < 111
+    assert np.all(cand[~ok] == 0xFF)
+    assert np.array_equal(ms[cand[ok]], m[ok])
+    sp = s.reshape(-1, 5)
+    acc = np.zeros(ok.sum())
+    idx = np.nonzero(ok)[0]
+    for j in range(7):
+        has = m[idx] > j
+        rows = f[idx[has]].astype(np.int64) + j
+        v = sp[rows, pl[cand[idx[has]], j]]
+        assert np.all(v > 0)
+        acc[has] = acc[has] + v
+    assert np.array_equal(bits(acc), bits(obj[ok]))
+    sl = slice(3_000_000, 3_050_000)
+    sub_f = (f[sl.start: sl.stop + 1] - f[sl.start]).astype(np.uint32)
+    sub_s = s[int(f[sl.start]) * 5: int(f[sl.stop]) * 5]
+    e, p, o = oracle.optimize_batch(sub_s, sub_f)
+    check_against(ctx, sub_s, sub_f, e, p, o, cand[sl], obj[sl])
