@@ -1,27 +1,64 @@
 // search_kernel.cu -- batched partition search (kernel (b)), one thread per instance.
 //
-// Data flow per CTA tile of kTile consecutive instances:
-//   1. offsets[t0 .. t0+kTile] -> shared; m_i = offsets[i+1] - offsets[i].
-//   2. the tile's packed speed rows (a contiguous byte range of the CSR speeds array) are
-//      streamed into shared memory with coalesced 16-byte loads;
-//   3. instances are bucketed by m inside the CTA (shared-memory counting sort) so the 32
-//      threads of a warp run the same straight-line search_m<M> (no 7-way divergence);
-//   4. each thread scores all candidates of its instance from registers (search.cuh);
-//   5. decisions/objectives are staged in shared memory and written back coalesced.
-// HBM traffic per instance = 40m (speeds) + 4 (offset) + 1 (cand) + 8 (objective) bytes.
+// Default path: optimize_pipe_kernel, a persistent warp-specialized pipeline (see below): a
+// producer warp streams kT-instance tiles (offsets + CSR speed rows) into a kS-stage
+// shared-memory ring with TMA bulk copies; consumer groups bucket each tile by job count m and
+// search one instance per thread from registers (search.cuh).
+// Fallback (speeds not 16-byte aligned, or MISO_B200_SIMPLE_SEARCH=1): optimize_tile_kernel,
+// one CTA per tile with a synchronous staged copy.
+//
+// HBM traffic per instance = 40m (speeds) + 4 (offset) + 1 (decision) + 8 (objective) bytes.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 #include "search.cuh"
+#include "tma.cuh"
+
+#ifndef MISO_B200_TRACE
+#define MISO_B200_TRACE 0
+#endif
 
 namespace miso_b200 {
 
+#if MISO_B200_TRACE
+// Debug timeline (tools/trace_search.cu): [blockIdx][event] = globaltimer.
+__device__ unsigned long long g_trace[148][4096];
+__device__ __forceinline__ void trace(int slot) {
+  if (blockIdx.x < 148 && slot < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[blockIdx.x][slot] = t;
+  }
+}
+#define TRACE(slot) trace(slot)
+#else
+#define TRACE(slot) ((void)0)
+#endif
+
+static bool force_simple_path() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MISO_B200_SIMPLE_SEARCH");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+__device__ __forceinline__ int valid_m(uint32_t mm) {
+  return (mm >= 1 && mm <= 7) ? static_cast<int>(mm) : 0;
+}
+
+// ---------------------------------------------------------------------------------------
+// Fallback: one-shot tile kernel.
+// ---------------------------------------------------------------------------------------
 constexpr int kTile = 256;
 constexpr int kMaxRowsPerTile = kTile * 7;
-constexpr size_t kStageBytes = size_t(kMaxRowsPerTile) * 5 * sizeof(double) + 16;
+constexpr size_t kTileStageBytes = size_t(kMaxRowsPerTile) * 5 * sizeof(double) + 16;
 
+template <bool kAll>
 __global__ void __launch_bounds__(kTile) optimize_tile_kernel(
     const double* __restrict__ speeds, const uint32_t* __restrict__ offsets, uint64_t n,
     uint8_t* __restrict__ cand_out, double* __restrict__ obj_out, uint64_t en0, uint64_t en1) {
@@ -46,10 +83,8 @@ __global__ void __launch_bounds__(kTile) optimize_tile_kernel(
   const uint32_t njobs = s_off[cnt] - j0;
   const bool staged = njobs <= uint32_t(kMaxRowsPerTile) && s_off[cnt] >= j0;
 
-  // --- 2. stage the tile's speed rows: 16-byte chunks, aligned on the absolute address ---
   const double* gsrc = speeds + size_t(j0) * 5;
-  const unsigned char* gbytes = reinterpret_cast<const unsigned char*>(gsrc);
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(gbytes);
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(gsrc);
   const uintptr_t abase = a0 & ~uintptr_t(15);
   const int lead = static_cast<int>(a0 - abase);  // 0 or 8 (rows are 8-byte aligned)
   double* srows = reinterpret_cast<double*>(smem_raw + lead);
@@ -68,11 +103,9 @@ __global__ void __launch_bounds__(kTile) optimize_tile_kernel(
       srows[size_t(njobs) * 5 - 1] = __ldg(gsrc + size_t(njobs) * 5 - 1);
   }
 
-  // --- 3. bucket instances by m ---
   int my_m = 0, my_rank = 0;
   if (tid < cnt) {
-    uint32_t mm = s_off[tid + 1] - s_off[tid];
-    my_m = (mm >= 1 && mm <= 7) ? static_cast<int>(mm) : 0;
+    my_m = valid_m(s_off[tid + 1] - s_off[tid]);
     my_rank = atomicAdd(&s_cnt[my_m], 1);
   }
   __syncthreads();
@@ -84,47 +117,294 @@ __global__ void __launch_bounds__(kTile) optimize_tile_kernel(
   if (tid < cnt) s_order[s_base[my_m] + my_rank] = static_cast<uint16_t>(tid);
   __syncthreads();
 
-  // --- 4. search ---
   if (tid < cnt) {
     const int l = s_order[tid];
     const uint32_t o = s_off[l];
-    const uint32_t mm = s_off[l + 1] - o;
-    const int m = (mm >= 1 && mm <= 7) ? static_cast<int>(mm) : 0;
+    const int m = valid_m(s_off[l + 1] - o);
     double obj = 0.0;
     uint8_t c;
     // Rows outside the staged range only occur with non-monotonic (malformed) offsets.
     if (staged && o >= j0 && o - j0 + uint32_t(m) <= njobs)
-      c = search_any(srows + size_t(o - j0) * 5, m, en0, en1, &obj);
+      c = search_any<kAll>(srows + size_t(o - j0) * 5, m, en0, en1, &obj);
     else
-      c = search_any(speeds + size_t(o) * 5, m, en0, en1, &obj);
+      c = search_any<kAll>(speeds + size_t(o) * 5, m, en0, en1, &obj);
     s_cand[l] = c;
     s_obj[l] = obj;
   }
   __syncthreads();
 
-  // --- 5. coalesced write-back ---
   if (tid < cnt) {
     cand_out[t0 + tid] = s_cand[tid];
     obj_out[t0 + tid] = s_obj[tid];
   }
 }
 
-cudaError_t launch_optimize(const double* speeds, const uint32_t* offsets, uint64_t n,
+// ---------------------------------------------------------------------------------------
+// Persistent warp-specialized TMA pipeline (default path).
+//
+//   producer warp: for each tile of kT instances, waits for a free stage of the kS-stage
+//     shared-memory ring and issues two cp.async.bulk (TMA 1-D bulk) copies -- the tile's
+//     kT+1 offsets and its contiguous speed rows -- completing on full[stage]. Tile boundaries
+//     (offsets[t0], offsets[t0+cnt]) are prefetched 32 tiles at a time (lane l holds tile
+//     k+l), so issuing never waits on a dependent global load.
+//   kG consumer groups of kT threads take alternate tiles: bucket the tile by job count m
+//     (shared-memory counting sort, so every warp runs one straight-line search_m<M>), search
+//     one instance per thread from registers (search.cuh), release the stage (empty[stage]),
+//     and flush the previous tile's decisions coalesced (double-buffered, 2 named barriers
+//     per tile).
+// ---------------------------------------------------------------------------------------
+template <int kT, int kS, int kCap>
+struct PipeLayout {
+  static constexpr int kOffWords = ((kT + 1 + 3) / 4) * 4;
+  static constexpr size_t kRowBytes = size_t(kCap) * 40 + 32;
+  static constexpr size_t kStageBytes = ((kOffWords * 4 + kRowBytes + 127) / 128) * 128;
+  static constexpr size_t kBytes = kStageBytes * kS + 128;
+};
+
+template <int kT, int kS, int kCap, int kG, bool kAll>
+__global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
+    const double* __restrict__ speeds, const uint32_t* __restrict__ offsets, uint64_t n,
+    uint8_t* __restrict__ cand_out, double* __restrict__ obj_out, uint64_t en0, uint64_t en1) {
+  static_assert(kS % kG == 0, "each consumer group owns every kG-th stage");
+  using L = PipeLayout<kT, kS, kCap>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full_bar[kS], empty_bar[kS];
+  __shared__ int s_cnt[kG][2][8];
+  __shared__ uint16_t s_order[kG][kT];
+  __shared__ double s_obj[kG][2][kT];
+  __shared__ uint8_t s_cand[kG][2][kT];
+
+  const int tid = threadIdx.x;
+  const uint64_t ntiles = (n + kT - 1) / kT;
+  if (tid == 0) {
+    for (int s = 0; s < kS; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], kT / 32);
+    }
+    fence_mbar_init();
+  }
+  if (tid < kG * 16) (&s_cnt[0][0][0])[tid] = 0;
+  __syncthreads();
+
+  auto stage_base = [&](int s) { return smem + size_t(s) * L::kStageBytes; };
+
+  if (tid >= kT * kG) {
+    // ------------------------------ producer warp ------------------------------
+    const int lane = tid & 31;
+    uint32_t pre0 = 0, pre1 = 0;
+    const uintptr_t speeds_end =
+        reinterpret_cast<uintptr_t>(speeds + size_t(__ldg(offsets + n)) * 5);
+    int k = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      if ((k & 31) == 0) {
+        const uint64_t tl = tile + uint64_t(lane) * gridDim.x;
+        if (tl < ntiles) {
+          const uint64_t t0l = tl * kT;
+          const uint64_t cl = n - t0l < uint64_t(kT) ? n - t0l : uint64_t(kT);
+          pre0 = __ldg(offsets + t0l);
+          pre1 = __ldg(offsets + t0l + cl);
+        }
+      }
+      const uint32_t o0 = __shfl_sync(0xffffffffu, pre0, k & 31);
+      const uint32_t oend = __shfl_sync(0xffffffffu, pre1, k & 31);
+      const int st = k % kS;
+      const uint32_t ph = (k / kS) & 1;
+      if (lane == 0) {
+        if (k >= kS) mbar_wait(&empty_bar[st], ph ^ 1);
+        TRACE(k * 16 + 3);
+        const uint64_t t0 = tile * kT;
+        const uint32_t cnt = static_cast<uint32_t>(n - t0 < uint64_t(kT) ? n - t0 : uint64_t(kT));
+        unsigned char* base = stage_base(st);
+        uint32_t* so = reinterpret_cast<uint32_t*>(base);
+        // offsets[t0 .. t0+cnt] by whole 16-byte chunks; words of a chunk that would run past
+        // offsets[n] (end of the array) are loaded directly instead.
+        uint32_t owords = (cnt + 1 + 3) & ~3u;
+        uint32_t odirect = 0;
+        if (t0 + owords > n + 1) {
+          owords = (cnt + 1) & ~3u;
+          odirect = cnt + 1 - owords;
+        }
+        const uint32_t njobs = oend - o0;
+        const bool staged = oend >= o0 && njobs <= uint32_t(kCap) && njobs > 0;
+        uint32_t rbytes = 0;
+        uintptr_t abase = 0, end = 0, aend_tma = 0;
+        if (staged) {
+          const uintptr_t a0 = reinterpret_cast<uintptr_t>(speeds + size_t(o0) * 5);
+          end = a0 + size_t(njobs) * 40;
+          abase = a0 & ~uintptr_t(15);
+          // Round the end up to 16 bytes when that stays inside the speeds array (the extra
+          // <= 8 bytes are the next tile's); otherwise load the trailing double directly.
+          const uintptr_t up = (end + 15) & ~uintptr_t(15);
+          aend_tma = up <= speeds_end ? up : (end & ~uintptr_t(15));
+          rbytes = static_cast<uint32_t>(aend_tma - abase);
+        }
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(
+                         smem_u32(&full_bar[st])),
+                     "r"(owords * 4 + rbytes)
+                     : "memory");
+        if (owords) bulk_g2s(so, offsets + t0, owords * 4, &full_bar[st]);
+        unsigned char* rows = base + L::kOffWords * 4;
+        if (rbytes) bulk_g2s(rows, reinterpret_cast<const void*>(abase), rbytes, &full_bar[st]);
+        for (uint32_t w = 0; w < odirect; ++w) so[owords + w] = __ldg(offsets + t0 + owords + w);
+        if (staged && aend_tma < end)
+          *reinterpret_cast<double*>(rows + rbytes) =
+              __ldg(reinterpret_cast<const double*>(aend_tma));
+        mbar_arrive(&full_bar[st]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // -------------------------------- consumers --------------------------------
+  const int g = tid / kT;   // consumer group
+  const int ct = tid % kT;  // thread within group
+  const int lane = tid & 31;
+  int k = 0;  // this group's tile count; it owns CTA tile numbers kk = g, g+kG, ...
+  uint64_t prev_t0 = 0;
+  int prev_cnt = 0;
+  for (uint64_t tile = blockIdx.x + uint64_t(g) * gridDim.x; tile < ntiles;
+       tile += uint64_t(kG) * gridDim.x) {
+    const int kk = k * kG + g;
+    ++k;
+    const int st = kk % kS;
+    const uint32_t ph = (kk / kS) & 1;
+    const int p = k & 1;
+    mbar_wait(&full_bar[st], ph);
+    if (ct == 0) TRACE(kk * 16 + 6);
+    const unsigned char* base = stage_base(st);
+    const uint32_t* so = reinterpret_cast<const uint32_t*>(base);
+    const uint64_t t0 = tile * kT;
+    const int cnt = static_cast<int>(n - t0 < uint64_t(kT) ? n - t0 : uint64_t(kT));
+    const uint32_t j0 = so[0], oend = so[cnt];
+    const uint32_t njobs = oend - j0;
+    const bool staged = oend >= j0 && njobs <= uint32_t(kCap) && njobs > 0;  // == producer's
+    const uint32_t lead =
+        static_cast<uint32_t>(reinterpret_cast<uintptr_t>(speeds + size_t(j0) * 5) & 15);
+    const double* srows = reinterpret_cast<const double*>(base + L::kOffWords * 4 + lead);
+
+    int my_m = 0, my_rank = 0;
+    if (ct < cnt) {
+      my_m = valid_m(so[ct + 1] - so[ct]);
+      my_rank = atomicAdd(&s_cnt[g][p][my_m], 1);
+    }
+    named_bar_sync(1 + g, kT);
+    // Everyone finished the previous tile: flush its decisions (coalesced) from buffer p^1.
+    if (ct < prev_cnt) {
+      cand_out[prev_t0 + ct] = s_cand[g][p ^ 1][ct];
+      obj_out[prev_t0 + ct] = s_obj[g][p ^ 1][ct];
+    }
+    if (ct == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s_cnt[g][p ^ 1][q] = 0;
+    }
+    if (ct < cnt) {
+      int b = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) b += q < my_m ? s_cnt[g][p][q] : 0;
+      s_order[g][b + my_rank] = static_cast<uint16_t>(ct);
+    }
+    named_bar_sync(1 + g, kT);
+    if (ct < cnt) {
+      const int l = s_order[g][ct];
+      const uint32_t o = so[l];
+      const int m = valid_m(so[l + 1] - o);
+      double obj = 0.0;
+      uint8_t c;
+      if (staged && o >= j0 && o - j0 + uint32_t(m) <= njobs)
+        c = search_any<kAll>(srows + size_t(o - j0) * 5, m, en0, en1, &obj);
+      else
+        c = search_any<kAll>(speeds + size_t(o) * 5, m, en0, en1, &obj);
+      s_cand[g][p][l] = c;
+      s_obj[g][p][l] = obj;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[st]);
+    if (ct == 0) TRACE(kk * 16 + 7);
+    prev_t0 = t0;
+    prev_cnt = cnt;
+  }
+  named_bar_sync(1 + g, kT);
+  if (ct < prev_cnt) {
+    const int p = k & 1;
+    cand_out[prev_t0 + ct] = s_cand[g][p][ct];
+    obj_out[prev_t0 + ct] = s_obj[g][p][ct];
+  }
+}
+
+template <int kT, int kS, int kCap, int kG, bool kAll>
+cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint64_t n,
                             uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
                             cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
+  using L = PipeLayout<kT, kS, kCap>;
+  auto kern = optimize_pipe_kernel<kT, kS, kCap, kG, kAll>;
+  static int grid_cap = 0;
+  if (!grid_cap) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(L::kBytes));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT * kG + 32, L::kBytes);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const uint64_t tiles = (n + kT - 1) / kT;
+  const unsigned grid = static_cast<unsigned>(tiles < uint64_t(grid_cap) ? tiles : uint64_t(grid_cap));
+  kern<<<grid, kT * kG + 32, L::kBytes, stream>>>(speeds, offsets, n, cand, obj, en0, en1);
+  return cudaGetLastError();
+}
+
+// MISO_B200_PIPE_CFG selects a tile/stage/group configuration (tuning only).
+static int pipe_cfg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MISO_B200_PIPE_CFG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <bool kAll>
+cudaError_t launch_pipe(const double* speeds, const uint32_t* offsets, uint64_t n, uint8_t* cand,
+                        double* obj, uint64_t en0, uint64_t en1, cudaStream_t stream) {
+  switch (pipe_cfg()) {
+    case 1: return launch_pipe_cfg<128, 8, 640, 4, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    case 2: return launch_pipe_cfg<128, 6, 640, 3, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    default: return launch_pipe_cfg<256, 4, 1280, 2, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+  }
+}
+
+template <bool kAll>
+cudaError_t launch_tile(const double* speeds, const uint32_t* offsets, uint64_t n, uint8_t* cand,
+                        double* obj, uint64_t en0, uint64_t en1, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(optimize_tile_kernel,
+    cudaError_t e = cudaFuncSetAttribute(optimize_tile_kernel<kAll>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kStageBytes));
+                                         static_cast<int>(kTileStageBytes));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const uint64_t blocks = (n + kTile - 1) / kTile;
-  optimize_tile_kernel<<<static_cast<unsigned>(blocks), kTile, kStageBytes, stream>>>(
+  optimize_tile_kernel<kAll><<<static_cast<unsigned>(blocks), kTile, kTileStageBytes, stream>>>(
       speeds, offsets, n, cand, obj, en0, en1);
   return cudaGetLastError();
+}
+
+constexpr uint64_t kAllEn0 = ~0ull, kAllEn1 = (1ull << (kNumCands - 64)) - 1;
+
+cudaError_t launch_optimize(const double* speeds, const uint32_t* offsets, uint64_t n,
+                            uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
+                            cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const bool all = en0 == kAllEn0 && en1 == kAllEn1;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(speeds) | reinterpret_cast<uintptr_t>(offsets)) & 15) == 0;
+  if (aligned && !force_simple_path())
+    return all ? launch_pipe<true>(speeds, offsets, n, cand, obj, en0, en1, stream)
+               : launch_pipe<false>(speeds, offsets, n, cand, obj, en0, en1, stream);
+  return all ? launch_tile<true>(speeds, offsets, n, cand, obj, en0, en1, stream)
+             : launch_tile<false>(speeds, offsets, n, cand, obj, en0, en1, stream);
 }
 
 }  // namespace miso_b200

@@ -181,3 +181,27 @@ def test_full_size_properties(ctx, oracle):
     sub_s = s[int(f[sl.start]) * 5: int(f[sl.stop]) * 5]
     e, p, o = oracle.optimize_batch(sub_s, sub_f)
     check_against(ctx, sub_s, sub_f, e, p, o, cand[sl], obj[sl])
+
+
+def test_simple_tile_path_subprocess(golden):
+    """The one-shot tile kernel (unaligned inputs / MISO_B200_SIMPLE_SEARCH=1) stays exact."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+import paper_2207_11428_b200 as m
+ctx = m.Context(0)
+for name in ("opt_random_0b5e55ed", "opt_accept_acce91", "opt_ties_71e5"):
+    g = np.load(f"tests/golden/{name}.npz")
+    cand, obj = ctx.optimize_batch(g["speeds"], g["offsets"])
+    e, p = ctx.decode(cand, g["offsets"])
+    assert np.array_equal(e, g["entry"].astype(np.int32)), name
+    assert np.array_equal(obj.view(np.uint64), g["obj"].view(np.uint64)), name
+print("ok")
+'''
+    root = golden.parent.parent
+    env = dict(os.environ, MISO_B200_SIMPLE_SEARCH="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr
