@@ -85,6 +85,45 @@ int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
 int miso_b200_optimize(miso_b200_ctx* ctx, const double* speeds, int m, int* entry,
                        uint8_t* place, double* obj);
 
+/* ---- predictor (kernel (a)) ------------------------------------------------------------ */
+
+/* The shared default small-slice model: fit_small_slice_model(make_training_corpus(3000,
+ * 0x5eed)) (sim.hpp:894-898, profiles.hpp:340-361, 469-475); weights over (f7, f4, f3, 1).
+ * Computed once on the host. */
+int miso_b200_default_model(double w2[4], double w1[4]);
+
+/* Batched predict_mig_speeds + extrapolate_small_slices (profiles.hpp:214-253, 370-384),
+ * DEVICE pointers. Column j is column j % cols_per_group of MPS group j / cols_per_group,
+ * whose call nonce is first_nonce + j / cols_per_group (real jobs occupy columns
+ * 0..cols_per_group-1, pad_to_seven profiles.hpp:106-113). truth3: (f7, f4, f3) per column;
+ * out5: the estimated speed table per column, kind order 1g..7g. mode 0 = oracle, 1 = noisy
+ * (PredictorSpec::Mode, profiles.hpp:173-178); target_mae in [0, 0.5] else -2. w2/w1 NULL =
+ * the default model. */
+int miso_b200_predict_batch(miso_b200_ctx* ctx, const double* truth3, uint64_t ncols,
+                            int cols_per_group, uint64_t first_nonce, uint64_t rng_seed, int mode,
+                            double target_mae, const double* w2, const double* w1, double* out5,
+                            void* stream);
+
+/* Fused per-GPU decision for n rosters, DEVICE pointers: for each instance i (jobs
+ * offsets[i]..offsets[i+1]-1 in columns 0..m-1, call nonce nonce[i]) predict every job's
+ * speeds, zero them by memory demand (mem_gb) and QoS floor (qos_kind: slice kind 0..4, -1 =
+ * none) as effective_speed does (profiles.hpp:60-65), then optimize_partition -- the
+ * finish_profiling -> reopt_and_apply step of the simulator (sim.hpp:691-733). Writes
+ * cand/obj as miso_b200_optimize_batch, and the zeroed speed tables to est5 (sum(m) x 5) when
+ * est5 != NULL. */
+int miso_b200_decide_batch(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
+                           const int8_t* qos_kind, const uint32_t* offsets, const uint64_t* nonce,
+                           uint64_t n, uint64_t rng_seed, int mode, double target_mae,
+                           const double* w2, const double* w1, uint8_t* cand, double* obj,
+                           double* est5, void* stream);
+
+/* One roster, HOST pointers (config 1: the reference CPU example's chain, latency path).
+ * Returns 1 (entry, place[m], *obj written), 0 (no valid partition) or a negative status.
+ * est5 (optional, m x 5) receives the zeroed estimated speed tables. Default model. */
+int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
+                     const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
+                     double target_mae, int* entry, uint8_t* place, double* obj, double* est5);
+
 /* Pinned host memory for the *_host paths. */
 int miso_b200_host_alloc(size_t bytes, void** out);
 void miso_b200_host_free(void* p);

@@ -15,6 +15,7 @@ from ._native import (  # noqa: F401
     AssignmentVector,
     Context,
     MisoError,
+    default_model,
     lib,
     lib_path,
 )

@@ -51,6 +51,13 @@ def _load():
     L.miso_b200_optimize_batch.argtypes = [vp, vp, vp, u64, vp, vp, vp]
     L.miso_b200_optimize_batch_host.argtypes = [vp, vp, vp, u64, vp, vp]
     L.miso_b200_optimize.argtypes = [vp, vp, i32, C.POINTER(i32), vp, vp]
+    L.miso_b200_default_model.argtypes = [vp, vp]
+    L.miso_b200_predict_batch.argtypes = [vp, vp, u64, i32, u64, u64, i32, C.c_double, vp, vp,
+                                          vp, vp]
+    L.miso_b200_decide_batch.argtypes = [vp, vp, vp, vp, vp, vp, u64, u64, i32, C.c_double, vp,
+                                         vp, vp, vp, vp, vp]
+    L.miso_b200_decide.argtypes = [vp, vp, vp, vp, i32, u64, u64, i32, C.c_double,
+                                   C.POINTER(i32), vp, C.POINTER(C.c_double), vp]
     L.miso_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.miso_b200_host_free.argtypes = [vp]
     L.miso_b200_host_free.restype = None
@@ -200,6 +207,98 @@ class Context:
         counts = tuple(int(x) for x in self.catalog()[e.value])
         asg = [Assignment(jobs[i][0], int(place[i]), float(sp[i, place[i]])) for i in range(m)]
         return AssignmentVector(counts, e.value, asg, objv.value)
+
+
+def _dev(x, dtype, device):
+    """torch tensor on `device` (copies numpy/host tensors)."""
+    import torch
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(x)).to(device=device, dtype=dtype).contiguous()
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def default_model():
+    """fit_small_slice_model(make_training_corpus(3000, 0x5eed)) weights (w2, w1)."""
+    w2 = np.zeros(4)
+    w1 = np.zeros(4)
+    _check(lib.miso_b200_default_model(w2.ctypes.data, w1.ctypes.data))
+    return w2, w1
+
+
+def _predict_batch(self, truth3, cols_per_group, first_nonce, rng_seed, mode, target_mae,
+                   w2=None, w1=None, out=None, stream=None):
+    """Batched predict_mig_speeds + extrapolate_small_slices; returns a (ncols, 5) tensor
+    (kind order 1g..7g) on the context's device."""
+    import torch
+    dev = torch.device("cuda", self.device)
+    t = _dev(truth3, torch.float64, dev).reshape(-1)
+    ncols = t.numel() // 3
+    if out is None:
+        out = torch.empty(ncols * 5, dtype=torch.float64, device=dev)
+    w2a = None if w2 is None else np.ascontiguousarray(w2, np.float64)
+    w1a = None if w1 is None else np.ascontiguousarray(w1, np.float64)
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    _check(lib.miso_b200_predict_batch(self._h, t.data_ptr(), ncols, cols_per_group, first_nonce,
+                                       rng_seed, mode, target_mae,
+                                       None if w2a is None else w2a.ctypes.data,
+                                       None if w1a is None else w1a.ctypes.data,
+                                       out.data_ptr(), s))
+    return out.reshape(ncols, 5)
+
+
+def _decide_batch(self, truth3, mem_gb, qos_kind, offsets, nonce, rng_seed, mode, target_mae,
+                  want_est=False, stream=None):
+    """Fused predict -> effective_speed -> optimize for n rosters (device). Returns
+    (cand, obj, est5 or None) as torch tensors."""
+    import torch
+    dev = torch.device("cuda", self.device)
+    t = _dev(truth3, torch.float64, dev).reshape(-1)
+    mem = _dev(mem_gb, torch.uint8, dev)
+    qos = _dev(qos_kind, torch.int8, dev)
+    off = _dev(np.asarray(offsets).astype(np.int64), torch.int64, dev).to(torch.int32)
+    non = _dev(np.asarray(nonce, np.uint64).view(np.int64), torch.int64, dev)
+    n = off.numel() - 1
+    cand = torch.empty(n, dtype=torch.uint8, device=dev)
+    obj = torch.empty(n, dtype=torch.float64, device=dev)
+    est = torch.empty(t.numel() // 3 * 5, dtype=torch.float64, device=dev) if want_est else None
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    _check(lib.miso_b200_decide_batch(self._h, t.data_ptr(), mem.data_ptr(), qos.data_ptr(),
+                                      off.data_ptr(), non.data_ptr(), n, rng_seed, mode,
+                                      target_mae, None, None, cand.data_ptr(), obj.data_ptr(),
+                                      _ptr(est), s))
+    return cand, obj, est
+
+
+def _decide(self, jobs, nonce, rng_seed, mode=1, target_mae=0.017):
+    """Config-1 chain for one roster (host pointers): jobs = [(job_id, (f7,f4,f3), mem_gb,
+    qos_kind or None)]. Returns (AssignmentVector or None, est5 (m,5))."""
+    m = len(jobs)
+    if m < 1 or m > 7:
+        raise ValueError(f"optimize_partition needs 1..7 jobs, got {m}")
+    t = np.ascontiguousarray([list(j[1]) for j in jobs], np.float64)
+    mem = np.ascontiguousarray([j[2] for j in jobs], np.uint8)
+    qos = np.ascontiguousarray([-1 if j[3] is None else j[3] for j in jobs], np.int8)
+    e = C.c_int()
+    place = np.zeros(7, np.uint8)
+    objv = C.c_double()
+    est = np.zeros((m, 5))
+    r = _check(lib.miso_b200_decide(self._h, t.ctypes.data, mem.ctypes.data, qos.ctypes.data, m,
+                                    nonce, rng_seed, mode, target_mae, C.byref(e),
+                                    place.ctypes.data, C.byref(objv), est.ctypes.data))
+    if r == 0:
+        return None, est
+    counts = tuple(int(x) for x in self.catalog()[e.value])
+    asg = [Assignment(jobs[i][0], int(place[i]), float(est[i, place[i]])) for i in range(m)]
+    return AssignmentVector(counts, e.value, asg, objv.value), est
+
+
+Context.predict_batch = _predict_batch
+Context.decide_batch = _decide_batch
+Context.decide = _decide
 
 
 def host_alloc(nbytes: int):

@@ -28,6 +28,8 @@ struct miso_b200_ctx {
   uint8_t* d_cand = nullptr;
   double* d_obj = nullptr;
   size_t cap_inst = 0;
+  void* h_stage = nullptr;  // single-decision staging (miso_b200_decide)
+  void* d_stage = nullptr;
 };
 
 namespace {
@@ -80,6 +82,8 @@ void apply_catalog(miso_b200_ctx* ctx) {
 int ensure_host_scratch(miso_b200_ctx* ctx, size_t rows, size_t inst) {
   if (!ctx->streams[0]) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  }
+  if (!ctx->streams[1]) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[1], cudaStreamNonBlocking));
   }
   if (rows > ctx->cap_rows) {
@@ -150,6 +154,8 @@ void miso_b200_destroy(miso_b200_ctx* ctx) {
   cudaFree(ctx->d_offsets);
   cudaFree(ctx->d_cand);
   cudaFree(ctx->d_obj);
+  cudaFree(ctx->d_stage);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   for (auto& s : ctx->streams)
     if (s) cudaStreamDestroy(s);
   delete ctx;
@@ -254,6 +260,105 @@ int miso_b200_optimize(miso_b200_ctx* ctx, const double* speeds, int m, int* ent
   if (entry) *entry = e;
   if (place) std::memcpy(place, p, size_t(m));
   if (obj) *obj = o;
+  return 1;
+}
+
+int miso_b200_default_model(double* w2, double* w1) {
+  if (!w2 || !w1) return fail(MISO_B200_E_INVALID, "null weights");
+  default_model(w2, w1);
+  return MISO_B200_OK;
+}
+
+static int check_predictor(int mode, double target_mae) {
+  if (mode != 0 && mode != 1) return fail(MISO_B200_E_INVALID, "mode must be 0 (oracle) or 1 (noisy)");
+  if (!(target_mae >= 0.0 && target_mae <= 0.5))  // validate_predictor_spec, profiles.hpp:180-183
+    return fail(MISO_B200_E_INVALID, "target_mae must be in [0, 0.5]");
+  return MISO_B200_OK;
+}
+
+int miso_b200_predict_batch(miso_b200_ctx* ctx, const double* truth3, uint64_t ncols,
+                            int cols_per_group, uint64_t first_nonce, uint64_t rng_seed, int mode,
+                            double target_mae, const double* w2, const double* w1, double* out5,
+                            void* stream) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (int rc = check_predictor(mode, target_mae)) return rc;
+  if (cols_per_group < 1 || cols_per_group > 7)
+    return fail(MISO_B200_E_INVALID, "cols_per_group must be 1..7 (pad_to_seven)");
+  if (ncols == 0) return MISO_B200_OK;
+  if (!truth3 || !out5) return fail(MISO_B200_E_INVALID, "null buffer");
+  double dw2[4], dw1[4];
+  if (!w2 || !w1) default_model(dw2, dw1);
+  DeviceGuard g(ctx->device);
+  CUDA_TRY(launch_predict(truth3, ncols, cols_per_group, first_nonce, rng_seed, mode, target_mae,
+                          w2 ? w2 : dw2, w1 ? w1 : dw1, out5, static_cast<cudaStream_t>(stream)));
+  return MISO_B200_OK;
+}
+
+int miso_b200_decide_batch(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
+                           const int8_t* qos_kind, const uint32_t* offsets, const uint64_t* nonce,
+                           uint64_t n, uint64_t rng_seed, int mode, double target_mae,
+                           const double* w2, const double* w1, uint8_t* cand, double* obj,
+                           double* est5, void* stream) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (int rc = check_predictor(mode, target_mae)) return rc;
+  if (n == 0) return MISO_B200_OK;
+  if (!truth3 || !mem_gb || !qos_kind || !offsets || !nonce || !cand || !obj)
+    return fail(MISO_B200_E_INVALID, "null buffer");
+  double dw2[4], dw1[4];
+  if (!w2 || !w1) default_model(dw2, dw1);
+  DeviceGuard g(ctx->device);
+  CUDA_TRY(launch_decide(truth3, mem_gb, qos_kind, offsets, nonce, n, rng_seed, mode, target_mae,
+                         w2 ? w2 : dw2, w1 ? w1 : dw1, ctx->en0, ctx->en1, cand, obj, est5,
+                         static_cast<cudaStream_t>(stream)));
+  return MISO_B200_OK;
+}
+
+int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
+                     const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
+                     double target_mae, int* entry, uint8_t* place, double* obj, double* est5) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (m < 1 || m > 7)
+    return fail(MISO_B200_E_INVALID, "optimize_partition needs 1..7 jobs, got " + std::to_string(m));
+  if (int rc = check_predictor(mode, target_mae)) return rc;
+  DeviceGuard g(ctx->device);
+  // One pinned staging block: [truth3 m*3 | est5 m*5 | obj | nonce | offsets 2 | mem m | qos m | cand]
+  struct Stage {
+    double truth[21], est[35], obj;
+    uint64_t nonce;
+    uint32_t off[2];
+    uint8_t mem[7];
+    int8_t qos[7];
+    uint8_t cand;
+  };
+  if (!ctx->h_stage) {
+    CUDA_TRY(cudaMallocHost(&ctx->h_stage, sizeof(Stage)));
+    CUDA_TRY(cudaMalloc(&ctx->d_stage, sizeof(Stage)));
+  }
+  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  Stage* h = static_cast<Stage*>(ctx->h_stage);
+  Stage* d = static_cast<Stage*>(ctx->d_stage);
+  std::memcpy(h->truth, truth3, sizeof(double) * 3 * m);
+  std::memcpy(h->mem, mem_gb, size_t(m));
+  std::memcpy(h->qos, qos_kind, size_t(m));
+  h->nonce = nonce;
+  h->off[0] = 0;
+  h->off[1] = static_cast<uint32_t>(m);
+  double dw2[4], dw1[4];
+  default_model(dw2, dw1);
+  cudaStream_t s = ctx->streams[0];
+  CUDA_TRY(cudaMemcpyAsync(d, h, sizeof(Stage), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(launch_decide(d->truth, d->mem, d->qos, d->off, &d->nonce, 1, rng_seed, mode,
+                         target_mae, dw2, dw1, ctx->en0, ctx->en1, &d->cand, &d->obj, d->est, s));
+  CUDA_TRY(cudaMemcpyAsync(h, d, sizeof(Stage), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (est5) std::memcpy(est5, h->est, sizeof(double) * 5 * m);
+  if (h->cand == MISO_B200_CAND_INFEASIBLE) return 0;
+  int e = -1, mm = 0;
+  uint8_t p[7];
+  miso_b200_candidate(ctx, h->cand, &e, &mm, p);
+  if (entry) *entry = e;
+  if (place) std::memcpy(place, p, size_t(m));
+  if (obj) *obj = h->obj;
   return 1;
 }
 

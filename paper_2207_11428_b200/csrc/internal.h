@@ -10,4 +10,17 @@ cudaError_t launch_optimize(const double* speeds, const uint32_t* offsets, uint6
                             uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
                             cudaStream_t stream);
 
+cudaError_t launch_predict(const double* truth3, uint64_t ncols, int cpg, uint64_t first_nonce,
+                           uint64_t rng_seed, int noisy, double target_mae, const double* w2,
+                           const double* w1, double* out5, cudaStream_t stream);
+
+cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int8_t* qos_kind,
+                          const uint32_t* offsets, const uint64_t* nonce, uint64_t n,
+                          uint64_t rng_seed, int noisy, double target_mae, const double* w2,
+                          const double* w1, uint64_t en0, uint64_t en1, uint8_t* cand,
+                          double* obj, double* est_out, cudaStream_t stream);
+
+// Host: fit_small_slice_model(make_training_corpus(3000, 0x5eed)) (sim.hpp:894-898).
+void default_model(double w2[4], double w1[4]);
+
 }  // namespace miso_b200

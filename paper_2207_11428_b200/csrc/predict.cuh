@@ -1,0 +1,147 @@
+// predict.cuh -- device restatement of the MISO MPS->MIG predictor chain (kernel (a)).
+//
+//   mix_seed / splitmix64            common.hpp:70-83
+//   DetRng(seed) first three draws   common.hpp:85-108 (std::mt19937_64, see below)
+//   perturb_speed                    profiles.hpp:193-205
+//   predict_mig_speeds (one column)  profiles.hpp:214-253
+//   extrapolate_small_slices         profiles.hpp:259-273, 370-384
+//   effective_speed                  profiles.hpp:60-65
+//
+// std::mt19937_64 draws 0..2 only depend on the seeded words x[0..3] and x[156..158]
+// (the first twist rewrites mt[i] from mt[i], mt[i+1], mt[i+156]), so a perturbed entry costs
+// 158 seeding steps instead of a 312-word seed plus a full 312-word twist.
+//
+// FP64 arithmetic is IEEE round-to-nearest without contraction (TU compiled --fmad=false), in
+// the reference's expression order. log and cos are bit-exact restatements of the glibc 2.39
+// FMA variants the reference runs (glibc_math.cuh), so predicted speeds are bit-identical.
+#pragma once
+#include <cstdint>
+
+#include "glibc_math.cuh"
+
+namespace miso_b200 {
+
+constexpr double kSpeedFloor = 1e-9;  // profiles.hpp:33
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix_seed(uint64_t seed, uint64_t tag) {
+  return splitmix64(splitmix64(seed) ^ splitmix64(tag));
+}
+
+__device__ __forceinline__ uint64_t mt64_temper(uint64_t y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+__device__ __forceinline__ uint64_t mt64_seed_step(uint64_t x, uint64_t i) {
+  return 6364136223846793005ull * (x ^ (x >> 62)) + i;  // [rand.eng.mers] seeding
+}
+
+__device__ __forceinline__ uint64_t mt64_twist_draw(uint64_t xk, uint64_t xk1, uint64_t xk156) {
+  constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+  const uint64_t y = (xk & UM) | (xk1 & LM);
+  return mt64_temper(xk156 ^ (y >> 1) ^ ((y & 1ull) ? 0xB5026F5AA96619E9ull : 0ull));
+}
+
+// First three outputs of std::mt19937_64(seed).
+__device__ __forceinline__ void mt64_first3(uint64_t seed, uint64_t out[3]) {
+  const uint64_t x0 = seed;
+  const uint64_t x1 = mt64_seed_step(x0, 1);
+  const uint64_t x2 = mt64_seed_step(x1, 2);
+  const uint64_t x3 = mt64_seed_step(x2, 3);
+  uint64_t x = x3;
+#pragma unroll 8
+  for (uint32_t i = 4; i <= 155; ++i) x = mt64_seed_step(x, i);
+  const uint64_t x156 = mt64_seed_step(x, 156);
+  const uint64_t x157 = mt64_seed_step(x156, 157);
+  const uint64_t x158 = mt64_seed_step(x157, 158);
+  out[0] = mt64_twist_draw(x0, x1, x156);
+  out[1] = mt64_twist_draw(x1, x2, x157);
+  out[2] = mt64_twist_draw(x2, x3, x158);
+}
+
+__device__ __forceinline__ double uniform01_of(uint64_t raw) {  // common.hpp:90
+  return static_cast<double>(raw >> 11) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {  // std::clamp
+  return v < lo ? lo : (hi < v ? hi : v);
+}
+
+// profiles.hpp:193-205
+__device__ __forceinline__ double perturb_speed(double truth, double target_mae, uint64_t entry_seed) {
+  if (target_mae <= 0.0) return truth;
+  uint64_t r[3];
+  mt64_first3(entry_seed, r);
+  double u1 = uniform01_of(r[0]);
+  const double u2 = uniform01_of(r[1]);
+  if (u1 <= 0.0) u1 = 0x1.0p-53;
+  const double n01 = sqrt(-2.0 * glibc::log_fma(u1)) *
+                     glibc::cos_fma(6.283185307179586476925287 * u2);  // common.hpp:103-108
+  const double sigma = target_mae * sqrt(3.14159265358979323846 / 2.0);
+  const double mag = fabs(n01) * sigma;
+  const bool up_ok = truth + mag <= 1.0;
+  const bool dn_ok = truth - mag >= kSpeedFloor;
+  const bool coin = uniform01_of(r[2]) < 0.5;
+  if (up_ok && dn_ok) return coin ? truth + mag : truth - mag;
+  if (up_ok) return truth + mag;
+  if (dn_ok) return truth - mag;
+  return (1.0 - truth >= truth - kSpeedFloor) ? 1.0 : kSpeedFloor;
+}
+
+struct ModelW {
+  double w2[4], w1[4];  // LinearMap weights over (f7, f4, f3, 1)
+};
+
+// One real (non-dummy) column: truth (f7, f4, f3) -> est speeds in kind order 1g..7g.
+// predict_mig_speeds column c of call `nonce` (profiles.hpp:234-248) then
+// extrapolate_small_slices (profiles.hpp:376-381).
+__device__ __forceinline__ void predict_column(double f7, double f4, double f3, int col,
+                                               uint64_t rng_seed, uint64_t nonce, bool noisy,
+                                               double target_mae, const ModelW& w,
+                                               double out5[5]) {
+  double v0 = f7, v1 = f4, v2 = f3;
+  if (noisy) {
+    const uint64_t base = mix_seed(rng_seed, nonce);
+    v1 = perturb_speed(f4, target_mae, mix_seed(base, static_cast<uint64_t>(col) * 8 + 1));
+    v2 = perturb_speed(f3, target_mae, mix_seed(base, static_cast<uint64_t>(col) * 8 + 2));
+  }
+  double mx = v0;  // std::max({a, b, c})
+  if (mx < v1) mx = v1;
+  if (mx < v2) mx = v2;
+  v0 = clampd(v0 / mx, kSpeedFloor, 1.0);
+  v1 = clampd(v1 / mx, kSpeedFloor, 1.0);
+  v2 = clampd(v2 / mx, kSpeedFloor, 1.0);
+  const double p2 = w.w2[0] * v0 + w.w2[1] * v1 + w.w2[2] * v2 + w.w2[3];
+  const double p1 = w.w1[0] * v0 + w.w1[1] * v1 + w.w1[2] * v2 + w.w1[3];
+  const double f2 = clampd(p2, kSpeedFloor, v2);
+  const double f1 = clampd(p1, kSpeedFloor, f2);
+  out5[0] = f1;
+  out5[1] = f2;
+  out5[2] = v2;
+  out5[3] = v1;
+  out5[4] = v0;
+}
+
+// profiles.hpp:60-65 with kind tables (topology.hpp:39-45). qos_kind < 0: no QoS floor.
+__host__ __device__ __forceinline__ int kind_mem_gb(int kind) {
+  return kind < 2 ? (kind == 0 ? 5 : 10) : (kind < 4 ? 20 : 40);
+}
+__host__ __device__ __forceinline__ int kind_gpc(int kind) { return kind < 4 ? kind + 1 : 7; }
+
+__device__ __forceinline__ double effective_speed(double s, int kind, int mem_gb, int qos_kind) {
+  if (kind_mem_gb(kind) < mem_gb) return 0.0;
+  if (qos_kind >= 0 && kind_gpc(kind) < kind_gpc(qos_kind)) return 0.0;
+  return s;
+}
+
+}  // namespace miso_b200
