@@ -124,6 +124,88 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
                      const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
                      double target_mae, int* entry, uint8_t* place, double* obj, double* est5);
 
+/* ---- cluster simulator (kernel (c)) ------------------------------------------------------ */
+
+/* Policies (sim.hpp:42): nopart, oracle, miso. (optsta is not on the device yet.) */
+#define MISO_B200_POLICY_NOPART 0
+#define MISO_B200_POLICY_ORACLE 2
+#define MISO_B200_POLICY_MISO 3
+
+/* Per-seed status (SimInvariantError and friends become per-seed codes; 0 = ok). */
+#define MISO_B200_SIM_INVARIANT 1         /* work conservation / accounting / plan mismatch */
+#define MISO_B200_SIM_NO_PARTITION 2      /* "no feasible partition for admitted roster" */
+#define MISO_B200_SIM_INFEASIBLE_SLICE 3  /* "placed on infeasible slice" */
+#define MISO_B200_SIM_EVENT_BUDGET 4      /* max_events exceeded (counts live events) */
+
+/* SimOptions (sim.hpp:81-96) + OverheadSpec (:62-67) + PredictorSpec (profiles.hpp:173-178).
+ * Durations in seconds are converted with us_from_s = llround(s * 1e6) (sim.hpp:136). */
+typedef struct {
+  int policy;                      /* MISO_B200_POLICY_* */
+  int cluster_size;                /* GPUs, >= 1 */
+  double mig_reconfig_s;           /* default 4 */
+  double checkpoint_restart_s;     /* default 30 */
+  double mps_window_s;             /* default 10 */
+  double interference;             /* default 0.8, in (0, 1] */
+  int predictor_noisy;             /* 0 oracle predictor, 1 noisy */
+  double target_mae;               /* default 0.017, [0, 0.5] */
+  int check_invariants;            /* default 1 */
+  double reprofile_drift_threshold;/* default 0 (off) */
+  uint64_t max_events;             /* default 100000000 */
+} miso_b200_sim_options;
+
+/* MetricsReport (sim.hpp:106-122) scalars, per seed. */
+typedef struct {
+  int status, completed, job_count, completed_count, repartitions, migrations, mps_sessions, pad;
+  double avg_jct_s, makespan_s, stp_time_avg, jct_sum_s;
+  double queue_frac, mps_frac, checkpoint_frac, run_frac, idle_frac;
+  int64_t events, log_records, stp_points;
+} miso_b200_sim_metrics;
+
+/* Compact event-log record; render with the reference's text format (sim.hpp:365-367). */
+typedef struct {
+  int64_t t;       /* now_, integer microseconds */
+  uint8_t kind;    /* MISO_B200_LOG_* */
+  uint8_t x;       /* slice kind / roster size */
+  uint16_t gpu;    /* 0xFFFF = none */
+  int32_t job;     /* job index in the trace, -1 = none */
+  uint32_t a, b;   /* payload (counts, levels, packed partition, 64-bit durations as a|b<<32) */
+  double v;        /* rate for "start" */
+} miso_b200_log_record;
+
+#define MISO_B200_LOG_ARRIVAL 0
+#define MISO_B200_LOG_ADMIT 1
+#define MISO_B200_LOG_START 2
+#define MISO_B200_LOG_CKPT_START 3
+#define MISO_B200_LOG_MPS_START 4
+#define MISO_B200_LOG_MPS_WINDOW 5
+#define MISO_B200_LOG_MPS_END 6
+#define MISO_B200_LOG_RECONFIG_START 7
+#define MISO_B200_LOG_PARTITION 8  /* x = roster size, a = packed counts (4 bits per kind) */
+#define MISO_B200_LOG_ASSIGN 9     /* follows PARTITION: job, x = slice kind */
+#define MISO_B200_LOG_COMPLETE 10
+#define MISO_B200_LOG_SHRINK 11
+
+/* generate_trace (workload.hpp:97-114) on the host: dist 0 lognormal(sigma), 1 fixed(fixed_s),
+ * 2 uniform(lo_s, hi_s). Arrays of job_count; speeds5 kind order 1g..7g. */
+int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
+                             double max_duration_s, int dist, double sigma, double fixed_s,
+                             double lo_s, double hi_s, double* arrival_s, double* duration_s,
+                             double* speeds5, int* mem_gb);
+
+/* run_simulation (sim.hpp:976-979) for n_seeds independent traces at once, one warp per seed,
+ * DEVICE pointers. Trace s owns jobs job_offsets[s]..job_offsets[s+1]-1 (arrival_s as in
+ * TraceJob, converted with us_from_s on the device; must be non-decreasing with the first at 0,
+ * sim.hpp:251-254; base duration s; truth speeds; memory GB; QoS kind or -1). rng_seed[s] seeds the noisy predictor (experiment.hpp:305 sets it to the trace
+ * seed). Outputs: metrics[s]; optional job_jct_us (completion - arrival, -1 if unfinished),
+ * event log (log_cap records per seed) and STP series (stp_cap (t, stp) pairs per seed). */
+int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                             const int32_t* job_offsets, const double* arrival_s,
+                             const double* base_s, const double* speeds5, const uint8_t* mem_gb,
+                             const int8_t* qos_kind, const uint64_t* rng_seed,
+                             miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
+                             miso_b200_log_record* log, int64_t log_cap, double* stp_series,
+                             int64_t stp_cap, void* stream);
+
 /* Pinned host memory for the *_host paths. */
 int miso_b200_host_alloc(size_t bytes, void** out);
 void miso_b200_host_free(void* p);

@@ -285,6 +285,73 @@ int64_t ref_simulate(uint64_t seed, int job_count, double lambda_s, double max_d
   return static_cast<int64_t>(s.size());
 }
 
+// run_simulation on an explicit trace (arrays; job ids "j<i>", qos kind -1 = none).
+int64_t ref_simulate_trace(int job_count, const double* arrival_s, const double* duration_s,
+                           const double* speeds5, const int* mem_gb, const int* qos_kind,
+                           uint64_t seed, int cluster_size, int policy, double mig_reconfig_s,
+                           double checkpoint_restart_s, double mps_window_s, double interference,
+                           int noisy, double target_mae, uint64_t rng_seed, RefSimOut* out,
+                           char* log_buf, int64_t log_cap, double* stp_series, int64_t stp_cap) {
+  miso::JobTrace trace;
+  trace.spec.job_count = job_count;
+  trace.spec.seed = seed;
+  for (int i = 0; i < job_count; ++i) {
+    miso::TraceJob j;
+    j.arrival_s = arrival_s[i];
+    j.profile.job_id = "j" + std::to_string(i);
+    j.profile.base_duration_s = duration_s[i];
+    for (int k = 0; k < 5; ++k) j.profile.speed_table.v[k] = speeds5[5 * i + k];
+    j.profile.mem_demand_gb = mem_gb[i];
+    if (qos_kind[i] >= 0) j.profile.qos_min_slice = static_cast<miso::Slice>(qos_kind[i]);
+    j.profile.mps_rates = {1.0, 0.7, 0.4};
+    trace.jobs.push_back(j);
+  }
+  miso::SimOptions opt;
+  opt.policy = static_cast<miso::Policy>(policy);
+  opt.cluster_size = cluster_size;
+  opt.overheads.mig_reconfig_s = mig_reconfig_s;
+  opt.overheads.checkpoint_restart_s = checkpoint_restart_s;
+  opt.overheads.mps_window_s = mps_window_s;
+  opt.overheads.interference = interference;
+  opt.predictor.mode = noisy ? miso::PredictorSpec::Mode::noisy : miso::PredictorSpec::Mode::oracle;
+  opt.predictor.target_mae = target_mae;
+  opt.predictor.rng_seed = rng_seed;
+  std::ostringstream log;
+  if (log_buf) opt.event_log = &log;
+  miso::MetricsReport r;
+  try {
+    r = miso::run_simulation(trace, opt);
+  } catch (const std::exception& e) {
+    out->completed = -1;
+    return -1;
+  }
+  out->completed = r.completed;
+  out->job_count = r.job_count;
+  out->completed_count = r.completed_count;
+  out->repartitions = r.repartitions;
+  out->migrations = r.migrations;
+  out->mps_sessions = r.mps_sessions;
+  out->avg_jct_s = r.avg_jct_s;
+  out->makespan_s = r.makespan_s;
+  out->stp_time_avg = r.stp_time_avg;
+  out->queue_frac = r.queue_frac;
+  out->mps_frac = r.mps_frac;
+  out->checkpoint_frac = r.checkpoint_frac;
+  out->run_frac = r.run_frac;
+  out->idle_frac = r.idle_frac;
+  out->stp_points = static_cast<int64_t>(r.stp_series.size());
+  if (stp_series)
+    for (size_t i = 0; i < r.stp_series.size() && static_cast<int64_t>(i) < stp_cap; ++i) {
+      stp_series[2 * i] = r.stp_series[i].first;
+      stp_series[2 * i + 1] = r.stp_series[i].second;
+    }
+  if (!log_buf) return 0;
+  std::string s = log.str();
+  size_t n = std::min<size_t>(s.size(), static_cast<size_t>(log_cap));
+  std::memcpy(log_buf, s.data(), n);
+  return static_cast<int64_t>(s.size());
+}
+
 // Raw std::mt19937_64 draws of DetRng(seed) (common.hpp:85-119), for fixture generators.
 void ref_rng_raw(uint64_t seed, size_t n, uint64_t* out) {
   miso::DetRng rng(seed);

@@ -20,6 +20,7 @@ from ._native import (  # noqa: F401
     lib_path,
 )
 from .catalog import DEFAULT_CATALOG, partition_name  # noqa: F401
+from .sim import SimOptions, Trace, generate_trace, render_log, simulate_batch  # noqa: F401
 
 __all__ = [
     "Context", "Assignment", "AssignmentVector", "MisoError", "DEFAULT_CATALOG",

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -11,6 +12,7 @@
 #include "../../include/miso_b200.h"
 #include "candidates_gen.cuh"
 #include "internal.h"
+#include "sim_types.h"
 
 using namespace miso_b200;
 
@@ -30,6 +32,11 @@ struct miso_b200_ctx {
   size_t cap_inst = 0;
   void* h_stage = nullptr;  // single-decision staging (miso_b200_decide)
   void* d_stage = nullptr;
+  // simulator
+  int8_t* d_spare_lut = nullptr;  // max_spare_slice_for LUT of the active catalog
+  bool lut_valid = false;
+  unsigned char* d_sim_ws = nullptr;
+  size_t sim_ws_bytes = 0;
 };
 
 namespace {
@@ -155,6 +162,8 @@ void miso_b200_destroy(miso_b200_ctx* ctx) {
   cudaFree(ctx->d_cand);
   cudaFree(ctx->d_obj);
   cudaFree(ctx->d_stage);
+  cudaFree(ctx->d_spare_lut);
+  cudaFree(ctx->d_sim_ws);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   for (auto& s : ctx->streams)
     if (s) cudaStreamDestroy(s);
@@ -177,6 +186,7 @@ int miso_b200_set_catalog(miso_b200_ctx* ctx, const uint8_t* counts, int n) {
   std::memcpy(ctx->counts, counts, size_t(n) * 5);
   std::memcpy(ctx->default_to_active, map, sizeof(map));
   apply_catalog(ctx);
+  ctx->lut_valid = false;
   return MISO_B200_OK;
 }
 
@@ -360,6 +370,116 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
   if (place) std::memcpy(place, p, size_t(m));
   if (obj) *obj = h->obj;
   return 1;
+}
+
+int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
+                             double max_duration_s, int dist, double sigma, double fixed_s,
+                             double lo_s, double hi_s, double* arrival_s, double* duration_s,
+                             double* speeds5, int* mem_gb) {
+  // validate_trace_spec (workload.hpp:37-46)
+  if (job_count < 1) return fail(MISO_B200_E_INVALID, "job_count must be >= 1");
+  if (!(lambda_s > 0)) return fail(MISO_B200_E_INVALID, "lambda_s must be positive");
+  if (!(max_duration_s > 0)) return fail(MISO_B200_E_INVALID, "max_duration_s must be positive");
+  if (dist < 0 || dist > 2) return fail(MISO_B200_E_INVALID, "unknown duration distribution");
+  if (dist == 0 && !(sigma > 0)) return fail(MISO_B200_E_INVALID, "lognormal sigma must be positive");
+  if (dist == 2 && !(lo_s > 0 && lo_s <= hi_s))
+    return fail(MISO_B200_E_INVALID, "uniform bounds must satisfy 0 < lo_s <= hi_s");
+  if (!arrival_s || !duration_s || !speeds5 || !mem_gb) return fail(MISO_B200_E_INVALID, "null buffer");
+  host_generate_trace(seed, job_count, lambda_s, max_duration_s, dist, sigma, fixed_s, lo_s, hi_s,
+                      arrival_s, duration_s, speeds5, mem_gb);
+  return MISO_B200_OK;
+}
+
+static int64_t us_from_s_host(double s) { return static_cast<int64_t>(std::llround(s * 1e6)); }
+
+int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                             const int32_t* job_offsets, const double* arrival_s,
+                             const double* base_s, const double* speeds5, const uint8_t* mem_gb,
+                             const int8_t* qos_kind, const uint64_t* rng_seed,
+                             miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
+                             miso_b200_log_record* log, int64_t log_cap, double* stp_series,
+                             int64_t stp_cap, void* stream) {
+  if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
+  if (n_seeds < 0) return fail(MISO_B200_E_INVALID, "n_seeds < 0");
+  if (n_seeds == 0) return MISO_B200_OK;
+  if (opt->policy != MISO_B200_POLICY_NOPART && opt->policy != MISO_B200_POLICY_ORACLE &&
+      opt->policy != MISO_B200_POLICY_MISO)
+    return fail(MISO_B200_E_INVALID, "policy must be nopart, oracle or miso (optsta: host only)");
+  if (opt->cluster_size < 1 || opt->cluster_size > 32767)
+    return fail(MISO_B200_E_INVALID, "cluster_size must be >= 1");
+  // validate_overheads (sim.hpp:69-74), validate_predictor_spec (profiles.hpp:180-183)
+  if (opt->mig_reconfig_s < 0 || opt->checkpoint_restart_s < 0 || opt->mps_window_s < 0)
+    return fail(MISO_B200_E_INVALID, "overhead durations must be >= 0");
+  if (!(opt->interference > 0.0 && opt->interference <= 1.0))
+    return fail(MISO_B200_E_INVALID, "interference must be in (0, 1]");
+  if (int rc = check_predictor(opt->predictor_noisy ? 1 : 0, opt->target_mae)) return rc;
+  if (!job_offsets || !arrival_s || !base_s || !speeds5 || !mem_gb || !qos_kind || !rng_seed ||
+      !metrics)
+    return fail(MISO_B200_E_INVALID, "null buffer");
+  DeviceGuard g(ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // max jobs per seed (offsets are device memory: read them back once)
+  std::vector<int32_t> offs(size_t(n_seeds) + 1);
+  CUDA_TRY(cudaMemcpyAsync(offs.data(), job_offsets, offs.size() * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int max_jobs = 0;
+  for (int i = 0; i < n_seeds; ++i) {
+    const int J = offs[i + 1] - offs[i];
+    if (J < 1) return fail(MISO_B200_E_INVALID, "trace has no jobs");  // sim.hpp:210
+    max_jobs = std::max(max_jobs, J);
+  }
+  if (!ctx->lut_valid) {
+    std::vector<int8_t> lut(16807);
+    host_spare_lut(&ctx->counts[0][0], ctx->n_entries, lut.data());
+    if (!ctx->d_spare_lut) CUDA_TRY(cudaMalloc(&ctx->d_spare_lut, lut.size()));
+    CUDA_TRY(cudaMemcpy(ctx->d_spare_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+    ctx->lut_valid = true;
+  }
+  const size_t stride = sim_workspace_stride(max_jobs, opt->cluster_size);
+  const size_t need = stride * size_t(n_seeds);
+  if (need > ctx->sim_ws_bytes) {
+    cudaFree(ctx->d_sim_ws);
+    ctx->d_sim_ws = nullptr;
+    CUDA_TRY(cudaMalloc(&ctx->d_sim_ws, need));
+    ctx->sim_ws_bytes = need;
+  }
+  SimParams p{};
+  p.policy = opt->policy;
+  p.cluster_size = opt->cluster_size;
+  p.noisy = opt->predictor_noisy ? 1 : 0;
+  p.check_invariants = opt->check_invariants ? 1 : 0;
+  p.window_us = us_from_s_host(opt->mps_window_s);
+  p.reconfig_us = us_from_s_host(opt->mig_reconfig_s);
+  p.ckpt_us = us_from_s_host(opt->checkpoint_restart_s);
+  p.interference = opt->interference;
+  p.target_mae = opt->target_mae;
+  p.drift_threshold = opt->reprofile_drift_threshold;
+  p.max_events = opt->max_events ? opt->max_events : 100000000ull;
+  p.en0 = ctx->en0;
+  p.en1 = ctx->en1;
+  SimBatch b{};
+  b.n_seeds = n_seeds;
+  b.max_jobs = max_jobs;
+  b.job_offsets = job_offsets;
+  b.arrival_s = arrival_s;
+  b.base_s = base_s;
+  b.speeds5 = speeds5;
+  b.mem_gb = mem_gb;
+  b.qos_kind = qos_kind;
+  b.rng_seed = rng_seed;
+  b.spare_lut = ctx->d_spare_lut;
+  b.workspace = ctx->d_sim_ws;
+  b.ws_stride = stride;
+  b.metrics = metrics;
+  b.job_jct_us = job_jct_us;
+  b.log = log;
+  b.log_cap = log ? log_cap : 0;
+  b.stp_series = stp_series;
+  b.stp_cap = stp_series ? stp_cap : 0;
+  double w2[4], w1[4];
+  default_model(w2, w1);
+  CUDA_TRY(launch_simulate(b, p, w2, w1, s));
+  return MISO_B200_OK;
 }
 
 int miso_b200_host_alloc(size_t bytes, void** out) {

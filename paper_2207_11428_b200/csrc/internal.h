@@ -20,6 +20,14 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
                           const double* w1, uint64_t en0, uint64_t en1, uint8_t* cand,
                           double* obj, double* est_out, cudaStream_t stream);
 
+// Host: generate_trace (workload.hpp:97-114); dist_kind 0 lognormal, 1 fixed, 2 uniform.
+void host_generate_trace(uint64_t seed, int job_count, double lambda_s, double max_duration_s,
+                         int dist_kind, double sigma, double fixed_s, double lo_s, double hi_s,
+                         double* arrival_s, double* duration_s, double* speeds5, int* mem_gb);
+
+// Host: max_spare_slice_for (topology.hpp:227-252) tabulated over min-kind count vectors.
+void host_spare_lut(const uint8_t* counts, int n_entries, int8_t* lut);
+
 // Host: fit_small_slice_model(make_training_corpus(3000, 0x5eed)) (sim.hpp:894-898).
 void default_model(double w2[4], double w1[4]);
 

@@ -1,0 +1,977 @@
+// sim_kernel.cu -- kernel (c): batched event-step cluster simulator, one warp per trace seed.
+//
+// Restates SimEngine (sim.hpp:202-972) for the nopart, oracle and miso policies. Every event
+// of one seed is processed by one warp in lockstep: all 32 lanes execute the (sequential)
+// event logic redundantly -- uniform loads are warp broadcasts, uniform stores are idempotent
+// -- and split only for the data-parallel parts:
+//   * next event: warp argmin over the per-job and per-GPU event slots (below);
+//   * placement (place_dynamic, sim.hpp:581-607): warp argmin over GPUs, with
+//     max_spare_slice_for (topology.hpp:227-252) replaced by a LUT over the roster's min-kind
+//     counts, cached per GPU;
+//   * predictor (finish_profiling, sim.hpp:691-714): one lane per roster column (mt19937_64
+//     seeding + glibc-exact log/cos, predict.cuh), results exchanged by shuffles;
+//   * STP refresh (sim.hpp:353-361): progressing jobs kept as a bitmask; the FP64 sum itself
+//     stays sequential in job-index order (bit-exact STP series).
+// The partition search of reopt_and_apply (sim.hpp:716-733) is search.cuh's straight-line
+// search, executed redundantly by all lanes.
+//
+// Event queue: the reference keeps a binary heap with lazy deletion (stale events are popped
+// and skipped, sim.hpp:284-299). Each job has at most one live job-scoped event and each GPU
+// at most one live GPU-scoped event (every push is preceded by an epoch bump), so this engine
+// keeps one slot per job and per GPU holding that live event's (t, prio, seq) key, with `seq`
+// the same global push counter (sim.hpp:280-282); the next event is the minimum live key --
+// the same total order the heap pops. A slot is cleared whenever its epoch is bumped.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/miso_b200.h"
+#include "internal.h"
+#include "predict.cuh"
+#include "search.cuh"
+#include "sim_types.h"
+
+namespace miso_b200 {
+namespace sim {
+
+enum Phase : uint8_t { kQueued = 0, kMps = 1, kCkpt = 2, kRunning = 3, kIdle = 4 };
+enum Mode : uint8_t { kGpuIdle = 0, kGpuMig = 1, kGpuMps = 2, kGpuReconfig = 3 };
+enum EvKind : uint32_t { kEvArrival = 0, kEvMpsEnd = 1, kEvReconfigDone = 2, kEvCkptDone = 3,
+                         kEvCompletion = 4 };
+enum JobFlag : uint8_t { kRunState = 1, kDone = 2, kHasEst = 4 };
+
+constexpr int64_t kNoEvent = INT64_MAX;
+
+struct DJob {
+  double remaining, consumed, rate, base;
+  double truth[5];
+  double est[5];
+  int64_t arrival_us, last_update_us, first_progress_us, completion_us;
+  int64_t acc[5];
+  uint32_t epoch;
+  int16_t gpu;
+  uint8_t phase, slice, mem, min_kind, flags;
+  int8_t qos;
+  uint8_t pad[6];
+};
+
+struct DGpu {
+  double objective, plan_obj;
+  double plan_speed[7];
+  int32_t roster[7];
+  int32_t plan_job[7];
+  uint32_t epoch;
+  uint8_t mode, mps_level, nroster, plan_n, plan_valid;
+  uint8_t part[5], plan_part[5], kind_cnt[5];
+  int8_t spare;
+  uint8_t plan_slice[7];
+  uint8_t pad[3];
+};
+
+static_assert(sizeof(DJob) <= kSimJobBytes, "workspace job stride");
+static_assert(sizeof(DGpu) <= kSimGpuBytes, "workspace gpu stride");
+
+struct Slot {
+  int64_t t;
+  uint64_t pk;  // prio << 62 | seq << 3 | kind
+};
+
+struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
+  DJob* jobs;
+  DGpu* gpus;
+  Slot* slots;          // [J job slots][G gpu slots]
+  int32_t* queue;       // FCFS order (arrival_us, idx), qhead..qtail
+  uint32_t* prog_mask;  // bit j: job j progressing and not done
+  double* scratch;      // rate compaction for refresh_stp
+  LogRec* log;
+  int64_t log_cap, log_n;
+  int J, G;
+  int qhead, qtail;
+  int64_t now;
+  uint64_t seq;
+  uint64_t nonce;
+  double stp_cur, stp_integral;
+  int64_t stp_last;
+  int64_t stp_points;
+  double* stp_series;  // optional (t_s, stp) pairs
+  int64_t stp_cap;
+  bool stp_dirty;
+  int repartitions, mps_sessions, done_count;
+  int64_t first_progress, last_completion;
+  int status;
+  uint64_t processed;
+  // options
+  const SimParams* p;
+  const int8_t* spare_lut;
+  uint64_t rng_seed;
+  ModelW w;
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ double s_from_us(int64_t us) { return static_cast<double>(us) * 1e-6; }
+__device__ __forceinline__ int64_t us_from_s(double s) {  // llround: half away from zero
+  return static_cast<int64_t>(llround(s * 1e6));
+}
+
+__device__ __forceinline__ bool progressing(uint8_t ph) { return ph == kMps || ph == kRunning; }
+
+__device__ __forceinline__ void fail(Ctx& c, int code) {
+  if (c.status == 0) c.status = code;
+}
+
+// ---- event log (optional) -------------------------------------------------------------
+__device__ __forceinline__ void log_rec(Ctx& c, uint8_t kind, int gpu, int job, uint8_t x,
+                                        uint32_t a, uint32_t b, double v) {
+  if (!c.log) return;
+  if (c.log_n < c.log_cap && lane_id() == 0) {
+    LogRec r;
+    r.t = c.now;
+    r.kind = kind;
+    r.x = x;
+    r.gpu = static_cast<uint16_t>(gpu < 0 ? 0xFFFF : gpu);
+    r.job = job;
+    r.a = a;
+    r.b = b;
+    r.v = v;
+    c.log[c.log_n] = r;
+  }
+  __syncwarp();
+  ++c.log_n;
+}
+
+__device__ __forceinline__ uint32_t pack_part(const uint8_t* p) {
+  return p[0] | (p[1] << 4) | (p[2] << 8) | (p[3] << 12) | (p[4] << 16);
+}
+
+// ---- event slots -----------------------------------------------------------------------
+__device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t prio,
+                                           uint32_t kind) {
+  Slot s;
+  s.t = t;
+  s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
+  ++c.seq;
+  c.slots[slot] = s;
+}
+
+__device__ __forceinline__ void clear_slot(Ctx& c, int slot) {
+  c.slots[slot].t = kNoEvent;
+}
+
+// Warp argmin over live slots: returns slot index (or -1), with its key.
+__device__ int next_event(Ctx& c, Slot* out) {
+  const int n = c.J + c.G;
+  int64_t bt = kNoEvent;
+  uint64_t bk = ~0ull;
+  int bi = -1;
+  for (int i = lane_id(); i < n; i += 32) {
+    const Slot s = c.slots[i];
+    if (s.t < bt || (s.t == bt && s.pk < bk)) {
+      bt = s.t;
+      bk = s.pk;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
+    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    if (ot < bt || (ot == bt && ok < bk)) {
+      bt = ot;
+      bk = ok;
+      bi = oi;
+    }
+  }
+  out->t = bt;
+  out->pk = bk;
+  return bt == kNoEvent ? -1 : bi;
+}
+
+// ---- job state ---------------------------------------------------------------------------
+__device__ __forceinline__ void set_prog_bit(Ctx& c, int j, bool on) {
+  uint32_t* w = c.prog_mask + (j >> 5);
+  const uint32_t bit = 1u << (j & 31);
+  const uint32_t cur = *w;
+  const uint32_t nv = on ? (cur | bit) : (cur & ~bit);
+  __syncwarp();
+  *w = nv;
+  __syncwarp();
+}
+
+// sim.hpp:319-329
+__device__ void advance_job(Ctx& c, DJob& j) {
+  const int64_t dt = c.now - j.last_update_us;
+  j.last_update_us = c.now;
+  if (dt <= 0 || (j.flags & kDone)) return;
+  j.acc[j.phase] += dt;
+  if (progressing(j.phase)) {
+    const double w = j.rate * s_from_us(dt);
+    j.remaining -= w;
+    j.consumed += w;
+  }
+}
+
+// sim.hpp:333-343 (+ slot invalidation: every epoch bump retires the job's pending event)
+__device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
+  DJob& j = c.jobs[ji];
+  advance_job(c, j);
+  j.phase = phase;
+  j.rate = progressing(phase) ? rate : 0.0;
+  ++j.epoch;
+  clear_slot(c, ji);
+  if (progressing(phase)) {
+    j.flags |= kRunState;
+    if (j.first_progress_us < 0) j.first_progress_us = c.now;
+    if (c.first_progress < 0) c.first_progress = c.now;
+  }
+  set_prog_bit(c, ji, progressing(phase) && !(j.flags & kDone));
+  c.stp_dirty = true;
+}
+
+// sim.hpp:345-351
+__device__ void schedule_completion(Ctx& c, int ji) {
+  DJob& j = c.jobs[ji];
+  if ((j.flags & kDone) || !(j.rate > 0)) return;
+  const double dt_s = (j.remaining > 0.0 ? j.remaining : 0.0) / j.rate;  // std::max(0.0, r)
+  int64_t dt = us_from_s(dt_s);
+  if (dt < 0) dt = 0;
+  push_event(c, ji, c.now + dt, 0, kEvCompletion);
+}
+
+// sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). The
+// progressing set is a bitmask; lanes compact the rates into scratch in index order (warp
+// scan), then the FP64 sum runs sequentially in that order, exactly as the reference's loop.
+__device__ void refresh_stp(Ctx& c) {
+  if (!c.stp_dirty) return;
+  c.stp_dirty = false;
+  const int nw = (c.J + 31) >> 5;
+  const int lane = lane_id();
+  int base = 0;
+  for (int w0 = 0; w0 < nw; w0 += 32) {
+    const int wi = w0 + lane;
+    uint32_t word = wi < nw ? c.prog_mask[wi] : 0u;
+    const int cnt = __popc(word);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    int k = base + incl - cnt;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      word &= word - 1;
+      c.scratch[k++] = c.jobs[(wi << 5) + b].rate;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+  double s = 0.0;
+  int i = 0;
+  for (; i + 4 <= base; i += 4) {
+    const double a0 = c.scratch[i], a1 = c.scratch[i + 1], a2 = c.scratch[i + 2],
+                 a3 = c.scratch[i + 3];
+    s = s + a0;
+    s = s + a1;
+    s = s + a2;
+    s = s + a3;
+  }
+  for (; i < base; ++i) s = s + c.scratch[i];
+  __syncwarp();
+  if (s != c.stp_cur) {
+    c.stp_cur = s;
+    if (c.stp_series && c.stp_points < c.stp_cap && lane == 0) {
+      c.stp_series[2 * c.stp_points] = s_from_us(c.now);
+      c.stp_series[2 * c.stp_points + 1] = s;
+    }
+    ++c.stp_points;
+  }
+}
+
+__device__ __forceinline__ double true_rate(const DJob& j, int k) {
+  return effective_speed(j.truth[k], k, j.mem, j.qos);
+}
+__device__ __forceinline__ double est_rate(const DJob& j, int k) {
+  return effective_speed(j.est[k], k, j.mem, j.qos);
+}
+
+// ---- queue (std::set ordered by (arrival_us, entry_seq == idx)) -------------------------
+__device__ void enqueue(Ctx& c, int ji) {
+  const int64_t a = c.jobs[ji].arrival_us;
+  int pos = c.qtail;
+  while (pos > c.qhead) {  // sorted insert; arrivals append at the tail
+    const int prev = c.queue[pos - 1];
+    const int64_t pa = c.jobs[prev].arrival_us;
+    if (pa < a || (pa == a && prev < ji)) break;
+    __syncwarp();
+    c.queue[pos] = prev;
+    __syncwarp();
+    --pos;
+  }
+  c.queue[pos] = ji;
+  __syncwarp();
+  ++c.qtail;
+}
+
+// ---- GPU roster helpers -----------------------------------------------------------------
+__device__ __forceinline__ int lut_index(const uint8_t* k) {
+  return (((k[0] * 7 + k[1]) * 7 + k[2]) * 7 + k[3]) * 7 + k[4];
+}
+
+__device__ void roster_push(Ctx& c, DGpu& g, int ji) {
+  g.roster[g.nroster] = ji;
+  __syncwarp();
+  ++g.nroster;
+  ++g.kind_cnt[c.jobs[ji].min_kind];
+  g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
+}
+
+__device__ void roster_erase(Ctx& c, DGpu& g, int ji) {
+  int i = 0;
+  while (i < g.nroster && g.roster[i] != ji) ++i;
+  for (int k = i; k + 1 < g.nroster; ++k) {
+    const int v = g.roster[k + 1];
+    __syncwarp();
+    g.roster[k] = v;
+    __syncwarp();
+  }
+  --g.nroster;
+  --g.kind_cnt[c.jobs[ji].min_kind];
+  g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
+}
+
+// ---- forward declarations of the mutually recursive steps ---------------------------------
+__device__ __noinline__ void reopt_and_apply(Ctx& c, int gi, bool force);
+__device__ void finish_profiling(Ctx& c, int gi);
+
+// sim.hpp:480-489
+__device__ void start_running(Ctx& c, int ji, int s) {
+  DJob& j = c.jobs[ji];
+  const double r = true_rate(j, s);
+  if (c.p->check_invariants && !(r > 0)) fail(c, MISO_B200_SIM_INFEASIBLE_SLICE);
+  j.slice = static_cast<uint8_t>(s);
+  set_phase(c, ji, kRunning, r);
+  schedule_completion(c, ji);
+  log_rec(c, kLogStart, j.gpu, ji, static_cast<uint8_t>(s), 0, 0, r);
+}
+
+// sim.hpp:457-461 (spawn_instances is a no-op for instance_count == 1, the only supported)
+__device__ __forceinline__ void cache_estimates(DJob& j, const double* est) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) j.est[k] = est[k];
+  j.flags |= kHasEst;
+}
+
+// sim.hpp:670-680 with simulate_mps_rates / interp_speed (profiles.hpp:391-431)
+__device__ void rate_roster_mps(Ctx& c, int gi, int level) {
+  DGpu& g = c.gpus[gi];
+  const int n = g.nroster;
+  double share = static_cast<double>(level);
+  const double eq = 100.0 / static_cast<double>(n);
+  if (eq < share) share = eq;  // std::min(level, 100/n)
+  const double gpc = clampd(share / 100.0 * 7.0, 1.0, 7.0);
+  for (int i = 0; i < n; ++i) {
+    const int ji = g.roster[i];
+    const DJob& j = c.jobs[ji];
+    double sp;
+    if (gpc <= 1.0) {
+      sp = j.truth[0];
+    } else if (gpc >= 7.0) {
+      sp = j.truth[4];
+    } else {
+      const double knots[5] = {1, 2, 3, 4, 7};
+      int k = 1;
+      while (!(gpc <= knots[k])) ++k;
+      const double wgt = (gpc - knots[k - 1]) / (knots[k] - knots[k - 1]);
+      sp = j.truth[k - 1] + wgt * (j.truth[k] - j.truth[k - 1]);
+    }
+    const double rate = clampd(c.p->interference * sp, kSpeedFloor, 1.0);
+    set_phase(c, ji, kMps, rate);
+    schedule_completion(c, ji);
+  }
+}
+
+// sim.hpp:660-666
+__device__ void start_mps_window(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  const int level = g.mps_level == 0 ? 100 : (g.mps_level == 1 ? 50 : 14);  // kMpsLevels
+  rate_roster_mps(c, gi, level);
+  ++g.epoch;
+  push_event(c, c.J + gi, c.now + c.p->window_us, 2, kEvMpsEnd);
+  log_rec(c, kLogMpsWindow, gi, -1, 0, static_cast<uint32_t>(level), 0, 0);
+}
+
+// sim.hpp:654-658
+__device__ void begin_mps_windows(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  g.mps_level = 0;
+  log_rec(c, kLogMpsStart, gi, -1, 0, g.nroster, 0, 0);
+  start_mps_window(c, gi);
+}
+
+// sim.hpp:625-652
+__device__ void start_profiling_session(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  g.mode = kGpuMps;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) g.part[k] = 0;
+  g.objective = 0;
+  if (c.p->window_us == 0) {
+    finish_profiling(c, gi);
+    return;
+  }
+  ++c.mps_sessions;
+  bool need_ckpt = false;
+  if (c.p->ckpt_us > 0)
+    for (int i = 0; i < g.nroster; ++i)
+      if (c.jobs[g.roster[i]].flags & kRunState) need_ckpt = true;
+  if (need_ckpt) {
+    for (int i = 0; i < g.nroster; ++i) {
+      const int ji = g.roster[i];
+      set_phase(c, ji, (c.jobs[ji].flags & kRunState) ? kCkpt : kQueued, 0.0);
+    }
+    ++g.epoch;
+    push_event(c, c.J + gi, c.now + c.p->ckpt_us, 2, kEvCkptDone);
+    log_rec(c, kLogCkptStart, gi, -1, 0, g.nroster, 0, 0);
+  } else {
+    begin_mps_windows(c, gi);
+  }
+}
+
+// sim.hpp:691-714. Noisy mode: lane c predicts roster column c (predict_mig_speeds with call
+// nonce ++predictor_nonce_, then extrapolate_small_slices); columns are exchanged by shuffles.
+__device__ void finish_profiling(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  const int n = g.nroster;
+  if (!c.p->noisy) {
+    for (int i = 0; i < n; ++i) {
+      DJob& j = c.jobs[g.roster[i]];
+      cache_estimates(j, j.truth);
+    }
+  } else {
+    const uint64_t nonce = ++c.nonce;
+    double e[5] = {0, 0, 0, 0, 0};
+    const int ln = lane_id();
+    if (ln < n) {
+      const DJob& j = c.jobs[g.roster[ln]];
+      predict_column(j.truth[4], j.truth[3], j.truth[2], ln, c.rng_seed, nonce, true,
+                     c.p->target_mae, c.w, e);
+    }
+    __syncwarp();  // reconverge before the column exchange
+    for (int i = 0; i < n; ++i) {
+      double ei[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) ei[k] = __shfl_sync(0xffffffffu, e[k], i);
+      cache_estimates(c.jobs[g.roster[i]], ei);
+    }
+  }
+  reopt_and_apply(c, gi, true);
+}
+
+// sim.hpp:765-794
+__device__ void apply_assignment(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  if (!g.plan_valid) {
+    fail(c, MISO_B200_SIM_INVARIANT);
+    return;
+  }
+  g.plan_valid = 0;
+  if (g.plan_n != g.nroster) {
+    fail(c, MISO_B200_SIM_INVARIANT);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k];
+  g.objective = g.plan_obj;
+  g.mode = kGpuMig;
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) cnt += g.plan_part[k];
+  if (c.p->check_invariants && cnt != g.nroster) fail(c, MISO_B200_SIM_INVARIANT);
+  for (int i = 0; i < g.nroster; ++i)
+    if (g.plan_job[i] != g.roster[i]) fail(c, MISO_B200_SIM_INVARIANT);
+  log_rec(c, kLogPartition, gi, -1, static_cast<uint8_t>(g.nroster), pack_part(g.part), 0, 0);
+  for (int i = 0; i < g.nroster; ++i)
+    log_rec(c, kLogAssign, gi, g.roster[i], g.plan_slice[i], 0, 0, 0);
+  for (int i = 0; i < g.nroster; ++i) {
+    const int ji = g.roster[i];
+    const DJob& j = c.jobs[ji];
+    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
+    start_running(c, ji, g.plan_slice[i]);
+  }
+}
+
+// sim.hpp:739-763
+__device__ void begin_reconfig(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  bool any = false, restart = false;
+  for (int i = 0; i < g.nroster; ++i) {
+    const DJob& j = c.jobs[g.roster[i]];
+    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
+    any = true;
+    if (j.flags & kRunState) restart = true;
+  }
+  const int64_t pause = c.p->reconfig_us + (restart ? c.p->ckpt_us : 0);
+  g.plan_valid = 1;
+  if (!any || pause == 0) {
+    apply_assignment(c, gi);
+    return;
+  }
+  g.mode = kGpuReconfig;
+  for (int i = 0; i < g.nroster; ++i) {
+    const int ji = g.roster[i];
+    const DJob& j = c.jobs[ji];
+    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
+    set_phase(c, ji, (j.flags & kRunState) ? kCkpt : kQueued, 0.0);
+  }
+  ++g.epoch;
+  push_event(c, c.J + gi, c.now + pause, 2, kEvReconfigDone);
+  log_rec(c, kLogReconfigStart, gi, -1, 0, static_cast<uint32_t>(pause & 0xFFFFFFFF),
+          static_cast<uint32_t>(pause >> 32), 0);
+}
+
+// sim.hpp:716-733
+__device__ __noinline__ void reopt_and_apply(Ctx& c, int gi, bool force) {
+  DGpu& g = c.gpus[gi];
+  const int m = g.nroster;
+  double rows[7 * 5];
+  for (int i = 0; i < m; ++i) {
+    const DJob& j = c.jobs[g.roster[i]];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) rows[i * 5 + k] = est_rate(j, k);
+  }
+  double obj = 0.0;
+  const uint8_t cand = search_any<false>(rows, m, c.p->en0, c.p->en1, &obj);
+  if (cand >= kNumCands) {  // nullopt (or m out of range): SimInvariantError
+    fail(c, MISO_B200_SIM_NO_PARTITION);
+    return;
+  }
+  if (!force && !(obj > g.objective + 1e-12)) return;
+  ++c.repartitions;
+  g.plan_obj = obj;
+  g.plan_n = static_cast<uint8_t>(m);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) g.plan_part[k] = 0;
+  for (int i = 0; i < m; ++i) {
+    const int s = kCandPlaceD[cand][i];
+    g.plan_slice[i] = static_cast<uint8_t>(s);
+    g.plan_job[i] = g.roster[i];
+    g.plan_speed[i] = rows[i * 5 + s];
+    ++g.plan_part[s];
+  }
+  begin_reconfig(c, gi);
+}
+
+// sim.hpp:612-623
+__device__ void settle_admissions(Ctx& c, int gi) {
+  DGpu& g = c.gpus[gi];
+  if (c.p->policy == MISO_B200_POLICY_ORACLE)
+    for (int i = 0; i < g.nroster; ++i) {
+      DJob& j = c.jobs[g.roster[i]];
+      if (!(j.flags & kHasEst)) cache_estimates(j, j.truth);
+    }
+  bool all_est = true;
+  for (int i = 0; i < g.nroster; ++i) all_est = all_est && (c.jobs[g.roster[i]].flags & kHasEst);
+  if (all_est) reopt_and_apply(c, gi, true);
+  else start_profiling_session(c, gi);
+}
+
+// sim.hpp:581-607: least-loaded GPU whose spare slice covers the job's minimum (ties: id)
+__device__ int place_dynamic(Ctx& c, int ji) {
+  const int need = c.jobs[ji].min_kind;
+  int best = -1, best_cnt = 8;
+  for (int gi = lane_id(); gi < c.G; gi += 32) {
+    const DGpu& g = c.gpus[gi];
+    if (g.mode != kGpuIdle && g.mode != kGpuMig) continue;
+    if (g.nroster >= 7) continue;
+    if (g.nroster > 0 && (g.spare < 0 || g.spare < need)) continue;
+    if (g.nroster < best_cnt) {
+      best = gi;
+      best_cnt = g.nroster;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const int ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oc = __shfl_xor_sync(0xffffffffu, best_cnt, off);
+    if (ob >= 0 && (best < 0 || oc < best_cnt || (oc == best_cnt && ob < best))) {
+      best = ob;
+      best_cnt = oc;
+    }
+  }
+  if (best < 0) return -1;
+  ++c.qhead;  // pop_queue: the placed job is always the queue head
+  DGpu& g = c.gpus[best];
+  roster_push(c, g, ji);
+  c.jobs[ji].gpu = static_cast<int16_t>(best);
+  log_rec(c, kLogAdmit, best, ji, 0, 0, 0, 0);
+  return best;
+}
+
+// sim.hpp:465-478
+__device__ bool admit_nopart(Ctx& c, int ji) {
+  int best = -1;
+  for (int gi = lane_id(); gi < c.G; gi += 32)
+    if (c.gpus[gi].mode == kGpuIdle) {
+      best = gi;
+      break;
+    }
+  const unsigned any = __ballot_sync(0xffffffffu, best >= 0);
+  if (!any) return false;
+  // lowest id among lanes' first idle GPUs
+  int b = best >= 0 ? best : INT32_MAX;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, off));
+  ++c.qhead;
+  DGpu& g = c.gpus[b];
+  g.mode = kGpuMig;
+  roster_push(c, g, ji);
+  c.jobs[ji].gpu = static_cast<int16_t>(b);
+  log_rec(c, kLogAdmit, b, ji, 0, 0, 0, 0);
+  start_running(c, ji, 4);
+  return true;
+}
+
+// sim.hpp:398-418
+__device__ void drain_queue(Ctx& c) {
+  if (c.p->policy == MISO_B200_POLICY_NOPART) {
+    while (c.qhead < c.qtail && c.status == 0)
+      if (!admit_nopart(c, c.queue[c.qhead])) break;
+    return;
+  }
+  for (;;) {
+    int touched[32];
+    int nt = 0;
+    while (c.qhead < c.qtail && c.status == 0) {
+      const int gi = place_dynamic(c, c.queue[c.qhead]);
+      if (gi < 0) break;
+      bool seen = false;
+      for (int i = 0; i < nt; ++i) seen = seen || touched[i] == gi;
+      if (!seen) {
+        if (nt == 32) {  // flush early (rare: > 32 GPUs touched at one instant)
+          for (int i = 0; i < nt; ++i) settle_admissions(c, touched[i]);
+          nt = 0;
+        }
+        touched[nt++] = gi;
+      }
+    }
+    if (nt == 0) return;
+    for (int i = 0; i < nt && c.status == 0; ++i) settle_admissions(c, touched[i]);
+  }
+}
+
+// sim.hpp:837-890
+__device__ void complete_dynamic(Ctx& c, int gi, int ji) {
+  DGpu& g = c.gpus[gi];
+  const DJob& j = c.jobs[ji];
+  if (g.mode == kGpuMps) {
+    if (g.nroster == 0) {
+      ++g.epoch;
+      clear_slot(c, c.J + gi);
+      g.mode = kGpuIdle;
+      return;
+    }
+    const int lv = g.mps_level == 0 ? 100 : (g.mps_level == 1 ? 50 : 14);
+    rate_roster_mps(c, gi, lv);
+    return;
+  }
+  if (g.mode == kGpuReconfig) {
+    for (int i = 0; i < g.plan_n; ++i) {
+      if (g.plan_job[i] != ji) continue;
+      g.plan_obj -= g.plan_speed[i];
+      --g.plan_part[g.plan_slice[i]];
+      for (int k = i; k + 1 < g.plan_n; ++k) {
+        g.plan_job[k] = g.plan_job[k + 1];
+        g.plan_slice[k] = g.plan_slice[k + 1];
+        g.plan_speed[k] = g.plan_speed[k + 1];
+        __syncwarp();
+      }
+      --g.plan_n;
+      break;
+    }
+    if (g.part[j.slice] == 0) fail(c, MISO_B200_SIM_INVARIANT);
+    else --g.part[j.slice];
+    log_rec(c, kLogShrink, gi, -1, 0, pack_part(g.part), 0, 0);
+    return;
+  }
+  if (g.part[j.slice] == 0) fail(c, MISO_B200_SIM_INVARIANT);
+  else --g.part[j.slice];
+  if (g.nroster == 0) {
+    g.mode = kGpuIdle;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) g.part[k] = 0;
+    g.objective = 0;
+    return;
+  }
+  log_rec(c, kLogShrink, gi, -1, 0, pack_part(g.part), 0, 0);
+  double obj = 0;
+  for (int i = 0; i < g.nroster; ++i) {
+    const DJob& r = c.jobs[g.roster[i]];
+    obj += est_rate(r, r.slice);
+  }
+  g.objective = obj;
+  if (c.p->drift_threshold > 0 && c.p->policy == MISO_B200_POLICY_MISO && c.p->window_us > 0) {
+    for (int i = 0; i < g.nroster; ++i) {
+      const DJob& r = c.jobs[g.roster[i]];
+      const double est = est_rate(r, r.slice);
+      const double truth = true_rate(r, r.slice);
+      if (est > 0 && fabs(truth - est) / est > c.p->drift_threshold) {
+        start_profiling_session(c, gi);
+        return;
+      }
+    }
+  }
+  reopt_and_apply(c, gi, false);
+}
+
+// sim.hpp:798-835
+__device__ void on_completion(Ctx& c, int ji) {
+  DJob& j = c.jobs[ji];
+  advance_job(c, j);
+  if (c.p->check_invariants) {
+    const double base = j.base;
+    if (fabs(j.consumed - base) > 1e-6 * base + 1e-9) fail(c, MISO_B200_SIM_INVARIANT);
+  }
+  j.remaining = 0;
+  j.flags |= kDone;
+  ++j.epoch;
+  clear_slot(c, ji);
+  set_prog_bit(c, ji, false);
+  c.stp_dirty = true;
+  j.completion_us = c.now;
+  ++c.done_count;
+  if (c.now > c.last_completion) c.last_completion = c.now;
+  if (c.p->check_invariants) {
+    int64_t total = 0;
+#pragma unroll
+    for (int b = 0; b < 5; ++b) total += j.acc[b];
+    if (total != c.now - j.arrival_us) fail(c, MISO_B200_SIM_INVARIANT);
+  }
+  const int64_t jct = c.now - j.arrival_us;
+  log_rec(c, kLogComplete, -1, ji, 0, static_cast<uint32_t>(jct & 0xFFFFFFFF),
+          static_cast<uint32_t>(jct >> 32), 0);
+  const int gi = j.gpu;
+  DGpu& g = c.gpus[gi];
+  roster_erase(c, g, ji);
+  if (c.p->policy == MISO_B200_POLICY_NOPART) {
+    g.mode = kGpuIdle;
+    return;
+  }
+  complete_dynamic(c, gi, ji);
+}
+
+// sim.hpp:301-313
+__device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
+  if (slot < c.J) {
+    const int ji = slot;
+    if (kind == kEvArrival) {
+      log_rec(c, kLogArrival, -1, ji, 0, 0, 0, 0);
+      enqueue(c, ji);
+    } else if (kind == kEvCompletion) {
+      on_completion(c, ji);
+    }
+    return;
+  }
+  const int gi = slot - c.J;
+  DGpu& g = c.gpus[gi];
+  if (kind == kEvMpsEnd) {  // on_mps_phase_end, sim.hpp:682-689
+    if (++g.mps_level < 3) {
+      start_mps_window(c, gi);
+    } else {
+      log_rec(c, kLogMpsEnd, gi, -1, 0, 0, 0, 0);
+      finish_profiling(c, gi);
+    }
+  } else if (kind == kEvReconfigDone) {
+    apply_assignment(c, gi);
+  } else if (kind == kEvCkptDone) {
+    begin_mps_windows(c, gi);
+  }
+}
+
+// One warp per seed.
+__global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
+  const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (warp >= b.n_seeds) return;
+  const int lane = lane_id();
+  const int J0 = b.job_offsets[warp];
+  const int J = b.job_offsets[warp + 1] - J0;
+  const int G = prm.cluster_size;
+  unsigned char* ws = b.workspace + size_t(warp) * b.ws_stride;
+  Ctx c;
+  c.jobs = reinterpret_cast<DJob*>(ws);  // stride kSimJobBytes == sizeof rounded (asserted)
+  c.gpus = reinterpret_cast<DGpu*>(ws + sim_ws_gpus_off(b.max_jobs));
+  c.slots = reinterpret_cast<Slot*>(ws + sim_ws_slots_off(b.max_jobs, G));
+  c.queue = reinterpret_cast<int32_t*>(ws + sim_ws_queue_off(b.max_jobs, G));
+  c.prog_mask = reinterpret_cast<uint32_t*>(ws + sim_ws_mask_off(b.max_jobs, G));
+  c.scratch = reinterpret_cast<double*>(ws + sim_ws_scratch_off(b.max_jobs, G));
+  c.log = b.log ? b.log + size_t(warp) * b.log_cap : nullptr;
+  c.log_cap = b.log_cap;
+  c.log_n = 0;
+  c.stp_series = b.stp_series ? b.stp_series + size_t(warp) * 2 * b.stp_cap : nullptr;
+  c.stp_cap = b.stp_cap;
+  c.J = J;
+  c.G = G;
+  c.qhead = c.qtail = 0;
+  c.now = 0;
+  c.seq = 0;
+  c.nonce = 0;
+  c.stp_cur = 0;
+  c.stp_integral = 0;
+  c.stp_last = 0;
+  c.stp_points = 0;
+  c.stp_dirty = false;
+  c.repartitions = c.mps_sessions = c.done_count = 0;
+  c.first_progress = -1;
+  c.last_completion = -1;
+  c.status = 0;
+  c.processed = 0;
+  c.p = &prm;
+  c.spare_lut = b.spare_lut;
+  c.rng_seed = b.rng_seed[warp];
+  c.w = w;
+
+  // ---- init_jobs / init_gpus (sim.hpp:240-276), lanes in parallel ----
+  for (int i = lane; i < J; i += 32) {
+    DJob& j = c.jobs[i];
+    const int64_t a = us_from_s(b.arrival_s[J0 + i]);
+    j.remaining = b.base_s[J0 + i];
+    j.base = j.remaining;
+    j.consumed = 0;
+    j.rate = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      j.truth[k] = b.speeds5[(size_t(J0) + i) * 5 + k];
+      j.est[k] = 0;
+      j.acc[k] = 0;
+    }
+    j.arrival_us = a;
+    j.last_update_us = a;
+    j.first_progress_us = -1;
+    j.completion_us = -1;
+    j.epoch = 0;
+    j.gpu = -1;
+    j.phase = kQueued;
+    j.slice = 4;
+    j.mem = b.mem_gb[J0 + i];
+    j.qos = b.qos_kind[J0 + i];
+    const int qg = j.qos >= 0 ? kind_gpc(j.qos) : 0;
+    int mk = -1;  // min_slice_for (topology.hpp:68-72)
+    for (int k = 4; k >= 0; --k)
+      if (kind_mem_gb(k) >= j.mem && kind_gpc(k) >= qg) mk = k;
+    j.min_kind = static_cast<uint8_t>(mk < 0 ? 0xFF : mk);
+    j.flags = 0;
+    Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
+    s.t = a;
+    s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
+    c.slots[i] = s;
+  }
+  for (int gi = lane; gi < G; gi += 32) {
+    DGpu& g = c.gpus[gi];
+    g.objective = 0;
+    g.plan_obj = 0;
+    g.epoch = 0;
+    g.mode = kGpuIdle;
+    g.mps_level = 0;
+    g.nroster = 0;
+    g.plan_n = 0;
+    g.plan_valid = 0;
+    for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k] = g.kind_cnt[k] = 0;
+    g.spare = 4;
+    c.slots[J + gi].t = kNoEvent;
+  }
+  for (int i = lane; i < ((J + 31) >> 5); i += 32) c.prog_mask[i] = 0;
+  __syncwarp();
+  c.seq = static_cast<uint64_t>(J);
+  bool bad_job = false;
+  for (int i = 0; i < J; ++i) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
+
+  // ---- event loop (sim.hpp:221-233) ----
+  if (bad_job && prm.policy != MISO_B200_POLICY_NOPART) c.status = MISO_B200_SIM_INVARIANT;
+  while (c.status == 0) {
+    Slot ev;
+    const int slot = next_event(c, &ev);
+    if (slot < 0) break;
+    if (++c.processed > prm.max_events) {
+      c.status = MISO_B200_SIM_EVENT_BUDGET;
+      break;
+    }
+    clear_slot(c, slot);
+    __syncwarp();
+    c.stp_integral += c.stp_cur * s_from_us(ev.t - c.stp_last);
+    c.stp_last = ev.t;
+    c.now = ev.t;
+    dispatch(c, slot, static_cast<uint32_t>(ev.pk & 7));
+    drain_queue(c);
+    refresh_stp(c);
+    __syncwarp();
+  }
+
+  // ---- finalize (sim.hpp:902-949) ----
+  SimMetrics m;
+  m.status = c.status;
+  m.job_count = J;
+  m.completed_count = c.done_count;
+  m.completed = c.done_count == J;
+  m.repartitions = c.repartitions;
+  m.migrations = 0;
+  m.mps_sessions = c.mps_sessions;
+  m.events = static_cast<int64_t>(c.processed);
+  m.log_records = c.log_n;
+  m.stp_points = c.stp_points;
+  double totals[5] = {0, 0, 0, 0, 0};
+  double jct_sum = 0;
+  for (int i = 0; i < J; ++i) {
+    const DJob& j = c.jobs[i];
+    if (b.job_jct_us && lane == 0) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
+    if (!(j.flags & kDone)) continue;
+    jct_sum += s_from_us(j.completion_us - j.arrival_us);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) totals[k] += s_from_us(j.acc[k]);
+  }
+  m.queue_frac = m.mps_frac = m.checkpoint_frac = m.run_frac = m.idle_frac = 0;
+  if (jct_sum > 0) {
+    m.queue_frac = totals[0] / jct_sum;
+    m.mps_frac = totals[1] / jct_sum;
+    m.checkpoint_frac = totals[2] / jct_sum;
+    m.run_frac = totals[3] / jct_sum;
+    m.idle_frac = totals[4] / jct_sum;
+  }
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+  m.avg_jct_s = inf;
+  m.makespan_s = inf;
+  m.stp_time_avg = 0;
+  if (m.completed) {
+    m.avg_jct_s = jct_sum / static_cast<double>(J);
+    m.makespan_s = s_from_us(c.last_completion - c.first_progress);
+    if (c.last_completion > c.first_progress)
+      m.stp_time_avg = c.stp_integral / s_from_us(c.last_completion - c.first_progress);
+  }
+  m.jct_sum_s = jct_sum;
+  if (lane == 0) b.metrics[warp] = m;
+}
+
+}  // namespace sim
+
+size_t sim_workspace_stride(int max_jobs, int cluster_size) {
+  return sim_ws_total(max_jobs, cluster_size);
+}
+
+size_t sim_sizeof_job() { return sizeof(sim::DJob); }
+size_t sim_sizeof_gpu() { return sizeof(sim::DGpu); }
+
+cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double* w2,
+                            const double* w1, cudaStream_t stream) {
+  if (b.n_seeds == 0) return cudaSuccess;
+  ModelW w;
+  for (int i = 0; i < 4; ++i) {
+    w.w2[i] = w2[i];
+    w.w1[i] = w1[i];
+  }
+  const int threads = 128;
+  const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
+  sim::simulate_kernel<<<blocks, threads, 0, stream>>>(b, p, w);
+  return cudaGetLastError();
+}
+
+}  // namespace miso_b200

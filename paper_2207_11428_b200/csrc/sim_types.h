@@ -1,0 +1,77 @@
+// sim_types.h -- shared host/device types of the batched simulator (kernel (c)).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/miso_b200.h"
+
+namespace miso_b200 {
+
+typedef miso_b200_sim_metrics SimMetrics;
+typedef miso_b200_log_record LogRec;
+
+enum LogKind : uint8_t {
+  kLogArrival = MISO_B200_LOG_ARRIVAL, kLogAdmit = MISO_B200_LOG_ADMIT,
+  kLogStart = MISO_B200_LOG_START, kLogCkptStart = MISO_B200_LOG_CKPT_START,
+  kLogMpsStart = MISO_B200_LOG_MPS_START, kLogMpsWindow = MISO_B200_LOG_MPS_WINDOW,
+  kLogMpsEnd = MISO_B200_LOG_MPS_END, kLogReconfigStart = MISO_B200_LOG_RECONFIG_START,
+  kLogPartition = MISO_B200_LOG_PARTITION, kLogAssign = MISO_B200_LOG_ASSIGN,
+  kLogComplete = MISO_B200_LOG_COMPLETE, kLogShrink = MISO_B200_LOG_SHRINK,
+};
+
+struct SimParams {
+  int policy, cluster_size, noisy, check_invariants;
+  int64_t window_us, reconfig_us, ckpt_us;
+  double interference, target_mae, drift_threshold;
+  uint64_t max_events;
+  uint64_t en0, en1;  // enabled-candidate mask of the context's catalog
+};
+
+struct SimBatch {
+  int n_seeds, max_jobs;
+  const int32_t* job_offsets;
+  const double* arrival_s;
+  const double* base_s;
+  const double* speeds5;
+  const uint8_t* mem_gb;
+  const int8_t* qos_kind;
+  const uint64_t* rng_seed;
+  const int8_t* spare_lut;
+  unsigned char* workspace;
+  size_t ws_stride;
+  SimMetrics* metrics;
+  int64_t* job_jct_us;
+  LogRec* log;
+  int64_t log_cap;
+  double* stp_series;
+  int64_t stp_cap;
+};
+
+// Per-seed workspace layout: [jobs][gpus][slots][queue][progress mask][rate scratch]
+constexpr size_t kSimJobBytes = 216;
+constexpr size_t kSimGpuBytes = 192;
+__host__ __device__ inline size_t sim_al(size_t x) { return (x + 127) & ~size_t(127); }
+__host__ __device__ inline size_t sim_ws_gpus_off(int J) { return sim_al(size_t(J) * kSimJobBytes); }
+__host__ __device__ inline size_t sim_ws_slots_off(int J, int G) {
+  return sim_ws_gpus_off(J) + sim_al(size_t(G) * kSimGpuBytes);
+}
+__host__ __device__ inline size_t sim_ws_queue_off(int J, int G) {
+  return sim_ws_slots_off(J, G) + sim_al(size_t(J + G) * 16);
+}
+__host__ __device__ inline size_t sim_ws_mask_off(int J, int G) {
+  return sim_ws_queue_off(J, G) + sim_al(size_t(J + 1) * 4);
+}
+__host__ __device__ inline size_t sim_ws_scratch_off(int J, int G) {
+  return sim_ws_mask_off(J, G) + sim_al(size_t((J + 31) / 32 + 32) * 4);
+}
+__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+  return sim_ws_scratch_off(J, G) + sim_al(size_t(J + 32) * 8);
+}
+
+size_t sim_workspace_stride(int max_jobs, int cluster_size);
+size_t sim_sizeof_job();
+size_t sim_sizeof_gpu();
+cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double* w2,
+                            const double* w1, cudaStream_t stream);
+
+}  // namespace miso_b200

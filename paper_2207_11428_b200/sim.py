@@ -1,0 +1,235 @@
+"""Python side of the batched simulator (kernel (c)): trace generation, options, batching,
+and rendering of the compact event-log records into the reference's text format.
+
+Mirrors the reference's simulator interface (sim.hpp): `SimOptions` (:81-96) with
+`OverheadSpec` (:62-67) and `PredictorSpec` (profiles.hpp:173-178), `run_simulation`
+(:976-979) -> `MetricsReport` (:106-122), and the event log text written by `log()`
+(:365-367). `simulate_batch` runs many traces (seeds) in one launch, one warp per seed.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._native import Context, _check, lib
+from .catalog import KIND_NAMES, partition_name
+
+POLICIES = {"nopart": 0, "oracle": 2, "miso": 3}
+
+
+class SimOptionsC(C.Structure):
+    _fields_ = [
+        ("policy", C.c_int), ("cluster_size", C.c_int), ("mig_reconfig_s", C.c_double),
+        ("checkpoint_restart_s", C.c_double), ("mps_window_s", C.c_double),
+        ("interference", C.c_double), ("predictor_noisy", C.c_int), ("target_mae", C.c_double),
+        ("check_invariants", C.c_int), ("reprofile_drift_threshold", C.c_double),
+        ("max_events", C.c_uint64),
+    ]
+
+
+class SimMetricsC(C.Structure):
+    _fields_ = [
+        ("status", C.c_int), ("completed", C.c_int), ("job_count", C.c_int),
+        ("completed_count", C.c_int), ("repartitions", C.c_int), ("migrations", C.c_int),
+        ("mps_sessions", C.c_int), ("pad", C.c_int), ("avg_jct_s", C.c_double),
+        ("makespan_s", C.c_double), ("stp_time_avg", C.c_double), ("jct_sum_s", C.c_double),
+        ("queue_frac", C.c_double), ("mps_frac", C.c_double), ("checkpoint_frac", C.c_double),
+        ("run_frac", C.c_double), ("idle_frac", C.c_double), ("events", C.c_int64),
+        ("log_records", C.c_int64), ("stp_points", C.c_int64),
+    ]
+
+
+LOG_DTYPE = np.dtype([("t", "<i8"), ("kind", "u1"), ("x", "u1"), ("gpu", "<u2"), ("job", "<i4"),
+                      ("a", "<u4"), ("b", "<u4"), ("v", "<f8")])
+METRIC_FIELDS = [f for f, _ in SimMetricsC._fields_ if f != "pad"]
+METRICS_DTYPE = np.dtype([(f, "<i4") for f in ("status", "completed", "job_count", "completed_count",
+                                               "repartitions", "migrations", "mps_sessions", "pad")]
+                         + [(f, "<f8") for f in ("avg_jct_s", "makespan_s", "stp_time_avg",
+                                                 "jct_sum_s", "queue_frac", "mps_frac",
+                                                 "checkpoint_frac", "run_frac", "idle_frac")]
+                         + [(f, "<i8") for f in ("events", "log_records", "stp_points")])
+assert METRICS_DTYPE.itemsize == C.sizeof(SimMetricsC)
+assert LOG_DTYPE.itemsize == 32
+
+lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_int,
+                                         C.c_double, C.c_double, C.c_double, C.c_double,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
+    [C.c_void_p] * 10 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
+
+
+@dataclass
+class SimOptions:
+    """SimOptions + OverheadSpec + PredictorSpec (defaults as in the reference)."""
+    policy: str = "miso"
+    cluster_size: int = 8
+    mig_reconfig_s: float = 4.0
+    checkpoint_restart_s: float = 30.0
+    mps_window_s: float = 10.0
+    interference: float = 0.8
+    predictor: str = "oracle"          # "oracle" | "noisy" (PredictorSpec::Mode default oracle)
+    target_mae: float = 0.017
+    check_invariants: bool = True
+    reprofile_drift_threshold: float = 0.0
+    max_events: int = 100_000_000
+
+    def to_c(self) -> SimOptionsC:
+        return SimOptionsC(POLICIES[self.policy], self.cluster_size, self.mig_reconfig_s,
+                           self.checkpoint_restart_s, self.mps_window_s, self.interference,
+                           1 if self.predictor == "noisy" else 0, self.target_mae,
+                           1 if self.check_invariants else 0, self.reprofile_drift_threshold,
+                           self.max_events)
+
+
+@dataclass
+class Trace:
+    """JobTrace (workload.hpp:61-64) as arrays; job ids are "j<i>"."""
+    arrival_s: np.ndarray
+    duration_s: np.ndarray
+    speeds5: np.ndarray         # (n, 5), kind order 1g..7g
+    mem_gb: np.ndarray
+    qos_kind: Optional[np.ndarray] = None
+    seed: int = 0
+
+    @property
+    def n(self) -> int:
+        return len(self.arrival_s)
+
+
+def generate_trace(seed: int, job_count: int = 100, lambda_s: float = 60.0,
+                   max_duration_s: float = 7200.0, dist: str = "lognormal", sigma: float = 1.5,
+                   fixed_s: float = 600.0, lo_s: float = 60.0, hi_s: float = 7200.0) -> Trace:
+    """generate_trace (workload.hpp:97-114), in this library's host C++."""
+    kind = {"lognormal": 0, "fixed": 1, "uniform": 2}[dist]
+    a = np.zeros(job_count)
+    d = np.zeros(job_count)
+    sp = np.zeros((job_count, 5))
+    mem = np.zeros(job_count, np.int32)
+    _check(lib.miso_b200_generate_trace(seed, job_count, lambda_s, max_duration_s, kind, sigma,
+                                        fixed_s, lo_s, hi_s, a.ctypes.data, d.ctypes.data,
+                                        sp.ctypes.data, mem.ctypes.data))
+    return Trace(a, d, sp, mem, None, seed)
+
+
+@dataclass
+class SimResult:
+    metrics: np.ndarray                    # METRICS_DTYPE per seed
+    job_jct_us: Optional[List[np.ndarray]] = None
+    logs: Optional[List[np.ndarray]] = None  # LOG_DTYPE records per seed
+    stp: Optional[List[np.ndarray]] = None   # (points, 2) per seed
+    traces: List[Trace] = field(default_factory=list)
+
+    def report(self, i: int) -> dict:
+        m = self.metrics[i]
+        return {f: m[f].item() for f in METRICS_DTYPE.names if f != "pad"}
+
+
+def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
+                   rng_seeds: Optional[Sequence[int]] = None, log_cap: int = 0,
+                   stp_cap: int = 0, want_jct: bool = False, stream=None) -> SimResult:
+    """run_simulation for every trace at once (device). rng_seeds default to each trace's seed
+    (experiment.hpp:305)."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    S = len(traces)
+    offs = np.zeros(S + 1, np.int32)
+    offs[1:] = np.cumsum([t.n for t in traces])
+    cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
+    arr = cat(lambda t: t.arrival_s, np.float64)
+    dur = cat(lambda t: t.duration_s, np.float64)
+    sp = cat(lambda t: t.speeds5, np.float64)
+    mem = cat(lambda t: t.mem_gb, np.uint8)
+    qos = cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8)
+    seeds = np.asarray(rng_seeds if rng_seeds is not None else [t.seed for t in traces], np.uint64)
+    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    d_offs, d_arr, d_dur, d_sp = T(offs, None), T(arr, None), T(dur, None), T(sp, None)
+    d_mem, d_qos, d_seed = T(mem, None), T(qos, None), T(seeds.view(np.int64), None)
+    d_met = torch.empty(S * METRICS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    d_jct = torch.empty(int(offs[-1]), dtype=torch.int64, device=dev) if want_jct else None
+    d_log = torch.empty(S * log_cap * 32, dtype=torch.uint8, device=dev) if log_cap else None
+    d_stp = torch.empty(S * stp_cap * 2, dtype=torch.float64, device=dev) if stp_cap else None
+    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    o = opts.to_c()
+    p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    _check(lib.miso_b200_simulate_batch(ctx._h, C.byref(o), S, p(d_offs), p(d_arr), p(d_dur),
+                                        p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
+                                        p(d_jct), p(d_log), log_cap, p(d_stp), stp_cap, s))
+    torch.cuda.synchronize(dev)
+    met = d_met.cpu().numpy().view(METRICS_DTYPE)
+    res = SimResult(met, traces=list(traces))
+    if want_jct:
+        j = d_jct.cpu().numpy()
+        res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(S)]
+    if log_cap:
+        lg = d_log.cpu().numpy().view(LOG_DTYPE).reshape(S, log_cap)
+        res.logs = [lg[i, : min(log_cap, int(met[i]["log_records"]))] for i in range(S)]
+    if stp_cap:
+        st = d_stp.cpu().numpy().reshape(S, stp_cap, 2)
+        res.stp = [st[i, : min(stp_cap, int(met[i]["stp_points"]))] for i in range(S)]
+    return res
+
+
+def fmt_g(v: float) -> str:
+    """fmt_g (common.hpp:126-132): %.10g, inf/nan spelled out."""
+    if np.isinf(v):
+        return "inf" if v > 0 else "-inf"
+    if np.isnan(v):
+        return "nan"
+    return "%.10g" % v
+
+
+def _counts(packed: int):
+    return tuple((packed >> (4 * k)) & 15 for k in range(5))
+
+
+def render_log(records: np.ndarray, job_ids=None) -> str:
+    """Render compact records as the reference's event log text (sim.hpp:365-367 and the
+    log() call sites listed in SURVEY.md 5)."""
+    jid = (lambda j: job_ids[j]) if job_ids is not None else (lambda j: f"j{j}")
+    out = []
+    i = 0
+    n = len(records)
+    while i < n:
+        r = records[i]
+        t, k, g, j = int(r["t"]), int(r["kind"]), int(r["gpu"]), int(r["job"])
+        a, b = int(r["a"]), int(r["b"])
+        if k == 0:
+            line = f"arrival job={jid(j)}"
+        elif k == 1:
+            line = f"admit gpu={g} job={jid(j)}"
+        elif k == 2:
+            line = f"start job={jid(j)} gpu={g} slice={KIND_NAMES[int(r['x'])]} rate={fmt_g(float(r['v']))}"
+        elif k == 3:
+            line = f"ckpt_start gpu={g} jobs={a}"
+        elif k == 4:
+            line = f"mps_start gpu={g} jobs={a}"
+        elif k == 5:
+            line = f"mps_window gpu={g} level={a}"
+        elif k == 6:
+            line = f"mps_end gpu={g}"
+        elif k == 7:
+            line = f"reconfig_start gpu={g} pause_us={a | (b << 32)}"
+        elif k == 8:
+            m = int(r["x"])
+            pairs = [f"{jid(int(q['job']))}@{KIND_NAMES[int(q['x'])]}" for q in records[i + 1: i + 1 + m]]
+            line = f"partition gpu={g} shape={partition_name(_counts(a))} assign={','.join(pairs)}"
+            i += m
+        elif k == 10:
+            line = f"complete job={jid(j)} jct_us={a | (b << 32)}"
+        elif k == 11:
+            line = f"shrink gpu={g} shape={partition_name(_counts(a))}"
+        else:
+            line = f"?kind={k}"
+        out.append(f"{t} {line}\n")
+        i += 1
+    return "".join(out)
+
+
+def _simulate(self, traces, opts=None, **kw):
+    return simulate_batch(self, traces, opts or SimOptions(), **kw)
+
+
+Context.simulate = _simulate

@@ -155,6 +155,12 @@ class Ref:
                                    C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
                                    C.c_double, C.c_int, C.POINTER(RefSimOut), C.c_char_p, C.c_int64]
         L.ref_simulate.restype = C.c_int64
+        _ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+        L.ref_simulate_trace.argtypes = [C.c_int, _dp, _dp, _dp, _ip, _ip, C.c_uint64, C.c_int,
+                                         C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                         C.c_int, C.c_double, C.c_uint64, C.POINTER(RefSimOut),
+                                         C.c_char_p, C.c_int64, C.c_void_p, C.c_int64]
+        L.ref_simulate_trace.restype = C.c_int64
         L.ref_rng_raw.argtypes = [C.c_uint64, C.c_size_t, np.ctypeslib.ndpointer(np.uint64)]
         L.ref_c1_chain.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_uint64,
                                    _dp, _i32p, _dp, C.POINTER(C.c_int), _u8p,
@@ -211,6 +217,24 @@ class Ref:
         self.lib.ref_predict_batch(np.ascontiguousarray(truth3), n, cpg, first_nonce, rng_seed,
                                    int(noisy), mae, threads, out)
         return out
+
+    def simulate_trace(self, arrival_s, duration_s, speeds5, mem_gb, qos_kind=None, seed=0,
+                       cluster_size=8, policy=3, mig_reconfig_s=4.0, checkpoint_restart_s=30.0,
+                       mps_window_s=10.0, interference=0.8, noisy=True, target_mae=0.017,
+                       rng_seed=0, want_log=False, log_cap=1 << 26, stp_cap=0):
+        n = len(arrival_s)
+        qos = np.full(n, -1, np.int32) if qos_kind is None else np.asarray(qos_kind, np.int32)
+        out = RefSimOut()
+        buf = C.create_string_buffer(log_cap) if want_log else None
+        stp = np.zeros(2 * stp_cap) if stp_cap else None
+        r = self.lib.ref_simulate_trace(
+            n, np.ascontiguousarray(arrival_s, np.float64), np.ascontiguousarray(duration_s, np.float64),
+            np.ascontiguousarray(speeds5, np.float64).reshape(-1), np.ascontiguousarray(mem_gb, np.int32),
+            qos, seed, cluster_size, policy, mig_reconfig_s, checkpoint_restart_s, mps_window_s,
+            interference, int(noisy), target_mae, rng_seed, C.byref(out), buf,
+            log_cap if want_log else 0, None if stp is None else stp.ctypes.data, stp_cap)
+        log = buf.raw[: min(r, log_cap)].decode() if (want_log and r >= 0) else None
+        return out, log, stp
 
     def gen_trace(self, seed, job_count, lambda_s=60.0, max_duration_s=7200.0, sigma=1.5):
         arr = np.zeros(job_count); dur = np.zeros(job_count)

@@ -1,0 +1,144 @@
+"""GPU parity tests for kernel (c), the batched event-step simulator (one warp per seed).
+
+Bar (north_star): simulated event orders bit-exact -- the rendered event log must equal the
+reference's text byte for byte -- and JCT statistics within 1e-5 (asserted bit-exact here,
+since the engine keeps the reference's FP64 evaluation order, including the sequential STP sum).
+The reference is run through oracle/_ref (the unmodified sim.hpp) on the same traces.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+POL = {"nopart": 0, "oracle": 2, "miso": 3}
+
+
+def ref_run(ref, tr, opts, rng_seed, want_log=True):
+    out, log, _ = ref.simulate_trace(
+        tr.arrival_s, tr.duration_s, tr.speeds5, tr.mem_gb, tr.qos_kind, seed=tr.seed,
+        cluster_size=opts.cluster_size, policy=POL[opts.policy],
+        mig_reconfig_s=opts.mig_reconfig_s, checkpoint_restart_s=opts.checkpoint_restart_s,
+        mps_window_s=opts.mps_window_s, interference=opts.interference,
+        noisy=opts.predictor == "noisy", target_mae=opts.target_mae, rng_seed=rng_seed,
+        want_log=want_log)
+    return out, log
+
+
+def check_metrics(got, want):
+    assert got["status"] == 0
+    assert bool(got["completed"]) == bool(want.completed)
+    assert got["completed_count"] == want.completed_count
+    assert got["repartitions"] == want.repartitions
+    assert got["mps_sessions"] == want.mps_sessions
+    for f in ("avg_jct_s", "makespan_s", "stp_time_avg", "queue_frac", "mps_frac",
+              "checkpoint_frac", "run_frac", "idle_frac"):
+        g, w = float(got[f]), float(getattr(want, f))
+        assert g == w or abs(g - w) <= 1e-12 * max(1.0, abs(w)), (f, g, w)
+    assert got["stp_points"] == want.stp_points
+
+
+def run_and_compare(ctx, ref, traces, opts, log_cap=1 << 16):
+    import paper_2207_11428_b200 as m
+    res = m.simulate_batch(ctx, traces, opts, log_cap=log_cap)
+    for i, tr in enumerate(traces):
+        want, wlog = ref_run(ref, tr, opts, tr.seed)
+        got = res.report(i)
+        assert got["log_records"] <= log_cap
+        text = m.render_log(res.logs[i])
+        assert wlog and wlog.count("\n") >= 3 * tr.n  # arrival + admit + complete per job at least
+        if text != wlog:
+            a, b = text.splitlines(), wlog.splitlines()
+            k = next((q for q in range(min(len(a), len(b))) if a[q] != b[q]), min(len(a), len(b)))
+            raise AssertionError(f"seed {tr.seed}: event logs diverge at line {k}: "
+                                 f"got {a[k:k+3]} want {b[k:k+3]}")
+        check_metrics(got, want)
+    return res
+
+
+@pytest.mark.parametrize("policy,predictor", [("miso", "noisy"), ("miso", "oracle"),
+                                              ("oracle", "oracle"), ("nopart", "oracle")])
+def test_event_log_parity_small(ctx, ref, policy, predictor):
+    import paper_2207_11428_b200 as m
+    traces = [m.generate_trace(seed, 100, lambda_s=60.0) for seed in (1, 2, 3, 1000)]
+    opts = m.SimOptions(policy=policy, cluster_size=8, predictor=predictor)
+    run_and_compare(ctx, ref, traces, opts)
+
+
+def test_event_log_parity_config4_shape(ctx, ref):
+    """Config 4: 100 GPUs, 1000-job Poisson trace (lambda 10 s), noisy predictor 0.017."""
+    import paper_2207_11428_b200 as m
+    traces = [m.generate_trace(seed, 1000, lambda_s=10.0) for seed in (0, 1)]
+    opts = m.SimOptions(policy="miso", cluster_size=100, predictor="noisy")
+    run_and_compare(ctx, ref, traces, opts, log_cap=1 << 16)
+
+
+def test_clairvoyant_equivalence(ctx):
+    """acceptance_test.cpp:141-177 / sim_test.cpp:161-221: zero overheads + oracle predictor
+    -> miso and oracle policies produce byte-identical event logs and equal metrics."""
+    import paper_2207_11428_b200 as m
+    traces = [m.generate_trace(9000 + t, 100, lambda_s=60.0) for t in range(50)]
+    kw = dict(cluster_size=8, mig_reconfig_s=0, checkpoint_restart_s=0, mps_window_s=0,
+              predictor="oracle")
+    a = m.simulate_batch(ctx, traces, m.SimOptions(policy="miso", **kw), log_cap=1 << 14)
+    b = m.simulate_batch(ctx, traces, m.SimOptions(policy="oracle", **kw), log_cap=1 << 14)
+    for i in range(len(traces)):
+        la, lb = m.render_log(a.logs[i]), m.render_log(b.logs[i])
+        assert la == lb and la
+        assert a.metrics[i]["avg_jct_s"] == b.metrics[i]["avg_jct_s"]
+
+
+def test_seven_parallel_friendly_jobs(ctx, ref):
+    """sim_test.cpp:135-159: seven f(g)=(g/7)^0.5 jobs on one GPU -> STP sqrt(7), 13
+    repartitions, no MPS sessions (zero overheads, oracle predictor)."""
+    import paper_2207_11428_b200 as m
+    g = np.array([1, 2, 3, 4, 7]) / 7.0
+    sp = np.tile(g ** 0.5, (7, 1))
+    tr = m.Trace(np.zeros(7), np.full(7, 100.0), sp, np.full(7, 5), None, 0)
+    opts = m.SimOptions(policy="miso", cluster_size=1, mig_reconfig_s=0, checkpoint_restart_s=0,
+                        mps_window_s=0, predictor="oracle")
+    res = run_and_compare(ctx, ref, [tr], opts)
+    r = res.report(0)
+    rate = np.sqrt(1.0 / 7.0)
+    assert r["completed"] == 1 and r["completed_count"] == 7
+    assert abs(r["avg_jct_s"] - 100.0 / rate) < 1e-5
+    assert abs(r["stp_time_avg"] - np.sqrt(7.0)) < 1e-9
+    assert r["repartitions"] == 13 and r["mps_sessions"] == 0
+
+
+def test_profiling_sessions_counted(ctx, ref):
+    """sim_test.cpp:223-246: j0 profiles alone; j1..j3 queue and share one batched session."""
+    import paper_2207_11428_b200 as m
+    sp = np.tile([0.3, 0.5, 0.7, 0.8, 1.0], (4, 1))
+    tr = m.Trace(np.arange(4) * 5.0, np.full(4, 300.0), sp, np.full(4, 5), None, 0)
+    opts = m.SimOptions(policy="miso", cluster_size=1, predictor="noisy", target_mae=0.05)
+    res = m.simulate_batch(ctx, [tr], opts, rng_seeds=[9], log_cap=4096)
+    want, wlog = ref_run(ref, tr, opts, 9)
+    assert m.render_log(res.logs[0]) == wlog
+    r = res.report(0)
+    assert r["mps_sessions"] == 2 and r["mps_frac"] > 0 and r["checkpoint_frac"] > 0
+    check_metrics(r, want)
+
+
+def test_memory_pinned_and_qos_jobs(ctx, ref):
+    """Traces with 40 GB jobs (7g only) and QoS floors exercise effective_speed zeroing,
+    spare-slice admission and head-of-line blocking."""
+    import paper_2207_11428_b200 as m
+    rng = np.random.default_rng(4)
+    traces = []
+    for s in range(4):
+        t = m.generate_trace(500 + s, 120, lambda_s=30.0)
+        t.mem_gb = np.where(rng.random(t.n) < 0.08, 40, t.mem_gb).astype(np.int32)
+        t.qos_kind = np.where(rng.random(t.n) < 0.15, rng.integers(0, 4, t.n), -1).astype(np.int8)
+        traces.append(t)
+    for pol, pred in (("miso", "noisy"), ("oracle", "oracle")):
+        run_and_compare(ctx, ref, traces, m.SimOptions(policy=pol, cluster_size=6, predictor=pred))
+
+
+def test_invalid_sim_options(ctx):
+    import paper_2207_11428_b200 as m
+    tr = [m.generate_trace(1, 10)]
+    for bad in (dict(cluster_size=0), dict(interference=0.0), dict(mig_reconfig_s=-1.0),
+                dict(target_mae=0.7, predictor="noisy")):
+        with pytest.raises(m.MisoError) as ei:
+            m.simulate_batch(ctx, tr, m.SimOptions(**bad))
+        assert ei.value.code == -2
