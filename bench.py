@@ -259,6 +259,59 @@ def bench_c3(args):
                       "cpu_baseline": cpu}), flush=True)
 
 
+def bench_c4(args):
+    """Config 4: cluster simulation, 100 GPUs, 1000-job Poisson traces (lambda 10 s), miso
+    policy with the noisy predictor (0.017, rng_seed = trace seed), default overheads; seeds
+    0..S-1 in one launch (one warp per seed). Secondary measurement: seeds/s and events/s,
+    beside the reference's run_simulation on every host thread."""
+    import torch
+    import paper_2207_11428_b200 as miso
+    from concurrent.futures import ThreadPoolExecutor
+    ctx = miso.Context(0)
+    S = args.seeds
+    traces = [miso.generate_trace(s, 1000, lambda_s=10.0) for s in range(S)]
+    opts = miso.SimOptions(policy="miso", cluster_size=100, predictor="noisy")
+    for _ in range(max(1, args.warmup)):
+        res = miso.simulate_batch(ctx, traces, opts)
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = miso.simulate_batch(ctx, traces, opts)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = statistics.median(times)
+    ev = int(res.metrics["events"].sum())
+    ok = int((res.metrics["status"] == 0).sum())
+    cpu = None
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    if oracle_lib.have_ref() and not args.no_cpu_baseline:
+        ref = oracle_lib.Ref()
+        threads = oracle_lib.host_threads()
+        k = min(S, 2 * threads)
+
+        def one(s):
+            t = traces[s]
+            ref.simulate_trace(t.arrival_s, t.duration_s, t.speeds5, t.mem_gb, None, seed=s,
+                               cluster_size=100, policy=3, noisy=True, rng_seed=s)
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, range(k)))
+        dt = time.perf_counter() - t0
+        cpu = {"value": k / dt, "unit": "seeds/s", "cores": threads, "kind": "reference",
+               "sample": f"{k} seeds, miso policy, {threads} threads"}
+    print(json.dumps({"metric": "cluster-simulation seeds/sec (config 4, miso, 100 GPUs x 1000 jobs)",
+                      "value": S / (ms / 1e3), "unit": "seeds/s", "ms_per_step": ms,
+                      "events_per_s": ev / (ms / 1e3), "events_per_seed": ev / S,
+                      "seeds": S, "seeds_ok": ok, "steps": args.steps, "warmup": args.warmup,
+                      "dtype": "f64", "data": "synthetic (generate_trace seeds 0..S-1)",
+                      "mean_avg_jct_s": float(res.metrics["avg_jct_s"].mean()),
+                      "cpu_baseline": cpu}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,11 +319,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", choices=["c2", "c3"], default="c2",
-                    help="c2 = headline (config 2); c3 = secondary predictor measurement")
+    ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
+                    help="c2 = headline (config 2); c3 / c4 = secondary measurements")
+    ap.add_argument("--seeds", type=int, default=1024, help="c4: trace seeds per launch")
     args = ap.parse_args()
     if args.config == "c3":
         bench_c3(args)
+        return
+    if args.config == "c4":
+        bench_c4(args)
         return
 
     rank = int(os.environ.get("RANK", "0"))

@@ -10,8 +10,9 @@
 //     counts, cached per GPU;
 //   * predictor (finish_profiling, sim.hpp:691-714): one lane per roster column (mt19937_64
 //     seeding + glibc-exact log/cos, predict.cuh), results exchanged by shuffles;
-//   * STP refresh (sim.hpp:353-361): progressing jobs kept as a bitmask; the FP64 sum itself
-//     stays sequential in job-index order (bit-exact STP series).
+//   * next event: per-lane register minima over owned slots, one warp argmin per event;
+//   * STP refresh (sim.hpp:353-361): a dense per-job effective-rate array summed sequentially
+//     over the window of arrived, unfinished jobs (bit-exact STP series).
 // The partition search of reopt_and_apply (sim.hpp:716-733) is search.cuh's straight-line
 // search, executed redundantly by all lanes.
 //
@@ -81,8 +82,13 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   DGpu* gpus;
   Slot* slots;          // [J job slots][G gpu slots]
   int32_t* queue;       // FCFS order (arrival_us, idx), qhead..qtail
-  uint32_t* prog_mask;  // bit j: job j progressing and not done
-  double* scratch;      // rate compaction for refresh_stp
+  double* rate_eff;     // [J] rate if progressing and not done, else 0.0 (refresh_stp)
+  int stp_lo, n_arrived; // jobs < stp_lo are done; jobs >= n_arrived have not arrived
+  // per-lane minimum of the event slots this lane owns (slot % 32 == lane); lazily rescanned
+  int64_t lmin_t;
+  uint64_t lmin_pk;
+  int lmin_idx;
+  bool lmin_valid;
   LogRec* log;
   int64_t log_cap, log_n;
   int J, G;
@@ -152,26 +158,48 @@ __device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t
   s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
   ++c.seq;
   c.slots[slot] = s;
+  if ((slot & 31) == lane_id()) {  // owner lane keeps its minimum current
+    if (c.lmin_idx == slot) c.lmin_valid = false;
+    else if (c.lmin_valid && (t < c.lmin_t || (t == c.lmin_t && s.pk < c.lmin_pk))) {
+      c.lmin_t = t;
+      c.lmin_pk = s.pk;
+      c.lmin_idx = slot;
+    }
+  }
 }
 
 __device__ __forceinline__ void clear_slot(Ctx& c, int slot) {
   c.slots[slot].t = kNoEvent;
+  if ((slot & 31) == lane_id() && c.lmin_idx == slot) c.lmin_valid = false;
 }
 
-// Warp argmin over live slots: returns slot index (or -1), with its key.
+// Next event = minimum live (t, prio, seq) key. Slot i is owned by lane i % 32, which keeps
+// the minimum of its slots in registers (updated on push, invalidated when that slot is
+// cleared or overwritten) and rescans its ~(J+G)/32 slots only when invalidated; the event is
+// then one warp argmin over the 32 lane minima.
 __device__ int next_event(Ctx& c, Slot* out) {
   const int n = c.J + c.G;
-  int64_t bt = kNoEvent;
-  uint64_t bk = ~0ull;
-  int bi = -1;
-  for (int i = lane_id(); i < n; i += 32) {
-    const Slot s = c.slots[i];
-    if (s.t < bt || (s.t == bt && s.pk < bk)) {
-      bt = s.t;
-      bk = s.pk;
-      bi = i;
+  if (!c.lmin_valid) {
+    int64_t bt = kNoEvent;
+    uint64_t bk = ~0ull;
+    int bi = -1;
+    for (int i = lane_id(); i < n; i += 32) {
+      const Slot s = c.slots[i];
+      if (s.t < bt || (s.t == bt && s.pk < bk)) {
+        bt = s.t;
+        bk = s.pk;
+        bi = i;
+      }
     }
+    c.lmin_t = bt;
+    c.lmin_pk = bk;
+    c.lmin_idx = bi;
+    c.lmin_valid = true;
   }
+  __syncwarp();
+  int64_t bt = c.lmin_t;
+  uint64_t bk = c.lmin_pk;
+  int bi = c.lmin_idx;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
@@ -189,16 +217,6 @@ __device__ int next_event(Ctx& c, Slot* out) {
 }
 
 // ---- job state ---------------------------------------------------------------------------
-__device__ __forceinline__ void set_prog_bit(Ctx& c, int j, bool on) {
-  uint32_t* w = c.prog_mask + (j >> 5);
-  const uint32_t bit = 1u << (j & 31);
-  const uint32_t cur = *w;
-  const uint32_t nv = on ? (cur | bit) : (cur & ~bit);
-  __syncwarp();
-  *w = nv;
-  __syncwarp();
-}
-
 // sim.hpp:319-329
 __device__ void advance_job(Ctx& c, DJob& j) {
   const int64_t dt = c.now - j.last_update_us;
@@ -225,7 +243,7 @@ __device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
     if (j.first_progress_us < 0) j.first_progress_us = c.now;
     if (c.first_progress < 0) c.first_progress = c.now;
   }
-  set_prog_bit(c, ji, progressing(phase) && !(j.flags & kDone));
+  c.rate_eff[ji] = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
   c.stp_dirty = true;
 }
 
@@ -239,52 +257,37 @@ __device__ void schedule_completion(Ctx& c, int ji) {
   push_event(c, ji, c.now + dt, 0, kEvCompletion);
 }
 
-// sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). The
-// progressing set is a bitmask; lanes compact the rates into scratch in index order (warp
-// scan), then the FP64 sum runs sequentially in that order, exactly as the reference's loop.
+// sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). Only
+// jobs in [stp_lo, n_arrived) can progress; rate_eff holds 0.0 for the others, and s + 0.0 == s
+// for the non-negative partial sums, so the sequential FP64 sum over that window is
+// bit-identical to the reference's loop over all jobs.
 __device__ void refresh_stp(Ctx& c) {
   if (!c.stp_dirty) return;
   c.stp_dirty = false;
-  const int nw = (c.J + 31) >> 5;
-  const int lane = lane_id();
-  int base = 0;
-  for (int w0 = 0; w0 < nw; w0 += 32) {
-    const int wi = w0 + lane;
-    uint32_t word = wi < nw ? c.prog_mask[wi] : 0u;
-    const int cnt = __popc(word);
-    int incl = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += y;
-    }
-    int k = base + incl - cnt;
-    while (word) {
-      const int b = __ffs(word) - 1;
-      word &= word - 1;
-      c.scratch[k++] = c.jobs[(wi << 5) + b].rate;
-    }
-    base += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  __syncwarp();
+  const double* r = c.rate_eff;
+  const int hi = c.n_arrived;
   double s = 0.0;
-  int i = 0;
-  for (; i + 4 <= base; i += 4) {
-    const double a0 = c.scratch[i], a1 = c.scratch[i + 1], a2 = c.scratch[i + 2],
-                 a3 = c.scratch[i + 3];
+  int i = c.stp_lo;
+  for (; i + 8 <= hi; i += 8) {
+    const double a0 = r[i], a1 = r[i + 1], a2 = r[i + 2], a3 = r[i + 3], a4 = r[i + 4],
+                 a5 = r[i + 5], a6 = r[i + 6], a7 = r[i + 7];
     s = s + a0;
     s = s + a1;
     s = s + a2;
     s = s + a3;
+    s = s + a4;
+    s = s + a5;
+    s = s + a6;
+    s = s + a7;
   }
-  for (; i < base; ++i) s = s + c.scratch[i];
-  __syncwarp();
+  for (; i < hi; ++i) s = s + r[i];
   if (s != c.stp_cur) {
     c.stp_cur = s;
-    if (c.stp_series && c.stp_points < c.stp_cap && lane == 0) {
+    if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
       c.stp_series[2 * c.stp_points] = s_from_us(c.now);
       c.stp_series[2 * c.stp_points + 1] = s;
     }
+    __syncwarp();
     ++c.stp_points;
   }
 }
@@ -737,8 +740,9 @@ __device__ void on_completion(Ctx& c, int ji) {
   j.flags |= kDone;
   ++j.epoch;
   clear_slot(c, ji);
-  set_prog_bit(c, ji, false);
+  c.rate_eff[ji] = 0.0;
   c.stp_dirty = true;
+  while (c.stp_lo < c.n_arrived && (c.jobs[c.stp_lo].flags & kDone)) ++c.stp_lo;
   j.completion_us = c.now;
   ++c.done_count;
   if (c.now > c.last_completion) c.last_completion = c.now;
@@ -766,6 +770,7 @@ __device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
   if (slot < c.J) {
     const int ji = slot;
     if (kind == kEvArrival) {
+      if (ji + 1 > c.n_arrived) c.n_arrived = ji + 1;
       log_rec(c, kLogArrival, -1, ji, 0, 0, 0, 0);
       enqueue(c, ji);
     } else if (kind == kEvCompletion) {
@@ -803,8 +808,13 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   c.gpus = reinterpret_cast<DGpu*>(ws + sim_ws_gpus_off(b.max_jobs));
   c.slots = reinterpret_cast<Slot*>(ws + sim_ws_slots_off(b.max_jobs, G));
   c.queue = reinterpret_cast<int32_t*>(ws + sim_ws_queue_off(b.max_jobs, G));
-  c.prog_mask = reinterpret_cast<uint32_t*>(ws + sim_ws_mask_off(b.max_jobs, G));
-  c.scratch = reinterpret_cast<double*>(ws + sim_ws_scratch_off(b.max_jobs, G));
+  c.rate_eff = reinterpret_cast<double*>(ws + sim_ws_scratch_off(b.max_jobs, G));
+  c.stp_lo = 0;
+  c.n_arrived = 0;
+  c.lmin_t = kNoEvent;
+  c.lmin_pk = ~0ull;
+  c.lmin_idx = -1;
+  c.lmin_valid = false;
   c.log = b.log ? b.log + size_t(warp) * b.log_cap : nullptr;
   c.log_cap = b.log_cap;
   c.log_n = 0;
@@ -880,7 +890,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
     g.spare = 4;
     c.slots[J + gi].t = kNoEvent;
   }
-  for (int i = lane; i < ((J + 31) >> 5); i += 32) c.prog_mask[i] = 0;
+  for (int i = lane; i < J; i += 32) c.rate_eff[i] = 0.0;
   __syncwarp();
   c.seq = static_cast<uint64_t>(J);
   bool bad_job = false;
