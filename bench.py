@@ -260,56 +260,66 @@ def bench_c3(args):
 
 
 def bench_c4(args):
-    """Config 4: cluster simulation, 100 GPUs, 1000-job Poisson traces (lambda 10 s), miso
-    policy with the noisy predictor (0.017, rng_seed = trace seed), default overheads; seeds
-    0..S-1 in one launch (one warp per seed). Secondary measurement: seeds/s and events/s,
-    beside the reference's run_simulation on every host thread."""
+    """Config 4 (BASELINE.json configs[3]): 100 GPUs, 1000-job Poisson traces (lambda 10 s),
+    seeds 0..S-1, default overheads; per trial the reference's run_trial_unit policy set:
+    nopart, optsta with best_static_partition (36 candidate simulations per trace) and miso
+    (noisy predictor 0.017, rng_seed = seed); JCT normalised by the same trial's nopart.
+    Everything runs on the device in three launches (one warp per simulation). Secondary
+    measurement: trials/s beside the reference's trial on every host thread."""
     import torch
     import paper_2207_11428_b200 as miso
     from concurrent.futures import ThreadPoolExecutor
     ctx = miso.Context(0)
     S = args.seeds
     traces = [miso.generate_trace(s, 1000, lambda_s=10.0) for s in range(S)]
-    opts = miso.SimOptions(policy="miso", cluster_size=100, predictor="noisy")
+
+    def trial_batch():
+        nop = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="nopart", cluster_size=100))
+        st = miso.best_static_partition(ctx, traces, cluster_size=100)
+        mis = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="miso", cluster_size=100,
+                                                               predictor="noisy"))
+        return nop, st, mis
+
     for _ in range(max(1, args.warmup)):
-        res = miso.simulate_batch(ctx, traces, opts)
+        trial_batch()
     times = []
     for _ in range(args.steps):
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        res = miso.simulate_batch(ctx, traces, opts)
-        b.record()
+        t0 = time.perf_counter()
+        nop, st, mis = trial_batch()
         torch.cuda.synchronize()
-        times.append(a.elapsed_time(b))
-    ms = statistics.median(times)
-    ev = int(res.metrics["events"].sum())
-    ok = int((res.metrics["status"] == 0).sum())
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    j_nop = nop.metrics["avg_jct_s"]
+    j_sta = np.array([tab[e] for e, tab in st])
+    j_mis = mis.metrics["avg_jct_s"]
+    ev = int(mis.metrics["events"].sum())
     cpu = None
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib
+    check = None
     if oracle_lib.have_ref() and not args.no_cpu_baseline:
         ref = oracle_lib.Ref()
         threads = oracle_lib.host_threads()
-        k = min(S, 2 * threads)
-
-        def one(s):
-            t = traces[s]
-            ref.simulate_trace(t.arrival_s, t.duration_s, t.speeds5, t.mem_gb, None, seed=s,
-                               cluster_size=100, policy=3, noisy=True, rng_seed=s)
+        k = min(S, threads)
         t0 = time.perf_counter()
         with ThreadPoolExecutor(threads) as ex:
-            list(ex.map(one, range(k)))
-        dt = time.perf_counter() - t0
-        cpu = {"value": k / dt, "unit": "seeds/s", "cores": threads, "kind": "reference",
-               "sample": f"{k} seeds, miso policy, {threads} threads"}
-    print(json.dumps({"metric": "cluster-simulation seeds/sec (config 4, miso, 100 GPUs x 1000 jobs)",
-                      "value": S / (ms / 1e3), "unit": "seeds/s", "ms_per_step": ms,
-                      "events_per_s": ev / (ms / 1e3), "events_per_seed": ev / S,
-                      "seeds": S, "seeds_ok": ok, "steps": args.steps, "warmup": args.warmup,
+            outs = list(ex.map(lambda s: ref.trial(s), range(k)))
+        cdt = time.perf_counter() - t0
+        cpu = {"value": k / cdt, "unit": "trials/s", "cores": threads, "kind": "reference",
+               "sample": f"{k} trials (nopart + best static search + optsta + miso), {threads} threads"}
+        got = np.stack([j_nop[:k], j_sta[:k], j_mis[:k]], 1)
+        want = np.stack([o for _, o in outs])
+        check = {"trials_compared": k, "avg_jct_bit_equal": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64))),
+                 "static_entry_equal": bool(all(e == st[i][0] for i, (e, _) in enumerate(outs)))}
+    print(json.dumps({"metric": "cluster-simulation trials/sec (config 4: nopart + optsta(best static) + miso, 100 GPUs x 1000 jobs)",
+                      "value": S / dt, "unit": "trials/s", "s_per_step": dt, "seeds": S,
+                      "simulations_per_step": int(S * 2 + sum(np.isfinite(t).sum() for _, t in st)),
+                      "miso_events_per_seed": ev / S, "steps": args.steps, "warmup": args.warmup,
                       "dtype": "f64", "data": "synthetic (generate_trace seeds 0..S-1)",
-                      "mean_avg_jct_s": float(res.metrics["avg_jct_s"].mean()),
-                      "cpu_baseline": cpu}), flush=True)
+                      "median_jct_norm": {"optsta": float(np.median(j_sta / j_nop)),
+                                          "miso": float(np.median(j_mis / j_nop))},
+                      "parity": check, "cpu_baseline": cpu}), flush=True)
 
 
 def main():

@@ -126,8 +126,9 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
 
 /* ---- cluster simulator (kernel (c)) ------------------------------------------------------ */
 
-/* Policies (sim.hpp:42): nopart, oracle, miso. (optsta is not on the device yet.) */
+/* Policies (sim.hpp:42). */
 #define MISO_B200_POLICY_NOPART 0
+#define MISO_B200_POLICY_OPTSTA 1
 #define MISO_B200_POLICY_ORACLE 2
 #define MISO_B200_POLICY_MISO 3
 
@@ -184,6 +185,8 @@ typedef struct {
 #define MISO_B200_LOG_ASSIGN 9     /* follows PARTITION: job, x = slice kind */
 #define MISO_B200_LOG_COMPLETE 10
 #define MISO_B200_LOG_SHRINK 11
+#define MISO_B200_LOG_ADMIT_SLOT 12 /* optsta admit: x = slot */
+#define MISO_B200_LOG_MIGRATE 13    /* optsta migration: x = slice kind, a = slot */
 
 /* generate_trace (workload.hpp:97-114) on the host: dist 0 lognormal(sigma), 1 fixed(fixed_s),
  * 2 uniform(lo_s, hi_s). Arrays of job_count; speeds5 kind order 1g..7g. */
@@ -192,13 +195,19 @@ int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
                              double lo_s, double hi_s, double* arrival_s, double* duration_s,
                              double* speeds5, int* mem_gb);
 
-/* run_simulation (sim.hpp:976-979) for n_seeds independent traces at once, one warp per seed,
- * DEVICE pointers. Trace s owns jobs job_offsets[s]..job_offsets[s+1]-1 (arrival_s as in
+/* run_simulation (sim.hpp:976-979) for n_seeds independent tasks at once, one warp per task,
+ * DEVICE pointers. Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r owns
+ * jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in
  * TraceJob, converted with us_from_s on the device; must be non-decreasing with the first at 0,
  * sim.hpp:251-254; base duration s; truth speeds; memory GB; QoS kind or -1). rng_seed[s] seeds the noisy predictor (experiment.hpp:305 sets it to the trace
- * seed). Outputs: metrics[s]; optional job_jct_us (completion - arrival, -1 if unfinished),
- * event log (log_cap records per seed) and STP series (stp_cap (t, stp) pairs per seed). */
+ * seed). Policy optsta needs static_counts (5 per task: the static partition's per-kind counts,
+ * a feasible partition; SimOptions::static_partition, sim.hpp:86) -- one launch can evaluate
+ * every candidate of best_static_partition (sim.hpp:1031-1066) for many traces.
+ * Outputs: metrics[s]; optional job_jct_us (completion - arrival, -1 if unfinished; only with
+ * task_trace == NULL), event log (log_cap records per task) and STP series (stp_cap (t, stp)
+ * pairs per task). */
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                             const int32_t* task_trace, const uint8_t* static_counts,
                              const int32_t* job_offsets, const double* arrival_s,
                              const double* base_s, const double* speeds5, const uint8_t* mem_gb,
                              const int8_t* qos_kind, const uint64_t* rng_seed,

@@ -290,8 +290,9 @@ int64_t ref_simulate_trace(int job_count, const double* arrival_s, const double*
                            const double* speeds5, const int* mem_gb, const int* qos_kind,
                            uint64_t seed, int cluster_size, int policy, double mig_reconfig_s,
                            double checkpoint_restart_s, double mps_window_s, double interference,
-                           int noisy, double target_mae, uint64_t rng_seed, RefSimOut* out,
-                           char* log_buf, int64_t log_cap, double* stp_series, int64_t stp_cap) {
+                           int noisy, double target_mae, uint64_t rng_seed, int static_entry,
+                           RefSimOut* out, char* log_buf, int64_t log_cap, double* stp_series,
+                           int64_t stp_cap) {
   miso::JobTrace trace;
   trace.spec.job_count = job_count;
   trace.spec.seed = seed;
@@ -316,6 +317,7 @@ int64_t ref_simulate_trace(int job_count, const double* arrival_s, const double*
   opt.predictor.mode = noisy ? miso::PredictorSpec::Mode::noisy : miso::PredictorSpec::Mode::oracle;
   opt.predictor.target_mae = target_mae;
   opt.predictor.rng_seed = rng_seed;
+  if (static_entry >= 0) opt.static_partition = miso::default_catalog().entries[static_entry];
   std::ostringstream log;
   if (log_buf) opt.event_log = &log;
   miso::MetricsReport r;
@@ -350,6 +352,56 @@ int64_t ref_simulate_trace(int job_count, const double* arrival_s, const double*
   size_t n = std::min<size_t>(s.size(), static_cast<size_t>(log_cap));
   std::memcpy(log_buf, s.data(), n);
   return static_cast<int64_t>(s.size());
+}
+
+// best_static_partition (sim.hpp:1031-1066) on an explicit trace; table[36] avg JCT per entry.
+int ref_best_static(int job_count, const double* arrival_s, const double* duration_s,
+                    const double* speeds5, const int* mem_gb, int cluster_size,
+                    double mig_reconfig_s, double checkpoint_restart_s, double mps_window_s,
+                    double interference, double* table) {
+  miso::JobTrace trace;
+  trace.spec.job_count = job_count;
+  for (int i = 0; i < job_count; ++i) {
+    miso::TraceJob j;
+    j.arrival_s = arrival_s[i];
+    j.profile.job_id = "j" + std::to_string(i);
+    j.profile.base_duration_s = duration_s[i];
+    for (int k = 0; k < 5; ++k) j.profile.speed_table.v[k] = speeds5[5 * i + k];
+    j.profile.mem_demand_gb = mem_gb[i];
+    j.profile.mps_rates = {1.0, 0.7, 0.4};
+    trace.jobs.push_back(j);
+  }
+  miso::OverheadSpec o;
+  o.mig_reconfig_s = mig_reconfig_s;
+  o.checkpoint_restart_s = checkpoint_restart_s;
+  o.mps_window_s = mps_window_s;
+  o.interference = interference;
+  auto res = miso::best_static_partition(trace, cluster_size, o);
+  for (size_t e = 0; e < res.table.size(); ++e) table[e] = res.table[e].second;
+  return catalog_index(miso::default_catalog(), res.chosen);
+}
+
+// One trial of the config-4 experiment (experiment.hpp:299-360 run_trial_unit without the
+// file/JSON plumbing): generate_trace(seed) -> nopart, best_static_partition + optsta, miso
+// (noisy predictor, rng_seed = seed). out[0..2] = avg JCT nopart/optsta/miso; returns the
+// chosen static catalog index.
+int ref_trial(uint64_t seed, int job_count, double lambda_s, int cluster_size, double target_mae,
+              double* out) {
+  miso::TraceSpec spec;
+  spec.job_count = job_count;
+  spec.lambda_s = lambda_s;
+  spec.seed = seed;
+  auto trace = miso::generate_trace(spec);
+  miso::OverheadSpec o;
+  miso::PredictorSpec ps;
+  ps.mode = miso::PredictorSpec::Mode::noisy;
+  ps.target_mae = target_mae;
+  ps.rng_seed = seed;
+  out[0] = miso::run_simulation(trace, cluster_size, miso::Policy::nopart, o, ps).avg_jct_s;
+  auto st = miso::best_static_partition(trace, cluster_size, o);
+  out[1] = miso::run_simulation(trace, cluster_size, miso::Policy::optsta, o, ps, st.chosen).avg_jct_s;
+  out[2] = miso::run_simulation(trace, cluster_size, miso::Policy::miso, o, ps).avg_jct_s;
+  return catalog_index(miso::default_catalog(), st.chosen);
 }
 
 // Raw std::mt19937_64 draws of DetRng(seed) (common.hpp:85-119), for fixture generators.

@@ -393,6 +393,7 @@ int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
 static int64_t us_from_s_host(double s) { return static_cast<int64_t>(std::llround(s * 1e6)); }
 
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                             const int32_t* task_trace, const uint8_t* static_counts,
                              const int32_t* job_offsets, const double* arrival_s,
                              const double* base_s, const double* speeds5, const uint8_t* mem_gb,
                              const int8_t* qos_kind, const uint64_t* rng_seed,
@@ -403,8 +404,10 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
   if (n_seeds < 0) return fail(MISO_B200_E_INVALID, "n_seeds < 0");
   if (n_seeds == 0) return MISO_B200_OK;
   if (opt->policy != MISO_B200_POLICY_NOPART && opt->policy != MISO_B200_POLICY_ORACLE &&
-      opt->policy != MISO_B200_POLICY_MISO)
-    return fail(MISO_B200_E_INVALID, "policy must be nopart, oracle or miso (optsta: host only)");
+      opt->policy != MISO_B200_POLICY_MISO && opt->policy != MISO_B200_POLICY_OPTSTA)
+    return fail(MISO_B200_E_INVALID, "unknown policy");
+  if (opt->policy == MISO_B200_POLICY_OPTSTA && !static_counts)  // sim.hpp:208-209
+    return fail(MISO_B200_E_INVALID, "optsta requires a static partition");
   if (opt->cluster_size < 1 || opt->cluster_size > 32767)
     return fail(MISO_B200_E_INVALID, "cluster_size must be >= 1");
   // validate_overheads (sim.hpp:69-74), validate_predictor_spec (profiles.hpp:180-183)
@@ -418,12 +421,32 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
     return fail(MISO_B200_E_INVALID, "null buffer");
   DeviceGuard g(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // max jobs per seed (offsets are device memory: read them back once)
-  std::vector<int32_t> offs(size_t(n_seeds) + 1);
+  // max jobs per task (device arrays: read the index arrays back once)
+  int n_traces = n_seeds;
+  std::vector<int32_t> tt;
+  if (task_trace) {
+    tt.resize(size_t(n_seeds));
+    CUDA_TRY(cudaMemcpyAsync(tt.data(), task_trace, tt.size() * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    n_traces = 0;
+    for (int v : tt) {
+      if (v < 0) return fail(MISO_B200_E_INVALID, "negative task_trace entry");
+      n_traces = std::max(n_traces, v + 1);
+    }
+  }
+  std::vector<int32_t> offs(size_t(n_traces) + 1);
   CUDA_TRY(cudaMemcpyAsync(offs.data(), job_offsets, offs.size() * 4, cudaMemcpyDeviceToHost, s));
+  if (static_counts && opt->policy == MISO_B200_POLICY_OPTSTA) {
+    std::vector<uint8_t> sc(size_t(n_seeds) * 5);
+    CUDA_TRY(cudaMemcpyAsync(sc.data(), static_counts, sc.size(), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (int i = 0; i < n_seeds; ++i)
+      if (!feasible(&sc[size_t(i) * 5]))
+        return fail(MISO_B200_E_INVALID, "static partition of task " + std::to_string(i) + " is not feasible");
+  }
   CUDA_TRY(cudaStreamSynchronize(s));
   int max_jobs = 0;
-  for (int i = 0; i < n_seeds; ++i) {
+  for (int i = 0; i < n_traces; ++i) {
     const int J = offs[i + 1] - offs[i];
     if (J < 1) return fail(MISO_B200_E_INVALID, "trace has no jobs");  // sim.hpp:210
     max_jobs = std::max(max_jobs, J);
@@ -461,6 +484,8 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
   b.n_seeds = n_seeds;
   b.max_jobs = max_jobs;
   b.job_offsets = job_offsets;
+  b.task_trace = task_trace;
+  b.static_counts = static_counts;
   b.arrival_s = arrival_s;
   b.base_s = base_s;
   b.speeds5 = speeds5;

@@ -53,7 +53,8 @@ struct DJob {
   int16_t gpu;
   uint8_t phase, slice, mem, min_kind, flags;
   int8_t qos;
-  uint8_t pad[6];
+  int8_t slot;  // optsta slot index on its GPU
+  uint8_t pad[5];
 };
 
 struct DGpu {
@@ -66,7 +67,9 @@ struct DGpu {
   uint8_t part[5], plan_part[5], kind_cnt[5];
   int8_t spare;
   uint8_t plan_slice[7];
-  uint8_t pad[3];
+  uint8_t nslots;           // optsta: fixed slots of the static partition (sim.hpp:167-170)
+  uint8_t slot_kind[7];
+  int32_t slot_job[7];
 };
 
 static_assert(sizeof(DJob) <= kSimJobBytes, "workspace job stride");
@@ -102,7 +105,7 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   double* stp_series;  // optional (t_s, stp) pairs
   int64_t stp_cap;
   bool stp_dirty;
-  int repartitions, mps_sessions, done_count;
+  int repartitions, migrations, mps_sessions, done_count;
   int64_t first_progress, last_completion;
   int status;
   uint64_t processed;
@@ -612,6 +615,46 @@ __device__ int place_dynamic(Ctx& c, int ji) {
   return best;
 }
 
+// sim.hpp:495-520: largest free slot the job can use (ties: first in (gpu, slot) order)
+__device__ bool admit_optsta(Ctx& c, int ji) {
+  const DJob& j = c.jobs[ji];
+  int bg = -1, bi = -1, bk = -1;  // best gpu, slot, gpc
+  for (int gi = lane_id(); gi < c.G; gi += 32) {
+    const DGpu& g = c.gpus[gi];
+    for (int i = 0; i < g.nslots; ++i) {
+      if (g.slot_job[i] != -1 || !(true_rate(j, g.slot_kind[i]) > 0)) continue;
+      const int gp = kind_gpc(g.slot_kind[i]);
+      if (gp > bk) {
+        bk = gp;
+        bg = gi;
+        bi = i;
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const int og = __shfl_xor_sync(0xffffffffu, bg, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+    const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
+    if (ok > bk || (ok == bk && ok >= 0 && (og < bg || (og == bg && oi < bi)))) {
+      bg = og;
+      bi = oi;
+      bk = ok;
+    }
+  }
+  if (bg < 0) return false;
+  ++c.qhead;
+  DGpu& g = c.gpus[bg];
+  g.slot_job[bi] = ji;
+  roster_push(c, g, ji);
+  DJob& jm = c.jobs[ji];
+  jm.gpu = static_cast<int16_t>(bg);
+  jm.slot = static_cast<int8_t>(bi);
+  log_rec(c, kLogAdmitSlot, bg, ji, static_cast<uint8_t>(bi), 0, 0, 0);
+  start_running(c, ji, g.slot_kind[bi]);
+  return true;
+}
+
 // sim.hpp:465-478
 __device__ bool admit_nopart(Ctx& c, int ji) {
   int best = -1;
@@ -641,6 +684,11 @@ __device__ void drain_queue(Ctx& c) {
   if (c.p->policy == MISO_B200_POLICY_NOPART) {
     while (c.qhead < c.qtail && c.status == 0)
       if (!admit_nopart(c, c.queue[c.qhead])) break;
+    return;
+  }
+  if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
+    while (c.qhead < c.qtail && c.status == 0)
+      if (!admit_optsta(c, c.queue[c.qhead])) break;
     return;
   }
   for (;;) {
@@ -728,6 +776,81 @@ __device__ void complete_dynamic(Ctx& c, int gi, int ji) {
   reopt_and_apply(c, gi, false);
 }
 
+// sim.hpp:526-572: one migration per freed slot -- the running job with the largest strictly
+// positive true-speed gain on a strictly larger slot kind (ties: earliest arrival, then entry
+// order) moves in and checkpoint-restarts; its old slot joins the worklist. The job scan is a
+// warp argmin over the window of arrived, unfinished jobs.
+__device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
+  int wl_g[64], wl_s[64];
+  int nw = 1;
+  wl_g[0] = gi0;
+  wl_s[0] = si0;
+  while (nw > 0 && c.status == 0) {
+    --nw;
+    const int gi = wl_g[nw], si = wl_s[nw];
+    drain_queue(c);
+    DGpu& g = c.gpus[gi];
+    if (g.slot_job[si] != -1) continue;
+    const int kind = g.slot_kind[si];
+    const int kg = kind_gpc(kind);
+    int best = -1;
+    double bgain = 0.0;
+    int64_t barr = 0;
+    for (int mi = c.stp_lo + lane_id(); mi < c.n_arrived; mi += 32) {
+      const DJob& m = c.jobs[mi];
+      if ((m.flags & kDone) || m.phase != kRunning) continue;
+      if (kind_gpc(m.slice) >= kg) continue;
+      const double ns = true_rate(m, kind);
+      if (!(ns > 0)) continue;
+      const double gain = ns - m.rate;
+      if (gain <= 0) continue;
+      if (best < 0 || gain > bgain || (gain == bgain && (m.arrival_us < barr ||
+                                                         (m.arrival_us == barr && mi < best)))) {
+        best = mi;
+        bgain = gain;
+        barr = m.arrival_us;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const double og = __shfl_xor_sync(0xffffffffu, bgain, off);
+      const int64_t oa = __shfl_xor_sync(0xffffffffu, barr, off);
+      if (ob >= 0 && (best < 0 || og > bgain ||
+                      (og == bgain && (oa < barr || (oa == barr && ob < best))))) {
+        best = ob;
+        bgain = og;
+        barr = oa;
+      }
+    }
+    if (best < 0) continue;
+    DJob& m = c.jobs[best];
+    DGpu& og = c.gpus[m.gpu];
+    og.slot_job[m.slot] = -1;
+    if (nw == 64) {
+      fail(c, MISO_B200_SIM_INVARIANT);
+      return;
+    }
+    wl_g[nw] = m.gpu;
+    wl_s[nw] = m.slot;
+    ++nw;
+    roster_erase(c, og, best);
+    roster_push(c, g, best);
+    g.slot_job[si] = best;
+    m.gpu = static_cast<int16_t>(gi);
+    m.slot = static_cast<int8_t>(si);
+    m.slice = static_cast<uint8_t>(kind);
+    ++c.migrations;
+    log_rec(c, kLogMigrate, gi, best, static_cast<uint8_t>(kind), static_cast<uint32_t>(si), 0, 0);
+    if (c.p->ckpt_us > 0) {
+      set_phase(c, best, kCkpt, 0.0);
+      push_event(c, best, c.now + c.p->ckpt_us, 2, kEvCkptDone);
+    } else {
+      start_running(c, best, m.slice);
+    }
+  }
+}
+
 // sim.hpp:798-835
 __device__ void on_completion(Ctx& c, int ji) {
   DJob& j = c.jobs[ji];
@@ -762,6 +885,11 @@ __device__ void on_completion(Ctx& c, int ji) {
     g.mode = kGpuIdle;
     return;
   }
+  if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
+    g.slot_job[j.slot] = -1;
+    process_freed_slots(c, gi, j.slot);
+    return;
+  }
   complete_dynamic(c, gi, ji);
 }
 
@@ -775,6 +903,8 @@ __device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
       enqueue(c, ji);
     } else if (kind == kEvCompletion) {
       on_completion(c, ji);
+    } else if (kind == kEvCkptDone) {  // on_migration_restart, sim.hpp:574
+      start_running(c, ji, c.jobs[ji].slice);
     }
     return;
   }
@@ -799,8 +929,9 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (warp >= b.n_seeds) return;
   const int lane = lane_id();
-  const int J0 = b.job_offsets[warp];
-  const int J = b.job_offsets[warp + 1] - J0;
+  const int tr = b.task_trace ? b.task_trace[warp] : warp;  // task -> trace
+  const int J0 = b.job_offsets[tr];
+  const int J = b.job_offsets[tr + 1] - J0;
   const int G = prm.cluster_size;
   unsigned char* ws = b.workspace + size_t(warp) * b.ws_stride;
   Ctx c;
@@ -831,14 +962,14 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   c.stp_last = 0;
   c.stp_points = 0;
   c.stp_dirty = false;
-  c.repartitions = c.mps_sessions = c.done_count = 0;
+  c.repartitions = c.migrations = c.mps_sessions = c.done_count = 0;
   c.first_progress = -1;
   c.last_completion = -1;
   c.status = 0;
   c.processed = 0;
   c.p = &prm;
   c.spare_lut = b.spare_lut;
-  c.rng_seed = b.rng_seed[warp];
+  c.rng_seed = b.rng_seed[warp];  // per task
   c.w = w;
 
   // ---- init_jobs / init_gpus (sim.hpp:240-276), lanes in parallel ----
@@ -871,6 +1002,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
       if (kind_mem_gb(k) >= j.mem && kind_gpc(k) >= qg) mk = k;
     j.min_kind = static_cast<uint8_t>(mk < 0 ? 0xFF : mk);
     j.flags = 0;
+    j.slot = -1;
     Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
     s.t = a;
     s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
@@ -888,6 +1020,18 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
     g.plan_valid = 0;
     for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k] = g.kind_cnt[k] = 0;
     g.spare = 4;
+    g.nslots = 0;
+    if (prm.policy == MISO_B200_POLICY_OPTSTA) {  // init_gpus, sim.hpp:266-276
+      const uint8_t* sc = b.static_counts + size_t(warp) * 5;
+      for (int k = 4; k >= 0; --k)
+        for (int r = 0; r < sc[k]; ++r) {
+          g.slot_kind[g.nslots] = static_cast<uint8_t>(k);
+          g.slot_job[g.nslots] = -1;
+          ++g.nslots;
+        }
+      for (int k = 0; k < 5; ++k) g.part[k] = sc[k];
+      g.mode = kGpuMig;
+    }
     c.slots[J + gi].t = kNoEvent;
   }
   for (int i = lane; i < J; i += 32) c.rate_eff[i] = 0.0;
@@ -897,7 +1041,8 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   for (int i = 0; i < J; ++i) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
 
   // ---- event loop (sim.hpp:221-233) ----
-  if (bad_job && prm.policy != MISO_B200_POLICY_NOPART) c.status = MISO_B200_SIM_INVARIANT;
+  if (bad_job && (prm.policy == MISO_B200_POLICY_MISO || prm.policy == MISO_B200_POLICY_ORACLE))
+    c.status = MISO_B200_SIM_INVARIANT;
   while (c.status == 0) {
     Slot ev;
     const int slot = next_event(c, &ev);
@@ -924,7 +1069,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   m.completed_count = c.done_count;
   m.completed = c.done_count == J;
   m.repartitions = c.repartitions;
-  m.migrations = 0;
+  m.migrations = c.migrations;
   m.mps_sessions = c.mps_sessions;
   m.events = static_cast<int64_t>(c.processed);
   m.log_records = c.log_n;
@@ -933,7 +1078,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   double jct_sum = 0;
   for (int i = 0; i < J; ++i) {
     const DJob& j = c.jobs[i];
-    if (b.job_jct_us && lane == 0) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
+    if (b.job_jct_us && !b.task_trace && lane == 0) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
     if (!(j.flags & kDone)) continue;
     jct_sum += s_from_us(j.completion_us - j.arrival_us);
 #pragma unroll

@@ -17,6 +17,7 @@ enum LogKind : uint8_t {
   kLogMpsEnd = MISO_B200_LOG_MPS_END, kLogReconfigStart = MISO_B200_LOG_RECONFIG_START,
   kLogPartition = MISO_B200_LOG_PARTITION, kLogAssign = MISO_B200_LOG_ASSIGN,
   kLogComplete = MISO_B200_LOG_COMPLETE, kLogShrink = MISO_B200_LOG_SHRINK,
+  kLogAdmitSlot = MISO_B200_LOG_ADMIT_SLOT, kLogMigrate = MISO_B200_LOG_MIGRATE,
 };
 
 struct SimParams {
@@ -29,7 +30,9 @@ struct SimParams {
 
 struct SimBatch {
   int n_seeds, max_jobs;
-  const int32_t* job_offsets;
+  const int32_t* job_offsets;   // per trace
+  const int32_t* task_trace;    // per task (nullable: task i = trace i)
+  const uint8_t* static_counts; // per task, optsta static partition
   const double* arrival_s;
   const double* base_s;
   const double* speeds5;
@@ -49,7 +52,7 @@ struct SimBatch {
 
 // Per-seed workspace layout: [jobs][gpus][slots][queue][progress mask][rate scratch]
 constexpr size_t kSimJobBytes = 216;
-constexpr size_t kSimGpuBytes = 192;
+constexpr size_t kSimGpuBytes = 256;
 __host__ __device__ inline size_t sim_al(size_t x) { return (x + 127) & ~size_t(127); }
 __host__ __device__ inline size_t sim_ws_gpus_off(int J) { return sim_al(size_t(J) * kSimJobBytes); }
 __host__ __device__ inline size_t sim_ws_slots_off(int J, int G) {

@@ -17,7 +17,7 @@ import numpy as np
 from ._native import Context, _check, lib
 from .catalog import KIND_NAMES, partition_name
 
-POLICIES = {"nopart": 0, "oracle": 2, "miso": 3}
+POLICIES = {"nopart": 0, "optsta": 1, "oracle": 2, "miso": 3}
 
 
 class SimOptionsC(C.Structure):
@@ -58,7 +58,7 @@ lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_do
                                          C.c_double, C.c_double, C.c_double, C.c_double,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
-    [C.c_void_p] * 10 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
+    [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
 
 
 @dataclass
@@ -129,13 +129,17 @@ class SimResult:
 
 def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
                    rng_seeds: Optional[Sequence[int]] = None, log_cap: int = 0,
-                   stp_cap: int = 0, want_jct: bool = False, stream=None) -> SimResult:
-    """run_simulation for every trace at once (device). rng_seeds default to each trace's seed
-    (experiment.hpp:305)."""
+                   stp_cap: int = 0, want_jct: bool = False, stream=None,
+                   task_trace: Optional[Sequence[int]] = None,
+                   static_partitions: Optional[Sequence[Sequence[int]]] = None) -> SimResult:
+    """run_simulation for every task at once (device), one warp per task. By default task i
+    simulates traces[i]; with task_trace, task t simulates traces[task_trace[t]] (one launch
+    can replay a trace under many static partitions). rng_seeds (per task) default to the
+    trace's seed (experiment.hpp:305). static_partitions: per-task kind counts (optsta)."""
     import torch
     dev = torch.device("cuda", ctx.device)
-    S = len(traces)
-    offs = np.zeros(S + 1, np.int32)
+    S = len(traces) if task_trace is None else len(task_trace)
+    offs = np.zeros(len(traces) + 1, np.int32)
     offs[1:] = np.cumsum([t.n for t in traces])
     cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
     arr = cat(lambda t: t.arrival_s, np.float64)
@@ -143,10 +147,17 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     sp = cat(lambda t: t.speeds5, np.float64)
     mem = cat(lambda t: t.mem_gb, np.uint8)
     qos = cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8)
-    seeds = np.asarray(rng_seeds if rng_seeds is not None else [t.seed for t in traces], np.uint64)
+    if rng_seeds is None:
+        rng_seeds = [traces[i if task_trace is None else task_trace[i]].seed for i in range(S)]
+    seeds = np.asarray(rng_seeds, np.uint64)
     T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
     d_offs, d_arr, d_dur, d_sp = T(offs, None), T(arr, None), T(dur, None), T(sp, None)
     d_mem, d_qos, d_seed = T(mem, None), T(qos, None), T(seeds.view(np.int64), None)
+    d_tt = None if task_trace is None else T(np.asarray(task_trace, np.int32), None)
+    if opts.policy == "optsta" and static_partitions is None:
+        raise ValueError("optsta requires a static partition")  # sim.hpp:208-209
+    d_sc = None if static_partitions is None else \
+        T(np.asarray(static_partitions, np.uint8).reshape(S, 5), None)
     d_met = torch.empty(S * METRICS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     d_jct = torch.empty(int(offs[-1]), dtype=torch.int64, device=dev) if want_jct else None
     d_log = torch.empty(S * log_cap * 32, dtype=torch.uint8, device=dev) if log_cap else None
@@ -154,7 +165,8 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     o = opts.to_c()
     p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    _check(lib.miso_b200_simulate_batch(ctx._h, C.byref(o), S, p(d_offs), p(d_arr), p(d_dur),
+    _check(lib.miso_b200_simulate_batch(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+                                        p(d_arr), p(d_dur),
                                         p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
                                         p(d_jct), p(d_log), log_cap, p(d_stp), stp_cap, s))
     torch.cuda.synchronize(dev)
@@ -162,7 +174,7 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     res = SimResult(met, traces=list(traces))
     if want_jct:
         j = d_jct.cpu().numpy()
-        res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(S)]
+        res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(len(traces))]
     if log_cap:
         lg = d_log.cpu().numpy().view(LOG_DTYPE).reshape(S, log_cap)
         res.logs = [lg[i, : min(log_cap, int(met[i]["log_records"]))] for i in range(S)]
@@ -221,11 +233,68 @@ def render_log(records: np.ndarray, job_ids=None) -> str:
             line = f"complete job={jid(j)} jct_us={a | (b << 32)}"
         elif k == 11:
             line = f"shrink gpu={g} shape={partition_name(_counts(a))}"
+        elif k == 12:
+            line = f"admit gpu={g} job={jid(j)} slot={int(r['x'])}"
+        elif k == 13:
+            line = f"migrate job={jid(j)} gpu={g} slot={a} slice={KIND_NAMES[int(r['x'])]}"
         else:
             line = f"?kind={k}"
         out.append(f"{t} {line}\n")
         i += 1
     return "".join(out)
+
+
+def min_kind(mem_gb: int, qos_kind=None):
+    """min_slice_for (topology.hpp:68-72) of a job; None if no kind fits."""
+    from .catalog import GPC, MEM_GB
+    q = GPC[qos_kind] if qos_kind is not None and qos_kind >= 0 else 0
+    for k in range(5):
+        if MEM_GB[k] >= mem_gb and GPC[k] >= q:
+            return k
+    return None
+
+
+def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: int,
+                          overheads: Optional[SimOptions] = None, catalog=None):
+    """best_static_partition (sim.hpp:1031-1066) for many traces in ONE launch: every
+    (trace, candidate partition) pair is an independent optsta simulation (one warp each).
+    Returns per trace (chosen catalog index, table of avg JCT per entry; inf = skipped or
+    incomplete). Raises ValueError (InfeasibleError) if a job fits no slice kind or no
+    partition can host the trace."""
+    from .catalog import DEFAULT_CATALOG
+    cat = list(catalog if catalog is not None else DEFAULT_CATALOG)
+    base = overheads or SimOptions()
+    opts = SimOptions(policy="optsta", cluster_size=cluster_size,
+                      mig_reconfig_s=base.mig_reconfig_s,
+                      checkpoint_restart_s=base.checkpoint_restart_s,
+                      mps_window_s=base.mps_window_s, interference=base.interference,
+                      check_invariants=base.check_invariants, max_events=base.max_events)
+    tasks, parts = [], []
+    for ti, t in enumerate(traces):
+        qos = t.qos_kind if t.qos_kind is not None else [None] * t.n
+        kinds = [min_kind(int(mm), None if q is None or q < 0 else int(q)) for mm, q in zip(t.mem_gb, qos)]
+        if any(k is None for k in kinds):
+            raise ValueError(f"trace {ti}: a job fits no slice kind")
+        need = max(kinds)
+        for e, counts in enumerate(cat):
+            largest = max(k for k in range(5) if counts[k] > 0)
+            if largest >= need:
+                tasks.append((ti, e))
+                parts.append(counts)
+    res = simulate_batch(ctx, traces, opts, task_trace=[t for t, _ in tasks], static_partitions=parts)
+    out = []
+    table = np.full((len(traces), len(cat)), np.inf)
+    for i, (ti, e) in enumerate(tasks):
+        table[ti, e] = res.metrics[i]["avg_jct_s"]
+    for ti in range(len(traces)):
+        best, chosen = np.inf, -1
+        for e in range(len(cat)):  # strict <, first wins (sim.hpp:1058)
+            if table[ti, e] < best:
+                best, chosen = table[ti, e], e
+        if chosen < 0:
+            raise ValueError(f"trace {ti}: no static partition can host this trace")
+        out.append((chosen, table[ti]))
+    return out
 
 
 def _simulate(self, traces, opts=None, **kw):

@@ -158,8 +158,12 @@ class Ref:
         _ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
         L.ref_simulate_trace.argtypes = [C.c_int, _dp, _dp, _dp, _ip, _ip, C.c_uint64, C.c_int,
                                          C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
-                                         C.c_int, C.c_double, C.c_uint64, C.POINTER(RefSimOut),
-                                         C.c_char_p, C.c_int64, C.c_void_p, C.c_int64]
+                                         C.c_int, C.c_double, C.c_uint64, C.c_int,
+                                         C.POINTER(RefSimOut), C.c_char_p, C.c_int64, C.c_void_p,
+                                         C.c_int64]
+        L.ref_trial.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_int, C.c_double, _dp]
+        L.ref_best_static.argtypes = [C.c_int, _dp, _dp, _dp, _ip, C.c_int, C.c_double, C.c_double,
+                                      C.c_double, C.c_double, _dp]
         L.ref_simulate_trace.restype = C.c_int64
         L.ref_rng_raw.argtypes = [C.c_uint64, C.c_size_t, np.ctypeslib.ndpointer(np.uint64)]
         L.ref_c1_chain.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_uint64,
@@ -221,7 +225,7 @@ class Ref:
     def simulate_trace(self, arrival_s, duration_s, speeds5, mem_gb, qos_kind=None, seed=0,
                        cluster_size=8, policy=3, mig_reconfig_s=4.0, checkpoint_restart_s=30.0,
                        mps_window_s=10.0, interference=0.8, noisy=True, target_mae=0.017,
-                       rng_seed=0, want_log=False, log_cap=1 << 26, stp_cap=0):
+                       rng_seed=0, want_log=False, log_cap=1 << 26, stp_cap=0, static_entry=-1):
         n = len(arrival_s)
         qos = np.full(n, -1, np.int32) if qos_kind is None else np.asarray(qos_kind, np.int32)
         out = RefSimOut()
@@ -231,10 +235,27 @@ class Ref:
             n, np.ascontiguousarray(arrival_s, np.float64), np.ascontiguousarray(duration_s, np.float64),
             np.ascontiguousarray(speeds5, np.float64).reshape(-1), np.ascontiguousarray(mem_gb, np.int32),
             qos, seed, cluster_size, policy, mig_reconfig_s, checkpoint_restart_s, mps_window_s,
-            interference, int(noisy), target_mae, rng_seed, C.byref(out), buf,
+            interference, int(noisy), target_mae, rng_seed, static_entry, C.byref(out), buf,
             log_cap if want_log else 0, None if stp is None else stp.ctypes.data, stp_cap)
         log = buf.raw[: min(r, log_cap)].decode() if (want_log and r >= 0) else None
         return out, log, stp
+
+    def trial(self, seed, job_count=1000, lambda_s=10.0, cluster_size=100, target_mae=0.017):
+        out = np.zeros(3)
+        e = self.lib.ref_trial(seed, job_count, lambda_s, cluster_size, target_mae, out)
+        return e, out
+
+    def best_static(self, arrival_s, duration_s, speeds5, mem_gb, cluster_size=8,
+                    mig_reconfig_s=4.0, checkpoint_restart_s=30.0, mps_window_s=10.0,
+                    interference=0.8):
+        table = np.zeros(36)
+        e = self.lib.ref_best_static(len(arrival_s), np.ascontiguousarray(arrival_s, np.float64),
+                                     np.ascontiguousarray(duration_s, np.float64),
+                                     np.ascontiguousarray(speeds5, np.float64).reshape(-1),
+                                     np.ascontiguousarray(mem_gb, np.int32), cluster_size,
+                                     mig_reconfig_s, checkpoint_restart_s, mps_window_s,
+                                     interference, table)
+        return e, table
 
     def gen_trace(self, seed, job_count, lambda_s=60.0, max_duration_s=7200.0, sigma=1.5):
         arr = np.zeros(job_count); dur = np.zeros(job_count)

@@ -142,3 +142,37 @@ def test_invalid_sim_options(ctx):
         with pytest.raises(m.MisoError) as ei:
             m.simulate_batch(ctx, tr, m.SimOptions(**bad))
         assert ei.value.code == -2
+
+
+def test_optsta_event_log_parity(ctx, ref):
+    """optsta policy (sim.hpp:493-572): fixed slots, largest-free-slot admission and
+    small-to-large migrations with checkpoint restarts, byte-identical logs."""
+    import paper_2207_11428_b200 as m
+    from paper_2207_11428_b200.catalog import DEFAULT_CATALOG
+    traces = [m.generate_trace(seed, 120, lambda_s=30.0) for seed in (11, 12)]
+    for entry in (1, 8, 9, 24, 0):  # 4g+2g+1g, 3g+2g+2g, 3g+2g+1g+1g, 2g+1g*4, 7g
+        opts = m.SimOptions(policy="optsta", cluster_size=6)
+        res = m.simulate_batch(ctx, traces, opts, static_partitions=[DEFAULT_CATALOG[entry]] * 2,
+                               log_cap=1 << 15)
+        for i, tr in enumerate(traces):
+            want, wlog = ref.simulate_trace(tr.arrival_s, tr.duration_s, tr.speeds5, tr.mem_gb,
+                                            None, seed=tr.seed, cluster_size=6, policy=1,
+                                            noisy=False, rng_seed=tr.seed, static_entry=entry,
+                                            want_log=True)[:2]
+            assert m.render_log(res.logs[i]) == wlog, (entry, tr.seed)
+            got = res.report(i)
+            assert got["migrations"] == want.migrations
+            check_metrics(got, want)
+
+
+def test_best_static_partition_matches_reference(ctx, ref):
+    """best_static_partition (sim.hpp:1031-1066): all 36 candidates x 3 traces in one launch."""
+    import paper_2207_11428_b200 as m
+    traces = [m.generate_trace(seed, 150, lambda_s=20.0) for seed in (21, 22, 23)]
+    got = m.best_static_partition(ctx, traces, cluster_size=8)
+    for (entry, table), tr in zip(got, traces):
+        we, wt = ref.best_static(tr.arrival_s, tr.duration_s, tr.speeds5, tr.mem_gb, cluster_size=8)
+        assert entry == we
+        assert np.array_equal(np.isinf(table), np.isinf(wt))
+        fin = ~np.isinf(wt)
+        assert np.array_equal(table[fin].view(np.uint64), wt[fin].view(np.uint64))
