@@ -18,7 +18,11 @@ import numpy as np
 
 from .catalog import DEFAULT_CATALOG, KIND_NAMES, partition_name
 
-lib_path = Path(__file__).resolve().parent / "_lib" / "libmiso_b200.so"
+import os
+
+# MISO_B200_LIB selects an alternative in-tree build (tuning experiments only).
+lib_path = Path(os.environ.get("MISO_B200_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libmiso_b200.so")
 
 CAND_INFEASIBLE = 0xFF
 CAND_BAD_M = 0xFE

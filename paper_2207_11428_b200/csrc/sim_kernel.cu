@@ -70,6 +70,7 @@ struct DGpu {
   uint8_t nslots;           // optsta: fixed slots of the static partition (sim.hpp:167-170)
   uint8_t slot_kind[7];
   int32_t slot_job[7];
+  uint8_t fcnt[5];          // optsta: free slots per kind
 };
 
 static_assert(sizeof(DJob) <= kSimJobBytes, "workspace job stride");
@@ -86,12 +87,18 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   Slot* slots;          // [J job slots][G gpu slots]
   int32_t* queue;       // FCFS order (arrival_us, idx), qhead..qtail
   double* rate_eff;     // [J] rate if progressing and not done, else 0.0 (refresh_stp)
+  double* stp_prefix;   // [J] cached sequential partial sums of rate_eff over the window
+  int stp_cmin;         // smallest job index whose rate_eff changed since the last refresh
   int stp_lo, n_arrived; // jobs < stp_lo are done; jobs >= n_arrived have not arrived
   // per-lane minimum of the event slots this lane owns (slot % 32 == lane); lazily rescanned
   int64_t lmin_t;
   uint64_t lmin_pk;
   int lmin_idx;
   bool lmin_valid;
+  int chunk;            // slots per lane: lane l owns [l*chunk, (l+1)*chunk)
+  uint8_t* jst;         // [J] SoA job state for warp scans: phase | slice << 3 | done << 6
+  uint32_t* freemask;   // optsta: [5][W] bit g set iff GPU g has a free slot of that kind
+  int W;                // words per freemask row
   LogRec* log;
   int64_t log_cap, log_n;
   int J, G;
@@ -124,6 +131,10 @@ __device__ __forceinline__ int64_t us_from_s(double s) {  // llround: half away 
 }
 
 __device__ __forceinline__ bool progressing(uint8_t ph) { return ph == kMps || ph == kRunning; }
+
+__device__ __forceinline__ void sync_jst(Ctx& c, int ji, const DJob& j) {
+  c.jst[ji] = static_cast<uint8_t>(j.phase | (j.slice << 3) | ((j.flags & 2) ? 64 : 0));
+}
 
 __device__ __forceinline__ void fail(Ctx& c, int code) {
   if (c.status == 0) c.status = code;
@@ -161,7 +172,7 @@ __device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t
   s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
   ++c.seq;
   c.slots[slot] = s;
-  if ((slot & 31) == lane_id()) {  // owner lane keeps its minimum current
+  if (slot / c.chunk == lane_id()) {  // owner lane keeps its minimum current
     if (c.lmin_idx == slot) c.lmin_valid = false;
     else if (c.lmin_valid && (t < c.lmin_t || (t == c.lmin_t && s.pk < c.lmin_pk))) {
       c.lmin_t = t;
@@ -173,20 +184,28 @@ __device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t
 
 __device__ __forceinline__ void clear_slot(Ctx& c, int slot) {
   c.slots[slot].t = kNoEvent;
-  if ((slot & 31) == lane_id() && c.lmin_idx == slot) c.lmin_valid = false;
+  if (slot / c.chunk == lane_id() && c.lmin_idx == slot) c.lmin_valid = false;
 }
 
-// Next event = minimum live (t, prio, seq) key. Slot i is owned by lane i % 32, which keeps
-// the minimum of its slots in registers (updated on push, invalidated when that slot is
-// cleared or overwritten) and rescans its ~(J+G)/32 slots only when invalidated; the event is
-// then one warp argmin over the 32 lane minima.
+// Next event = minimum live (t, prio, seq) key. Lane l owns the contiguous slot chunk
+// [l*chunk, (l+1)*chunk) and keeps its minimum in registers (updated on push, invalidated when
+// that slot is cleared or overwritten). Invalid chunks are rescanned by the whole warp (one
+// coalesced load per lane + a warp argmin); the event is then one warp argmin over the 32
+// lane minima.
 __device__ int next_event(Ctx& c, Slot* out) {
   const int n = c.J + c.G;
-  if (!c.lmin_valid) {
+  const int lane = lane_id();
+  unsigned inval = __ballot_sync(0xffffffffu, !c.lmin_valid);
+  while (inval) {
+    const int owner = __ffs(inval) - 1;
+    inval &= inval - 1;
+    const int lo = owner * c.chunk;
+    int hi = lo + c.chunk;
+    if (hi > n) hi = n;
     int64_t bt = kNoEvent;
     uint64_t bk = ~0ull;
     int bi = -1;
-    for (int i = lane_id(); i < n; i += 32) {
+    for (int i = lo + lane; i < hi; i += 32) {
       const Slot s = c.slots[i];
       if (s.t < bt || (s.t == bt && s.pk < bk)) {
         bt = s.t;
@@ -194,10 +213,23 @@ __device__ int next_event(Ctx& c, Slot* out) {
         bi = i;
       }
     }
-    c.lmin_t = bt;
-    c.lmin_pk = bk;
-    c.lmin_idx = bi;
-    c.lmin_valid = true;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ot < bt || (ot == bt && ok < bk)) {
+        bt = ot;
+        bk = ok;
+        bi = oi;
+      }
+    }
+    if (lane == owner) {
+      c.lmin_t = bt;
+      c.lmin_pk = bk;
+      c.lmin_idx = bi;
+      c.lmin_valid = true;
+    }
   }
   __syncwarp();
   int64_t bt = c.lmin_t;
@@ -248,6 +280,8 @@ __device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
   }
   c.rate_eff[ji] = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
   c.stp_dirty = true;
+  if (ji < c.stp_cmin) c.stp_cmin = ji;
+  sync_jst(c, ji, j);
 }
 
 // sim.hpp:345-351
@@ -263,27 +297,41 @@ __device__ void schedule_completion(Ctx& c, int ji) {
 // sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). Only
 // jobs in [stp_lo, n_arrived) can progress; rate_eff holds 0.0 for the others, and s + 0.0 == s
 // for the non-negative partial sums, so the sequential FP64 sum over that window is
-// bit-identical to the reference's loop over all jobs.
+// bit-identical to the reference's loop over all jobs. Partial sums are cached per index and
+// the chain restarts at the smallest index changed since the previous refresh.
 __device__ void refresh_stp(Ctx& c) {
   if (!c.stp_dirty) return;
   c.stp_dirty = false;
   const double* r = c.rate_eff;
-  const int hi = c.n_arrived;
-  double s = 0.0;
-  int i = c.stp_lo;
+  double* P = c.stp_prefix;
+  const int lo = c.stp_lo, hi = c.n_arrived;
+  int i = c.stp_cmin > lo ? c.stp_cmin : lo;
+  c.stp_cmin = INT32_MAX;
+  double s = i > lo ? P[i - 1] : 0.0;
   for (; i + 8 <= hi; i += 8) {
     const double a0 = r[i], a1 = r[i + 1], a2 = r[i + 2], a3 = r[i + 3], a4 = r[i + 4],
                  a5 = r[i + 5], a6 = r[i + 6], a7 = r[i + 7];
-    s = s + a0;
-    s = s + a1;
-    s = s + a2;
-    s = s + a3;
-    s = s + a4;
-    s = s + a5;
-    s = s + a6;
-    s = s + a7;
+    double p0, p1, p2, p3, p4, p5, p6, p7;
+    p0 = s = s + a0;
+    p1 = s = s + a1;
+    p2 = s = s + a2;
+    p3 = s = s + a3;
+    p4 = s = s + a4;
+    p5 = s = s + a5;
+    p6 = s = s + a6;
+    p7 = s = s + a7;
+    if (lane_id() == 0) {
+      P[i] = p0; P[i + 1] = p1; P[i + 2] = p2; P[i + 3] = p3;
+      P[i + 4] = p4; P[i + 5] = p5; P[i + 6] = p6; P[i + 7] = p7;
+    }
   }
-  for (; i < hi; ++i) s = s + r[i];
+  for (; i < hi; ++i) {
+    s = s + r[i];
+    if (lane_id() == 0) P[i] = s;
+  }
+  __syncwarp();
+  if (hi <= lo) s = 0.0;
+  else s = P[hi - 1];
   if (s != c.stp_cur) {
     c.stp_cur = s;
     if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
@@ -357,7 +405,7 @@ __device__ void start_running(Ctx& c, int ji, int s) {
   const double r = true_rate(j, s);
   if (c.p->check_invariants && !(r > 0)) fail(c, MISO_B200_SIM_INFEASIBLE_SLICE);
   j.slice = static_cast<uint8_t>(s);
-  set_phase(c, ji, kRunning, r);
+  set_phase(c, ji, kRunning, r);  // also syncs jst
   schedule_completion(c, ji);
   log_rec(c, kLogStart, j.gpu, ji, static_cast<uint8_t>(s), 0, 0, r);
 }
@@ -615,37 +663,57 @@ __device__ int place_dynamic(Ctx& c, int ji) {
   return best;
 }
 
-// sim.hpp:495-520: largest free slot the job can use (ties: first in (gpu, slot) order)
+// optsta free-slot bookkeeping: per GPU and kind a free count, per kind a GPU bitmask.
+__device__ __forceinline__ void occupy_slot(Ctx& c, int gi, int i, int ji) {
+  DGpu& g = c.gpus[gi];
+  const int k = g.slot_kind[i];
+  g.slot_job[i] = ji;
+  if (--g.fcnt[k] == 0) {
+    uint32_t* w = c.freemask + k * c.W + (gi >> 5);
+    const uint32_t v = *w & ~(1u << (gi & 31));
+    __syncwarp();
+    *w = v;
+  }
+}
+
+__device__ __forceinline__ void free_slot(Ctx& c, int gi, int i) {
+  DGpu& g = c.gpus[gi];
+  const int k = g.slot_kind[i];
+  g.slot_job[i] = -1;
+  if (g.fcnt[k]++ == 0) {
+    uint32_t* w = c.freemask + k * c.W + (gi >> 5);
+    const uint32_t v = *w | (1u << (gi & 31));
+    __syncwarp();
+    *w = v;
+  }
+}
+
+// sim.hpp:495-520: the largest free slot the job can use, ties to the first (gpu, slot). Kinds
+// have distinct GPC counts, so this is: the largest feasible kind with a free slot anywhere,
+// on the lowest-numbered GPU having one, at that GPU's first free slot of the kind.
 __device__ bool admit_optsta(Ctx& c, int ji) {
   const DJob& j = c.jobs[ji];
-  int bg = -1, bi = -1, bk = -1;  // best gpu, slot, gpc
-  for (int gi = lane_id(); gi < c.G; gi += 32) {
-    const DGpu& g = c.gpus[gi];
-    for (int i = 0; i < g.nslots; ++i) {
-      if (g.slot_job[i] != -1 || !(true_rate(j, g.slot_kind[i]) > 0)) continue;
-      const int gp = kind_gpc(g.slot_kind[i]);
-      if (gp > bk) {
-        bk = gp;
-        bg = gi;
-        bi = i;
+  int bg = -1, bk = -1;
+  for (int k = 4; k >= 0 && bg < 0; --k) {
+    if (!(true_rate(j, k) > 0)) continue;
+    for (int w0 = 0; w0 < c.W && bg < 0; w0 += 32) {
+      const int wi = w0 + lane_id();
+      const uint32_t word = wi < c.W ? c.freemask[k * c.W + wi] : 0u;
+      const unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+      if (nz) {
+        const int l = __ffs(nz) - 1;
+        const uint32_t wv = __shfl_sync(0xffffffffu, word, l);
+        bg = ((w0 + l) << 5) + __ffs(wv) - 1;
+        bk = k;
       }
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const int og = __shfl_xor_sync(0xffffffffu, bg, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-    const int ok = __shfl_xor_sync(0xffffffffu, bk, off);
-    if (ok > bk || (ok == bk && ok >= 0 && (og < bg || (og == bg && oi < bi)))) {
-      bg = og;
-      bi = oi;
-      bk = ok;
-    }
-  }
   if (bg < 0) return false;
-  ++c.qhead;
   DGpu& g = c.gpus[bg];
-  g.slot_job[bi] = ji;
+  int bi = 0;
+  while (!(g.slot_kind[bi] == bk && g.slot_job[bi] == -1)) ++bi;
+  ++c.qhead;
+  occupy_slot(c, bg, bi, ji);
   roster_push(c, g, ji);
   DJob& jm = c.jobs[ji];
   jm.gpu = static_cast<int16_t>(bg);
@@ -797,9 +865,10 @@ __device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
     double bgain = 0.0;
     int64_t barr = 0;
     for (int mi = c.stp_lo + lane_id(); mi < c.n_arrived; mi += 32) {
+      const uint8_t st = c.jst[mi];  // coalesced SoA state; job records only for candidates
+      if ((st & 64) || (st & 7) != kRunning) continue;
+      if (kind_gpc((st >> 3) & 7) >= kg) continue;
       const DJob& m = c.jobs[mi];
-      if ((m.flags & kDone) || m.phase != kRunning) continue;
-      if (kind_gpc(m.slice) >= kg) continue;
       const double ns = true_rate(m, kind);
       if (!(ns > 0)) continue;
       const double gain = ns - m.rate;
@@ -826,7 +895,7 @@ __device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
     if (best < 0) continue;
     DJob& m = c.jobs[best];
     DGpu& og = c.gpus[m.gpu];
-    og.slot_job[m.slot] = -1;
+    free_slot(c, m.gpu, m.slot);
     if (nw == 64) {
       fail(c, MISO_B200_SIM_INVARIANT);
       return;
@@ -836,10 +905,11 @@ __device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
     ++nw;
     roster_erase(c, og, best);
     roster_push(c, g, best);
-    g.slot_job[si] = best;
+    occupy_slot(c, gi, si, best);
     m.gpu = static_cast<int16_t>(gi);
     m.slot = static_cast<int8_t>(si);
     m.slice = static_cast<uint8_t>(kind);
+    sync_jst(c, best, m);
     ++c.migrations;
     log_rec(c, kLogMigrate, gi, best, static_cast<uint8_t>(kind), static_cast<uint32_t>(si), 0, 0);
     if (c.p->ckpt_us > 0) {
@@ -865,6 +935,8 @@ __device__ void on_completion(Ctx& c, int ji) {
   clear_slot(c, ji);
   c.rate_eff[ji] = 0.0;
   c.stp_dirty = true;
+  if (ji < c.stp_cmin) c.stp_cmin = ji;
+  sync_jst(c, ji, j);
   while (c.stp_lo < c.n_arrived && (c.jobs[c.stp_lo].flags & kDone)) ++c.stp_lo;
   j.completion_us = c.now;
   ++c.done_count;
@@ -886,7 +958,7 @@ __device__ void on_completion(Ctx& c, int ji) {
     return;
   }
   if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
-    g.slot_job[j.slot] = -1;
+    free_slot(c, gi, j.slot);
     process_freed_slots(c, gi, j.slot);
     return;
   }
@@ -898,7 +970,10 @@ __device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
   if (slot < c.J) {
     const int ji = slot;
     if (kind == kEvArrival) {
-      if (ji + 1 > c.n_arrived) c.n_arrived = ji + 1;
+      if (ji + 1 > c.n_arrived) {
+        if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;  // new window entries need sums
+        c.n_arrived = ji + 1;
+      }
       log_rec(c, kLogArrival, -1, ji, 0, 0, 0, 0);
       enqueue(c, ji);
     } else if (kind == kEvCompletion) {
@@ -925,7 +1000,10 @@ __device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
 }
 
 // One warp per seed.
-__global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
+#ifndef MISO_SIM_MIN_BLOCKS
+#define MISO_SIM_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
   const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (warp >= b.n_seeds) return;
   const int lane = lane_id();
@@ -940,12 +1018,18 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
   c.slots = reinterpret_cast<Slot*>(ws + sim_ws_slots_off(b.max_jobs, G));
   c.queue = reinterpret_cast<int32_t*>(ws + sim_ws_queue_off(b.max_jobs, G));
   c.rate_eff = reinterpret_cast<double*>(ws + sim_ws_scratch_off(b.max_jobs, G));
+  c.stp_prefix = reinterpret_cast<double*>(ws + sim_ws_prefix_off(b.max_jobs, G));
+  c.jst = ws + sim_ws_jst_off(b.max_jobs, G);
+  c.freemask = reinterpret_cast<uint32_t*>(ws + sim_ws_freemask_off(b.max_jobs, G));
+  c.W = (G + 31) / 32;
+  c.stp_cmin = INT32_MAX;
   c.stp_lo = 0;
   c.n_arrived = 0;
   c.lmin_t = kNoEvent;
   c.lmin_pk = ~0ull;
   c.lmin_idx = -1;
   c.lmin_valid = false;
+  c.chunk = (J + G + 31) / 32;
   c.log = b.log ? b.log + size_t(warp) * b.log_cap : nullptr;
   c.log_cap = b.log_cap;
   c.log_n = 0;
@@ -1003,6 +1087,7 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
     j.min_kind = static_cast<uint8_t>(mk < 0 ? 0xFF : mk);
     j.flags = 0;
     j.slot = -1;
+    c.jst[i] = kQueued | (4 << 3);
     Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
     s.t = a;
     s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
@@ -1021,8 +1106,10 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
     for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k] = g.kind_cnt[k] = 0;
     g.spare = 4;
     g.nslots = 0;
+    for (int k = 0; k < 5; ++k) g.fcnt[k] = 0;
     if (prm.policy == MISO_B200_POLICY_OPTSTA) {  // init_gpus, sim.hpp:266-276
       const uint8_t* sc = b.static_counts + size_t(warp) * 5;
+      for (int k = 0; k < 5; ++k) g.fcnt[k] = sc[k];
       for (int k = 4; k >= 0; --k)
         for (int r = 0; r < sc[k]; ++r) {
           g.slot_kind[g.nslots] = static_cast<uint8_t>(k);
@@ -1035,6 +1122,16 @@ __global__ void __launch_bounds__(128) simulate_kernel(SimBatch b, SimParams prm
     c.slots[J + gi].t = kNoEvent;
   }
   for (int i = lane; i < J; i += 32) c.rate_eff[i] = 0.0;
+  for (int wi = lane; wi < 5 * c.W; wi += 32) {  // optsta: every GPU starts with all slots free
+    const int k = wi / c.W, w = wi % c.W;
+    const uint8_t* sc = b.static_counts ? b.static_counts + size_t(warp) * 5 : nullptr;
+    uint32_t v = 0;
+    if (prm.policy == MISO_B200_POLICY_OPTSTA && sc[k] > 0) {
+      const int nb = G - (w << 5);
+      v = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    }
+    c.freemask[wi] = v;
+  }
   __syncwarp();
   c.seq = static_cast<uint64_t>(J);
   bool bad_job = false;

@@ -67,8 +67,17 @@ __host__ __device__ inline size_t sim_ws_mask_off(int J, int G) {
 __host__ __device__ inline size_t sim_ws_scratch_off(int J, int G) {
   return sim_ws_mask_off(J, G) + sim_al(size_t((J + 31) / 32 + 32) * 4);
 }
-__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+__host__ __device__ inline size_t sim_ws_prefix_off(int J, int G) {
   return sim_ws_scratch_off(J, G) + sim_al(size_t(J + 32) * 8);
+}
+__host__ __device__ inline size_t sim_ws_jst_off(int J, int G) {
+  return sim_ws_prefix_off(J, G) + sim_al(size_t(J + 32) * 8);
+}
+__host__ __device__ inline size_t sim_ws_freemask_off(int J, int G) {
+  return sim_ws_jst_off(J, G) + sim_al(size_t(J + 32));
+}
+__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+  return sim_ws_freemask_off(J, G) + sim_al(size_t(5) * ((G + 31) / 32) * 4);
 }
 
 size_t sim_workspace_stride(int max_jobs, int cluster_size);

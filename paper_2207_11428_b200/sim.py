@@ -269,18 +269,21 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
                       checkpoint_restart_s=base.checkpoint_restart_s,
                       mps_window_s=base.mps_window_s, interference=base.interference,
                       check_invariants=base.check_invariants, max_events=base.max_events)
+    from .catalog import GPC, MEM_GB
+    mem_gb = np.array(MEM_GB)
+    gpc = np.array(GPC)
+    largest = np.array([max(k for k in range(5) if c[k] > 0) for c in cat])
     tasks, parts = [], []
     for ti, t in enumerate(traces):
-        qos = t.qos_kind if t.qos_kind is not None else [None] * t.n
-        kinds = [min_kind(int(mm), None if q is None or q < 0 else int(q)) for mm, q in zip(t.mem_gb, qos)]
-        if any(k is None for k in kinds):
+        qos = np.full(t.n, -1) if t.qos_kind is None else np.asarray(t.qos_kind)
+        qg = np.where(qos >= 0, gpc[np.maximum(qos, 0)], 0)
+        ok = (mem_gb[None, :] >= np.asarray(t.mem_gb)[:, None]) & (gpc[None, :] >= qg[:, None])
+        if not ok.any(axis=1).all():
             raise ValueError(f"trace {ti}: a job fits no slice kind")
-        need = max(kinds)
-        for e, counts in enumerate(cat):
-            largest = max(k for k in range(5) if counts[k] > 0)
-            if largest >= need:
-                tasks.append((ti, e))
-                parts.append(counts)
+        need = int(ok.argmax(axis=1).max())  # min_slice_for per job, then the largest
+        for e in np.nonzero(largest >= need)[0]:
+            tasks.append((ti, int(e)))
+            parts.append(cat[e])
     res = simulate_batch(ctx, traces, opts, task_trace=[t for t, _ in tasks], static_partitions=parts)
     out = []
     table = np.full((len(traces), len(cat)), np.inf)
