@@ -443,7 +443,7 @@ def main():
             "configs_scored_per_s": world * cands * K / (total_ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "optimize_tile_kernel", "kernel_ms": kern_ms,
+                         "kernel": "optimize_pipe_kernel", "kernel_ms": kern_ms,
                          "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
             "e2e": {"value": world * n * E / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": nb_s + nb_o, "d2h_bytes_per_step": n * 9,

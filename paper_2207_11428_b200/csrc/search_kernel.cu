@@ -161,7 +161,10 @@ struct PipeLayout {
   static constexpr size_t kBytes = kStageBytes * kS + 128;
 };
 
-template <int kT, int kS, int kCap, int kG, bool kAll>
+// kPos: nibble m = position of job count m's bucket in the sorted tile (identity = ascending
+// m). Warps straddle bucket boundaries and run both paths, so an order that puts cheap m next
+// to expensive m shortens the slowest warp of a tile.
+template <int kT, int kS, int kCap, int kG, bool kAll, uint32_t kPos = 0x76543210u>
 __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     const double* __restrict__ speeds, const uint32_t* __restrict__ offsets, uint64_t n,
     uint8_t* __restrict__ cand_out, double* __restrict__ obj_out, uint64_t en0, uint64_t en1) {
@@ -301,7 +304,8 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     if (ct < cnt) {
       int b = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) b += q < my_m ? s_cnt[g][p][q] : 0;
+      for (int q = 0; q < 8; ++q)
+        b += ((kPos >> (4 * q)) & 15) < ((kPos >> (4 * my_m)) & 15) ? s_cnt[g][p][q] : 0;
       s_order[g][b + my_rank] = static_cast<uint16_t>(ct);
     }
     named_bar_sync(1 + g, kT);
@@ -332,12 +336,12 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
   }
 }
 
-template <int kT, int kS, int kCap, int kG, bool kAll>
+template <int kT, int kS, int kCap, int kG, bool kAll, uint32_t kPos = 0x76543210u>
 cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint64_t n,
                             uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
                             cudaStream_t stream) {
   using L = PipeLayout<kT, kS, kCap>;
-  auto kern = optimize_pipe_kernel<kT, kS, kCap, kG, kAll>;
+  auto kern = optimize_pipe_kernel<kT, kS, kCap, kG, kAll, kPos>;
   static int grid_cap = 0;
   if (!grid_cap) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -371,7 +375,10 @@ cudaError_t launch_pipe(const double* speeds, const uint32_t* offsets, uint64_t 
   switch (pipe_cfg()) {
     case 1: return launch_pipe_cfg<128, 8, 640, 4, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
     case 2: return launch_pipe_cfg<128, 6, 640, 3, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
-    default: return launch_pipe_cfg<256, 4, 1280, 2, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    case 3: return launch_pipe_cfg<256, 4, 1280, 2, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    // bucket order 3,2,5,7,6,1,4 (bad m last): adjacent buckets pair cheap and expensive
+    // searches (max adjacent cost 268 vs 361 for ascending m; costs ~ candidates + loads)
+    default: return launch_pipe_cfg<256, 4, 1280, 2, kAll, 0x34260157u>(speeds, offsets, n, cand, obj, en0, en1, stream);
   }
 }
 

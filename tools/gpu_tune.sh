@@ -1,4 +1,5 @@
+# A/B the search-kernel configurations (MISO_B200_PIPE_CFG) and check cfg 3 parity.
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.txt 2>&1
-timeout 600 python tools/tune_search.py > gpurun_out/tune.txt 2>&1
+python tools/tune_search.py ${CFGS:-0 3 4} > gpurun_out/tune.txt 2>&1
+MISO_B200_PIPE_CFG=${TESTCFG:-3} timeout 900 python -m pytest tests/test_search_gpu.py -x -q > gpurun_out/pytest_cfg.txt 2>&1
