@@ -259,6 +259,68 @@ def bench_c3(args):
                       "cpu_baseline": cpu}), flush=True)
 
 
+def bench_c1(args):
+    """Config 1 (BASELINE.json configs[0], the reference CPU example): one A100 with 3
+    co-located jobs (generate_trace seed 7), noisy predictor (target MAE 0.017, rng_seed 7) ->
+    default small-slice model -> effective_speed -> optimize_partition, through the C-ABI
+    host-pointer call miso_b200_decide (H2D, fused predict+search kernel, D2H, sync every
+    call). Latency metric: microseconds per decision, call nonce 1..K; beside it the reference's
+    own chain (oracle/_ref) on one host thread over the same nonces."""
+    import paper_2207_11428_b200 as miso
+    ctx = miso.Context(0)
+    tr = miso.generate_trace(7, 3)
+    jobs = [(f"j{i}", (tr.speeds5[i, 4], tr.speeds5[i, 3], tr.speeds5[i, 2]), int(tr.mem_gb[i]), None)
+            for i in range(3)]
+    K = max(args.steps, 1000)
+    # the C-ABI call a C++ host makes (ctypes, preallocated host buffers)
+    import ctypes as C
+    t3 = np.ascontiguousarray([list(j[1]) for j in jobs], np.float64)
+    mem = np.ascontiguousarray([j[2] for j in jobs], np.uint8)
+    qos = np.full(3, -1, np.int8)
+    e, objv, place = C.c_int(), C.c_double(), np.zeros(7, np.uint8)
+    fn = miso.lib.miso_b200_decide
+    args_c = (ctx._h, t3.ctypes.data, mem.ctypes.data, qos.ctypes.data, 3)
+    tail = (1, 0.017, C.byref(e), place.ctypes.data, C.byref(objv), None)
+    for r in range(max(args.warmup, 10)):
+        fn(*args_c, r + 1, 7, *tail)
+    lat = []
+    acc = 0.0
+    for r in range(K):
+        t0 = time.perf_counter()
+        rc = fn(*args_c, r + 1, 7, *tail)
+        lat.append(time.perf_counter() - t0)
+        assert rc >= 0
+        if rc == 1:
+            acc += objv.value
+    py_lat = []
+    for r in range(200):
+        t0 = time.perf_counter()
+        res, _ = ctx.decide(jobs, nonce=r + 1, rng_seed=7)
+        py_lat.append(time.perf_counter() - t0)
+    first, _ = ctx.decide(jobs, nonce=1, rng_seed=7)
+    lat_us = np.array(lat) * 1e6
+    line = {"metric": "config-1 decision latency (MPS profile -> predictor -> best MIG partition, 3 jobs)",
+            "value": float(np.median(lat_us)), "unit": "us/decision", "higher_is_better": False,
+            "p99_us": float(np.percentile(lat_us, 99)),
+            "python_api_us": float(np.median(py_lat) * 1e6), "steps": K, "warmup": max(args.warmup, 10),
+            "dtype": "f64", "data": "synthetic (generate_trace seed 7, 3 jobs; nonce 1..K)",
+            "config": {"workload": "config1: single A100 model, 3 co-located jobs",
+                       "api": "miso_b200_decide via ctypes (host pointers; roster passed in the launch, results in mapped pinned memory, completion flag)"},
+            "anchor": {"partition": first.partition_name if first else None,
+                       "objective": first.objective if first else None},
+            "e2e": {"value": float(np.median(lat_us)), "unit": "us/decision",
+                    "h2d_bytes_per_step": 3 * 24 + 3 * 2 + 8, "d2h_bytes_per_step": 1 + 8 + 3 * 40}}
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib
+    if oracle_lib.have_ref() and not args.no_cpu_baseline:
+        sec, ref_acc = oracle_lib.Ref().c1_time(K)
+        line["cpu_baseline"] = {"value": sec / K * 1e6, "unit": "us/decision", "cores": 1,
+                                "kind": "reference", "sample": f"{K} decisions, nonce 1..{K}, 1 thread"}
+        line["parity"] = {"objective_sum_bit_equal": bool(np.float64(acc).view(np.uint64) ==
+                                                          np.float64(ref_acc).view(np.uint64))}
+    print(json.dumps(line), flush=True)
+
+
 def bench_c4(args):
     """Config 4 (BASELINE.json configs[3]): 100 GPUs, 1000-job Poisson traces (lambda 10 s),
     seeds 0..S-1, default overheads; per trial the reference's run_trial_unit policy set:
@@ -329,10 +391,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", choices=["c2", "c3", "c4"], default="c2",
-                    help="c2 = headline (config 2); c3 / c4 = secondary measurements")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4"], default="c2",
+                    help="c2 = headline (config 2); c1 / c3 / c4 = secondary measurements")
     ap.add_argument("--seeds", type=int, default=1024, help="c4: trace seeds per launch")
     args = ap.parse_args()
+    if args.config == "c1":
+        bench_c1(args)
+        return
     if args.config == "c3":
         bench_c3(args)
         return

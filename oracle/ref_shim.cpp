@@ -8,6 +8,7 @@
 // Each entry point names the reference call it drives.
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <sstream>
@@ -415,6 +416,51 @@ void ref_rng_raw(uint64_t seed, size_t n, uint64_t* out) {
 // build_mps_matrix(pad_to_seven) -> predict_mig_speeds(noisy target_mae, rng_seed=seed, nonce)
 // -> extrapolate_small_slices(default model) -> effective_speed -> optimize_partition.
 // Outputs: truth3/mem per job (for the GPU path), est5 per job (post-zeroing), decision.
+// Config 1 latency: the reference CPU example's decision chain (build_mps_matrix ->
+// predict_mig_speeds -> extrapolate_small_slices -> effective_speed -> optimize_partition,
+// profiles.hpp:151-167, 214-253, 370-384, 60-65; optimizer.hpp:62-115) on the anchor roster,
+// repeated `reps` times on the calling thread with call nonce 1..reps. Inputs (trace, MPS rates)
+// are built once outside the timed loop. Returns seconds; *checksum sums the objectives.
+double ref_c1_time(uint64_t seed, int job_count, double interference, double target_mae,
+                   int reps, double* checksum) {
+  miso::TraceSpec spec;
+  spec.job_count = job_count;
+  spec.seed = seed;
+  auto tr = miso::generate_trace(spec);
+  std::vector<miso::JobProfile> profs;
+  for (auto& j : tr.jobs) profs.push_back(j.profile);
+  for (int level : miso::kMpsLevels) miso::simulate_mps_rates(profs, level, interference);
+  miso::PredictorSpec ps;
+  ps.mode = miso::PredictorSpec::Mode::noisy;
+  ps.target_mae = target_mae;
+  ps.rng_seed = seed;
+  const auto& model = default_model();
+  double acc = 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < reps; ++r) {
+    auto mps = miso::build_mps_matrix(miso::pad_to_seven(profs));
+    auto mig = miso::predict_mig_speeds(mps, profs, ps, static_cast<uint64_t>(r + 1));
+    auto small = miso::extrapolate_small_slices(mig, model);
+    std::vector<miso::JobSpeeds> jobs;
+    for (int c = 0; c < job_count; ++c) {
+      const auto& p = profs[c];
+      miso::SpeedTable est;
+      est.v = {small.at(p.job_id).f1, small.at(p.job_id).f2, mig.values[2][c], mig.values[1][c],
+               mig.values[0][c]};
+      miso::JobSpeeds js;
+      js.job_id = p.job_id;
+      for (miso::Slice k : miso::kAllSlices)
+        js.speeds[k] = miso::effective_speed(est[k], k, p.mem_demand_gb, p.qos_min_slice);
+      jobs.push_back(js);
+    }
+    auto res = miso::optimize_partition(jobs, miso::default_catalog());
+    if (res) acc += res->objective;
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  *checksum = acc;
+  return std::chrono::duration<double>(t1 - t0).count();
+}
+
 int ref_c1_chain(uint64_t seed, int job_count, double interference, double target_mae,
                  uint64_t nonce, double* truth3, int* mem_gb, double* est5, int* entry,
                  uint8_t* place, double* obj) {

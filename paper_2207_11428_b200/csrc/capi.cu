@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -32,6 +33,7 @@ struct miso_b200_ctx {
   size_t cap_inst = 0;
   void* h_stage = nullptr;  // single-decision staging (miso_b200_decide)
   void* d_stage = nullptr;
+  uint64_t decide_seq = 0;
   // simulator
   int8_t* d_spare_lut = nullptr;  // max_spare_slice_for LUT of the active catalog
   bool lut_valid = false;
@@ -161,7 +163,6 @@ void miso_b200_destroy(miso_b200_ctx* ctx) {
   cudaFree(ctx->d_offsets);
   cudaFree(ctx->d_cand);
   cudaFree(ctx->d_obj);
-  cudaFree(ctx->d_stage);
   cudaFree(ctx->d_spare_lut);
   cudaFree(ctx->d_sim_ws);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
@@ -331,36 +332,44 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
     return fail(MISO_B200_E_INVALID, "optimize_partition needs 1..7 jobs, got " + std::to_string(m));
   if (int rc = check_predictor(mode, target_mae)) return rc;
   DeviceGuard g(ctx->device);
-  // One pinned staging block: [truth3 m*3 | est5 m*5 | obj | nonce | offsets 2 | mem m | qos m | cand]
-  struct Stage {
-    double truth[21], est[35], obj;
-    uint64_t nonce;
-    uint32_t off[2];
-    uint8_t mem[7];
-    int8_t qos[7];
-    uint8_t cand;
-  };
+  // Latency path: the roster goes by value in the launch, results come back through mapped
+  // pinned memory, completion is a sequence number the kernel stores last (decide_one_kernel).
   if (!ctx->h_stage) {
-    CUDA_TRY(cudaMallocHost(&ctx->h_stage, sizeof(Stage)));
-    CUDA_TRY(cudaMalloc(&ctx->d_stage, sizeof(Stage)));
+    CUDA_TRY(cudaHostAlloc(&ctx->h_stage, sizeof(DecideOneOut), cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer(&ctx->d_stage, ctx->h_stage, 0));
+    std::memset(ctx->h_stage, 0, sizeof(DecideOneOut));
   }
   if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
-  Stage* h = static_cast<Stage*>(ctx->h_stage);
-  Stage* d = static_cast<Stage*>(ctx->d_stage);
-  std::memcpy(h->truth, truth3, sizeof(double) * 3 * m);
-  std::memcpy(h->mem, mem_gb, size_t(m));
-  std::memcpy(h->qos, qos_kind, size_t(m));
-  h->nonce = nonce;
-  h->off[0] = 0;
-  h->off[1] = static_cast<uint32_t>(m);
-  double dw2[4], dw1[4];
-  default_model(dw2, dw1);
+  DecideOneArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < m; ++c) {
+    for (int k = 0; k < 3; ++k) a.truth[c][k] = truth3[3 * c + k];
+    a.mem[c] = mem_gb[c];
+    a.qos[c] = qos_kind[c];
+  }
+  default_model(a.w2, a.w1);
+  a.target_mae = target_mae;
+  a.nonce = nonce;
+  a.rng_seed = rng_seed;
+  a.en0 = ctx->en0;
+  a.en1 = ctx->en1;
+  a.seq = ++ctx->decide_seq;
+  a.m = m;
+  a.noisy = mode;
+  DecideOneOut* h = static_cast<DecideOneOut*>(ctx->h_stage);
   cudaStream_t s = ctx->streams[0];
-  CUDA_TRY(cudaMemcpyAsync(d, h, sizeof(Stage), cudaMemcpyHostToDevice, s));
-  CUDA_TRY(launch_decide(d->truth, d->mem, d->qos, d->off, &d->nonce, 1, rng_seed, mode,
-                         target_mae, dw2, dw1, ctx->en0, ctx->en1, &d->cand, &d->obj, d->est, s));
-  CUDA_TRY(cudaMemcpyAsync(h, d, sizeof(Stage), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(launch_decide_one(a, static_cast<DecideOneOut*>(ctx->d_stage), s));
+  // Spin on the completion flag; after ~50 ms of spinning fall back to a stream sync, which
+  // also surfaces any launch/execution error.
+  const volatile uint64_t* flag = &h->seq;
+  for (long spin = 0; *flag != a.seq; ++spin) {
+    if (spin > (1l << 22)) {
+      CUDA_TRY(cudaStreamSynchronize(s));
+      if (*flag != a.seq) return fail(MISO_B200_E_UNEXPECTED, "decide kernel did not complete");
+      break;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   if (est5) std::memcpy(est5, h->est, sizeof(double) * 5 * m);
   if (h->cand == MISO_B200_CAND_INFEASIBLE) return 0;
   int e = -1, mm = 0;

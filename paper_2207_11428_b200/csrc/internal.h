@@ -20,6 +20,24 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
                           const double* w1, uint64_t en0, uint64_t en1, uint8_t* cand,
                           double* obj, double* est_out, cudaStream_t stream);
 
+// Single-roster decision (miso_b200_decide): everything by value, results in mapped memory.
+struct DecideOneArgs {
+  double truth[7][3];  // (f7, f4, f3) per job
+  double w2[4], w1[4];
+  double target_mae;
+  uint64_t nonce, rng_seed, en0, en1, seq;
+  int m, noisy;
+  uint8_t mem[7];
+  int8_t qos[7];
+};
+struct DecideOneOut {
+  double est[35];
+  double obj;
+  uint64_t seq;  // written last (after a system fence): the call's completion flag
+  uint8_t cand;
+};
+cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream);
+
 // Host: generate_trace (workload.hpp:97-114); dist_kind 0 lognormal, 1 fixed, 2 uniform.
 void host_generate_trace(uint64_t seed, int job_count, double lambda_s, double max_duration_s,
                          int dist_kind, double sigma, double fixed_s, double lo_s, double hi_s,

@@ -178,4 +178,65 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------
+// Single-roster latency path (config 1, miso_b200_decide): the whole roster travels as kernel
+// parameters (no device-side reads of host or global input), one warp predicts -- lane
+// 2c + e perturbs entry e (4g, 3g) of column c, so the two mt19937_64 seeding chains of a
+// column run side by side -- lane 0 searches, and the results plus a completion sequence
+// number are stored straight into mapped pinned host memory (the host spins on `seq`).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(32) decide_one_kernel(DecideOneArgs a, DecideOneOut* out) {
+  __shared__ double s_rows[7 * 5];
+  __shared__ double s_pert[7][2];
+  const int lane = threadIdx.x;
+  const int m = a.m;
+  // perturbed 4g / 3g entries (profiles.hpp:234-244), one per lane
+  if (lane < 2 * m) {
+    const int c = lane >> 1, e = lane & 1;
+    const double truth = a.truth[c][1 + e];
+    double v = truth;
+    if (a.noisy) {
+      const uint64_t base = mix_seed(a.rng_seed, a.nonce);
+      v = perturb_speed(truth, a.target_mae, mix_seed(base, static_cast<uint64_t>(c) * 8 + 1 + e));
+    }
+    s_pert[c][e] = v;
+  }
+  __syncwarp();
+  if (lane < m) {
+    // re-anchor, clamp and extrapolate exactly as predict_column (oracle-mode inputs)
+    ModelW w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      w.w2[i] = a.w2[i];
+      w.w1[i] = a.w1[i];
+    }
+    double e5[5];
+    predict_column(a.truth[lane][0], s_pert[lane][0], s_pert[lane][1], lane, 0, 0, false, 0.0,
+                   w, e5);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const double v = effective_speed(e5[k], k, a.mem[lane], a.qos[lane]);
+      s_rows[lane * 5 + k] = v;
+      out->est[lane * 5 + k] = v;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double ob = 0.0;
+    const bool all = a.en0 == ~0ull && a.en1 == (1ull << (kNumCands - 64)) - 1;
+    const uint8_t c = all ? search_any<true>(s_rows, m, a.en0, a.en1, &ob)
+                          : search_any<false>(s_rows, m, a.en0, a.en1, &ob);
+    out->cand = c;
+    out->obj = ob;
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) *reinterpret_cast<volatile uint64_t*>(&out->seq) = a.seq;
+}
+
+cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream) {
+  decide_one_kernel<<<1, 32, 0, stream>>>(a, out);
+  return cudaGetLastError();
+}
+
 }  // namespace miso_b200

@@ -175,6 +175,15 @@ class Ref:
         self.lib.ref_rng_raw(seed, n, out)
         return out
 
+    def c1_time(self, reps: int, seed=7, job_count=3, interference=0.8, target_mae=0.017):
+        """Seconds for `reps` config-1 decisions on this thread (ref_c1_time) and the sum of
+        their objectives (nonce 1..reps)."""
+        cs = C.c_double()
+        f = self.lib.ref_c1_time
+        f.restype = C.c_double
+        f.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double)]
+        return f(seed, job_count, interference, target_mae, reps, C.byref(cs)), cs.value
+
     def c1_chain(self, seed=7, job_count=3, interference=0.8, target_mae=0.017, nonce=1):
         t = np.zeros(3 * job_count); mem = np.zeros(job_count, np.int32)
         est = np.zeros(5 * job_count); e = C.c_int(); pl = np.zeros(7, np.uint8); ob = C.c_double()
