@@ -47,6 +47,16 @@ static bool force_simple_path() {
   return v == 1;
 }
 
+// Programmatic dependent launch for the persistent search kernel (MISO_B200_NO_PDL=1 disables).
+static bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MISO_B200_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 __device__ __forceinline__ int valid_m(uint32_t mm) {
   return (mm >= 1 && mm <= 7) ? static_cast<int>(mm) : 0;
 }
@@ -179,6 +189,7 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
 
   const int tid = threadIdx.x;
   const uint64_t ntiles = (n + kT - 1) / kT;
+  if (tid == 0) TRACE(4095);
   if (tid == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -187,6 +198,12 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     fence_mbar_init();
   }
   if (tid < kG * 16) (&s_cnt[0][0][0])[tid] = 0;
+  // Programmatic dependent launch: the shared-memory prologue above overlaps the previous grid
+  // on the stream; let the next grid be scheduled now (its CTAs take over SMs as ours retire),
+  // then wait until every earlier grid has completed and its writes are visible before
+  // touching global memory. Both are no-ops without the launch attribute.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
 
   auto stage_base = [&](int s) { return smem + size_t(s) * L::kStageBytes; };
@@ -355,8 +372,17 @@ cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint6
   }
   const uint64_t tiles = (n + kT - 1) / kT;
   const unsigned grid = static_cast<unsigned>(tiles < uint64_t(grid_cap) ? tiles : uint64_t(grid_cap));
-  kern<<<grid, kT * kG + 32, L::kBytes, stream>>>(speeds, offsets, n, cand, obj, en0, en1);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kT * kG + 32);
+  cfg.dynamicSmemBytes = L::kBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, speeds, offsets, n, cand, obj, en0, en1);
 }
 
 // MISO_B200_PIPE_CFG selects a tile/stage/group configuration (tuning only).

@@ -31,8 +31,23 @@ int main() {
   printf("kernel %.1f us  err=%s\n", ms * 1e3, cudaGetErrorString(cudaGetLastError()));
   static unsigned long long tr[148][4096];
   cudaMemcpyFromSymbol(tr, miso_b200::g_trace, sizeof(tr));
+  // Per-CTA summary: kernel entry (slot 4095), first TMA issue, first consumer start, last
+  // consumer done -- all relative to the earliest kernel entry.
+  unsigned long long g0 = ~0ull;
+  for (int c = 0; c < 148; ++c) if (tr[c][4095] && tr[c][4095] < g0) g0 = tr[c][4095];
+  double s_entry = 0, s_issue = 0, s_first = 0, s_last = 0, mx_last = 0, mn_last = 1e18;
+  for (int c = 0; c < 148; ++c) {
+    unsigned long long last = 0;
+    for (int k = 0; k < 255; ++k) if (tr[c][k * 16 + 7] > last) last = tr[c][k * 16 + 7];
+    s_entry += tr[c][4095] - g0; s_issue += tr[c][3] - g0; s_first += tr[c][6] - g0;
+    s_last += last - g0;
+    if (last - g0 > mx_last) mx_last = last - g0;
+    if (last - g0 < mn_last) mn_last = last - g0;
+  }
+  printf("mean over CTAs (ns from first entry): entry %.0f  first-issue %.0f  first-consume %.0f  last-done %.0f (min %.0f max %.0f)\n",
+         s_entry / 148, s_issue / 148, s_first / 148, s_last / 148, mn_last, mx_last);
   for (int cta : {0, 77}) {
-    unsigned long long t0 = tr[cta][0];
+    unsigned long long t0 = tr[cta][4095];
     printf("CTA %d (ns rel. to first producer iteration):\n k  - - - p.issue - - c.start c.done | chunk done times\n", cta);
     for (int k = 0; k < 27; ++k) {
       printf("%2d", k);
