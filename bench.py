@@ -333,7 +333,7 @@ def bench_c4(args):
     from concurrent.futures import ThreadPoolExecutor
     ctx = miso.Context(0)
     S = args.seeds
-    traces = [miso.generate_trace(s, 1000, lambda_s=10.0) for s in range(S)]
+    traces = miso.generate_traces(range(S), 1000, lambda_s=10.0)
 
     def trial_batch():
         nop = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="nopart", cluster_size=100))
@@ -461,7 +461,7 @@ def bench_c5(args):
     # ---- trials ----
     s_lo, s_hi = shard_range(S, rank, world)
     t0 = time.perf_counter()
-    traces = [miso.generate_trace(sd, 1000, lambda_s=10.0) for sd in range(s_lo, s_hi)]
+    traces = miso.generate_traces(range(s_lo, s_hi), 1000, lambda_s=10.0)
     gen_s = time.perf_counter() - t0
     rows = np.zeros((s_hi - s_lo, 3))
     if dist is not None:

@@ -195,6 +195,14 @@ int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
                              double lo_s, double hi_s, double* arrival_s, double* duration_s,
                              double* speeds5, int* mem_gb);
 
+/* generate_trace for n_traces seeds at once on `threads` host threads (<= 0: all hardware
+ * threads), same spec for every trace; trace r writes job_count entries at offset r*job_count of
+ * each output array (speeds5: 5 per job). Bit-identical to n calls of miso_b200_generate_trace. */
+int miso_b200_generate_traces(const uint64_t* seeds, int n_traces, int job_count, double lambda_s,
+                              double max_duration_s, int dist, double sigma, double fixed_s,
+                              double lo_s, double hi_s, int threads, double* arrival_s,
+                              double* duration_s, double* speeds5, int* mem_gb);
+
 /* run_simulation (sim.hpp:976-979) for n_seeds independent tasks at once, one warp per task,
  * DEVICE pointers. Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r owns
  * jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in
@@ -214,6 +222,23 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
                              miso_b200_log_record* log, int64_t log_cap, double* stp_series,
                              int64_t stp_cap, void* stream);
+
+/* miso_b200_simulate_batch with flags. MISO_B200_SIM_JCT_ONLY: the tasks' consumer needs only
+ * the job-completion metrics (avg_jct_s, jct_sum_s, makespan, the time fractions, counters):
+ * the STP series (refresh_stp, sim.hpp:353-361) is not maintained, stp_time_avg/stp_points
+ * read 0 and stp_series must be NULL. Every other field, the event order and the event log are
+ * unchanged (STP never feeds back into decisions). best_static_partition (sim.hpp:1031-1066)
+ * reads only avg_jct_s of its candidate runs. */
+#define MISO_B200_SIM_JCT_ONLY 1u
+int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                                const int32_t* task_trace, const uint8_t* static_counts,
+                                const int32_t* job_offsets, const double* arrival_s,
+                                const double* base_s, const double* speeds5,
+                                const uint8_t* mem_gb, const int8_t* qos_kind,
+                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
+                                double* stp_series, int64_t stp_cap, unsigned flags,
+                                void* stream);
 
 /* Pinned host memory for the *_host paths. */
 int miso_b200_host_alloc(size_t bytes, void** out);

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -399,6 +400,34 @@ int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
   return MISO_B200_OK;
 }
 
+int miso_b200_generate_traces(const uint64_t* seeds, int n_traces, int job_count, double lambda_s,
+                              double max_duration_s, int dist, double sigma, double fixed_s,
+                              double lo_s, double hi_s, int threads, double* arrival_s,
+                              double* duration_s, double* speeds5, int* mem_gb) {
+  if (n_traces < 0) return fail(MISO_B200_E_INVALID, "n_traces < 0");
+  if (n_traces == 0) return MISO_B200_OK;
+  if (!seeds) return fail(MISO_B200_E_INVALID, "null buffer");
+  // validate once with the first trace (same spec for all)
+  int rc = miso_b200_generate_trace(seeds[0], job_count, lambda_s, max_duration_s, dist, sigma,
+                                    fixed_s, lo_s, hi_s, arrival_s, duration_s, speeds5, mem_gb);
+  if (rc) return rc;
+  int nt = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  nt = std::max(1, std::min(nt, n_traces - 1));
+  std::atomic<int> next{1};
+  auto work = [&]() {
+    for (int r = next.fetch_add(1); r < n_traces; r = next.fetch_add(1)) {
+      const size_t o = size_t(r) * size_t(job_count);
+      host_generate_trace(seeds[r], job_count, lambda_s, max_duration_s, dist, sigma, fixed_s,
+                          lo_s, hi_s, arrival_s + o, duration_s + o, speeds5 + 5 * o, mem_gb + o);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  return MISO_B200_OK;
+}
+
 static int64_t us_from_s_host(double s) { return static_cast<int64_t>(std::llround(s * 1e6)); }
 
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
@@ -409,7 +438,25 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
                              miso_b200_log_record* log, int64_t log_cap, double* stp_series,
                              int64_t stp_cap, void* stream) {
+  return miso_b200_simulate_batch_ex(ctx, opt, n_seeds, task_trace, static_counts, job_offsets,
+                                     arrival_s, base_s, speeds5, mem_gb, qos_kind, rng_seed,
+                                     metrics, job_jct_us, log, log_cap, stp_series, stp_cap, 0u,
+                                     stream);
+}
+
+int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                                const int32_t* task_trace, const uint8_t* static_counts,
+                                const int32_t* job_offsets, const double* arrival_s,
+                                const double* base_s, const double* speeds5,
+                                const uint8_t* mem_gb, const int8_t* qos_kind,
+                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
+                                double* stp_series, int64_t stp_cap, unsigned flags,
+                                void* stream) {
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
+  if (flags & ~MISO_B200_SIM_JCT_ONLY) return fail(MISO_B200_E_INVALID, "unknown flags");
+  if ((flags & MISO_B200_SIM_JCT_ONLY) && stp_series)
+    return fail(MISO_B200_E_INVALID, "JCT_ONLY runs keep no STP series");
   if (n_seeds < 0) return fail(MISO_B200_E_INVALID, "n_seeds < 0");
   if (n_seeds == 0) return MISO_B200_OK;
   if (opt->policy != MISO_B200_POLICY_NOPART && opt->policy != MISO_B200_POLICY_ORACLE &&
@@ -487,6 +534,7 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
   p.target_mae = opt->target_mae;
   p.drift_threshold = opt->reprofile_drift_threshold;
   p.max_events = opt->max_events ? opt->max_events : 100000000ull;
+  p.track_stp = (flags & MISO_B200_SIM_JCT_ONLY) ? 0 : 1;
   p.en0 = ctx->en0;
   p.en1 = ctx->en1;
   SimBatch b{};

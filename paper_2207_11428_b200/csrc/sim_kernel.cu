@@ -23,6 +23,7 @@
 // the same global push counter (sim.hpp:280-282); the next event is the minimum live key --
 // the same total order the heap pops. A slot is cleared whenever its epoch is bumped.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cstdint>
 
@@ -300,7 +301,7 @@ __device__ void schedule_completion(Ctx& c, int ji) {
 // bit-identical to the reference's loop over all jobs. Partial sums are cached per index and
 // the chain restarts at the smallest index changed since the previous refresh.
 __device__ void refresh_stp(Ctx& c) {
-  if (!c.stp_dirty) return;
+  if (!c.stp_dirty || !c.p->track_stp) return;
   c.stp_dirty = false;
   const double* r = c.rate_eff;
   double* P = c.stp_prefix;
@@ -1222,7 +1223,16 @@ cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double*
   }
   const int threads = 128;
   const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
-  sim::simulate_kernel<<<blocks, threads, 0, stream>>>(b, p, w);
+  // MISO_SIM_SMEM_PAD (tuning only): dynamic shared memory reserved per block to cap how many
+  // simulations share an SM's L1/L2 working set.
+  static int pad = -1;
+  if (pad < 0) {
+    const char* e = getenv("MISO_SIM_SMEM_PAD");
+    pad = e ? atoi(e) : 0;
+    if (pad > 0)
+      cudaFuncSetAttribute(sim::simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+  }
+  sim::simulate_kernel<<<blocks, threads, pad, stream>>>(b, p, w);
   return cudaGetLastError();
 }
 

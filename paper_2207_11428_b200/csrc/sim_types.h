@@ -22,6 +22,7 @@ enum LogKind : uint8_t {
 
 struct SimParams {
   int policy, cluster_size, noisy, check_invariants;
+  int track_stp;  // 0: JCT-only run, refresh_stp skipped (MISO_B200_SIM_JCT_ONLY)
   int64_t window_us, reconfig_us, ckpt_us;
   double interference, target_mae, drift_threshold;
   uint64_t max_events;

@@ -59,6 +59,8 @@ lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_do
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
     [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
+lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
+    [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
 
 
 @dataclass
@@ -114,6 +116,32 @@ def generate_trace(seed: int, job_count: int = 100, lambda_s: float = 60.0,
     return Trace(a, d, sp, mem, None, seed)
 
 
+lib.miso_b200_generate_traces.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                          C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                                          C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+
+
+def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float = 60.0,
+                    max_duration_s: float = 7200.0, dist: str = "lognormal", sigma: float = 1.5,
+                    fixed_s: float = 600.0, lo_s: float = 60.0, hi_s: float = 7200.0,
+                    threads: int = 0) -> List[Trace]:
+    """generate_trace for many seeds on every host thread (miso_b200_generate_traces);
+    identical to [generate_trace(s, ...) for s in seeds]."""
+    kind = {"lognormal": 0, "fixed": 1, "uniform": 2}[dist]
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    n = len(sd)
+    a = np.zeros((n, job_count))
+    d = np.zeros((n, job_count))
+    sp = np.zeros((n, job_count, 5))
+    mem = np.zeros((n, job_count), np.int32)
+    if n:
+        _check(lib.miso_b200_generate_traces(sd.ctypes.data, n, job_count, lambda_s, max_duration_s,
+                                             kind, sigma, fixed_s, lo_s, hi_s, threads,
+                                             a.ctypes.data, d.ctypes.data, sp.ctypes.data,
+                                             mem.ctypes.data))
+    return [Trace(a[i], d[i], sp[i], mem[i], None, int(sd[i])) for i in range(n)]
+
+
 @dataclass
 class SimResult:
     metrics: np.ndarray                    # METRICS_DTYPE per seed
@@ -131,11 +159,13 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
                    rng_seeds: Optional[Sequence[int]] = None, log_cap: int = 0,
                    stp_cap: int = 0, want_jct: bool = False, stream=None,
                    task_trace: Optional[Sequence[int]] = None,
-                   static_partitions: Optional[Sequence[Sequence[int]]] = None) -> SimResult:
+                   static_partitions: Optional[Sequence[Sequence[int]]] = None,
+                   jct_only: bool = False) -> SimResult:
     """run_simulation for every task at once (device), one warp per task. By default task i
     simulates traces[i]; with task_trace, task t simulates traces[task_trace[t]] (one launch
     can replay a trace under many static partitions). rng_seeds (per task) default to the
-    trace's seed (experiment.hpp:305). static_partitions: per-task kind counts (optsta)."""
+    trace's seed (experiment.hpp:305). static_partitions: per-task kind counts (optsta).
+    jct_only: MISO_B200_SIM_JCT_ONLY (no STP series; stp metrics read 0)."""
     import torch
     dev = torch.device("cuda", ctx.device)
     S = len(traces) if task_trace is None else len(task_trace)
@@ -165,10 +195,11 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     o = opts.to_c()
     p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    _check(lib.miso_b200_simulate_batch(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
-                                        p(d_arr), p(d_dur),
-                                        p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
-                                        p(d_jct), p(d_log), log_cap, p(d_stp), stp_cap, s))
+    _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+                                           p(d_arr), p(d_dur),
+                                           p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
+                                           p(d_jct), p(d_log), log_cap, p(d_stp), stp_cap,
+                                           1 if jct_only else 0, s))
     torch.cuda.synchronize(dev)
     met = d_met.cpu().numpy().view(METRICS_DTYPE)
     res = SimResult(met, traces=list(traces))
@@ -284,7 +315,9 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
         for e in np.nonzero(largest >= need)[0]:
             tasks.append((ti, int(e)))
             parts.append(cat[e])
-    res = simulate_batch(ctx, traces, opts, task_trace=[t for t, _ in tasks], static_partitions=parts)
+    # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs
+    res = simulate_batch(ctx, traces, opts, task_trace=[t for t, _ in tasks], static_partitions=parts,
+                         jct_only=True)
     out = []
     table = np.full((len(traces), len(cat)), np.inf)
     for i, (ti, e) in enumerate(tasks):

@@ -27,3 +27,15 @@ def test_generate_trace_validation():
         args.update(kw)
         with pytest.raises(m.MisoError):
             m.generate_trace(**args)
+
+
+def test_generate_traces_batched_equals_single():
+    """miso_b200_generate_traces (thread pool) == per-seed generate_trace, bit for bit."""
+    import paper_2207_11428_b200 as m
+    seeds = [0, 1, 7, 123456789, 2**63 + 5]
+    many = m.generate_traces(seeds, 200, lambda_s=10.0, threads=3)
+    for s, t in zip(seeds, many):
+        one = m.generate_trace(s, 200, lambda_s=10.0)
+        for f in ("arrival_s", "duration_s", "speeds5", "mem_gb"):
+            assert np.array_equal(getattr(one, f), getattr(t, f)), (s, f)
+    assert m.generate_traces([], 10) == []
