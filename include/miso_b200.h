@@ -223,12 +223,16 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              miso_b200_log_record* log, int64_t log_cap, double* stp_series,
                              int64_t stp_cap, void* stream);
 
-/* miso_b200_simulate_batch with flags. MISO_B200_SIM_JCT_ONLY: the tasks' consumer needs only
- * the job-completion metrics (avg_jct_s, jct_sum_s, makespan, the time fractions, counters):
- * the STP series (refresh_stp, sim.hpp:353-361) is not maintained, stp_time_avg/stp_points
- * read 0 and stp_series must be NULL. Every other field, the event order and the event log are
- * unchanged (STP never feeds back into decisions). best_static_partition (sim.hpp:1031-1066)
- * reads only avg_jct_s of its candidate runs. */
+/* miso_b200_simulate_batch with flags and per-job outputs. MISO_B200_SIM_JCT_ONLY: the tasks'
+ * consumer needs only the job-completion metrics (avg_jct_s, jct_sum_s, makespan, the time
+ * fractions, counters): the STP series (refresh_stp, sim.hpp:353-361) is not maintained,
+ * stp_time_avg/stp_points read 0 and stp_series must be NULL. Every other field, the event
+ * order and the event log are unchanged (STP never feeds back into decisions).
+ * best_static_partition (sim.hpp:1031-1066) reads only avg_jct_s of its candidate runs.
+ * job_out (optional, any task_trace): per task max_jobs x 6 int64 -- the job's completion time
+ * in us (-1 if it never finished) and its per-phase accumulated us (queued, mps, checkpoint,
+ * running, idle): the inputs of MetricsReport::per_job (sim.hpp:916-929); max_jobs = the
+ * longest trace of the batch. */
 #define MISO_B200_SIM_JCT_ONLY 1u
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
                                 const int32_t* task_trace, const uint8_t* static_counts,
@@ -236,9 +240,22 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
                                 const double* base_s, const double* speeds5,
                                 const uint8_t* mem_gb, const int8_t* qos_kind,
                                 const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
-                                int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
-                                double* stp_series, int64_t stp_cap, unsigned flags,
-                                void* stream);
+                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
+                                int64_t log_cap, double* stp_series, int64_t stp_cap,
+                                unsigned flags, void* stream);
+
+/* The same with HOST pointers (synchronous): inputs are copied to the device, results back.
+ * n_traces = entries of job_offsets minus one. The C++ binding include/miso_b200_sim.hpp builds
+ * run_simulation / best_static_partition / run_experiment_in_memory on this call. */
+int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
+                                  int n_tasks, int n_traces, const int32_t* task_trace,
+                                  const uint8_t* static_counts, const int32_t* job_offsets,
+                                  const double* arrival_s, const double* base_s,
+                                  const double* speeds5, const uint8_t* mem_gb,
+                                  const int8_t* qos_kind, const uint64_t* rng_seed,
+                                  miso_b200_sim_metrics* metrics, int64_t* job_out,
+                                  miso_b200_log_record* log, int64_t log_cap,
+                                  double* stp_series, int64_t stp_cap, unsigned flags);
 
 /* Pinned host memory for the *_host paths. */
 int miso_b200_host_alloc(size_t bytes, void** out);

@@ -440,8 +440,8 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              int64_t stp_cap, void* stream) {
   return miso_b200_simulate_batch_ex(ctx, opt, n_seeds, task_trace, static_counts, job_offsets,
                                      arrival_s, base_s, speeds5, mem_gb, qos_kind, rng_seed,
-                                     metrics, job_jct_us, log, log_cap, stp_series, stp_cap, 0u,
-                                     stream);
+                                     metrics, job_jct_us, nullptr, log, log_cap, stp_series,
+                                     stp_cap, 0u, stream);
 }
 
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
@@ -450,9 +450,9 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
                                 const double* base_s, const double* speeds5,
                                 const uint8_t* mem_gb, const int8_t* qos_kind,
                                 const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
-                                int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
-                                double* stp_series, int64_t stp_cap, unsigned flags,
-                                void* stream) {
+                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
+                                int64_t log_cap, double* stp_series, int64_t stp_cap,
+                                unsigned flags, void* stream) {
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (flags & ~MISO_B200_SIM_JCT_ONLY) return fail(MISO_B200_E_INVALID, "unknown flags");
   if ((flags & MISO_B200_SIM_JCT_ONLY) && stp_series)
@@ -554,6 +554,7 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
   b.ws_stride = stride;
   b.metrics = metrics;
   b.job_jct_us = job_jct_us;
+  b.job_out = job_out;
   b.log = log;
   b.log_cap = log ? log_cap : 0;
   b.stp_series = stp_series;
@@ -561,6 +562,90 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
   double w2[4], w1[4];
   default_model(w2, w1);
   CUDA_TRY(launch_simulate(b, p, w2, w1, s));
+  return MISO_B200_OK;
+}
+
+extern "C++" {
+namespace {
+struct DevBuf {  // owning device allocation for the synchronous host-pointer calls
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+};
+template <class T>
+int upload(DevBuf& d, const T* src, size_t n, cudaStream_t s) {
+  if (!src || n == 0) return MISO_B200_OK;
+  CUDA_TRY(cudaMalloc(&d.p, n * sizeof(T)));
+  CUDA_TRY(cudaMemcpyAsync(d.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  return MISO_B200_OK;
+}
+int alloc_out(DevBuf& d, size_t bytes) {
+  if (bytes == 0) return MISO_B200_OK;
+  CUDA_TRY(cudaMalloc(&d.p, bytes));
+  return MISO_B200_OK;
+}
+}  // namespace
+}  // extern "C++"
+
+int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
+                                  int n_tasks, int n_traces, const int32_t* task_trace,
+                                  const uint8_t* static_counts, const int32_t* job_offsets,
+                                  const double* arrival_s, const double* base_s,
+                                  const double* speeds5, const uint8_t* mem_gb,
+                                  const int8_t* qos_kind, const uint64_t* rng_seed,
+                                  miso_b200_sim_metrics* metrics, int64_t* job_out,
+                                  miso_b200_log_record* log, int64_t log_cap,
+                                  double* stp_series, int64_t stp_cap, unsigned flags) {
+  if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
+  if (n_tasks < 0 || n_traces < 0) return fail(MISO_B200_E_INVALID, "negative count");
+  if (n_tasks == 0) return MISO_B200_OK;
+  if (!job_offsets || !arrival_s || !base_s || !speeds5 || !mem_gb || !qos_kind || !rng_seed ||
+      !metrics)
+    return fail(MISO_B200_E_INVALID, "null buffer");
+  if (!task_trace && n_traces < n_tasks) return fail(MISO_B200_E_INVALID, "fewer traces than tasks");
+  for (int i = 0; i < n_traces; ++i)
+    if (job_offsets[i + 1] < job_offsets[i]) return fail(MISO_B200_E_INVALID, "job_offsets must be non-decreasing");
+  if (task_trace)
+    for (int t = 0; t < n_tasks; ++t)
+      if (task_trace[t] < 0 || task_trace[t] >= n_traces) return fail(MISO_B200_E_INVALID, "task_trace out of range");
+  int max_jobs = 0;
+  for (int i = 0; i < n_traces; ++i) max_jobs = std::max(max_jobs, job_offsets[i + 1] - job_offsets[i]);
+  const size_t J = size_t(job_offsets[n_traces]);
+  DeviceGuard g(ctx->device);
+  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  cudaStream_t s = ctx->streams[0];
+  DevBuf d_tt, d_sc, d_off, d_arr, d_base, d_sp, d_mem, d_qos, d_seed, d_met, d_jo, d_log, d_stp;
+  int rc;
+  if ((rc = upload(d_tt, task_trace, task_trace ? size_t(n_tasks) : 0, s))) return rc;
+  if ((rc = upload(d_sc, static_counts, static_counts ? size_t(n_tasks) * 5 : 0, s))) return rc;
+  if ((rc = upload(d_off, job_offsets, size_t(n_traces) + 1, s))) return rc;
+  if ((rc = upload(d_arr, arrival_s, J, s))) return rc;
+  if ((rc = upload(d_base, base_s, J, s))) return rc;
+  if ((rc = upload(d_sp, speeds5, J * 5, s))) return rc;
+  if ((rc = upload(d_mem, mem_gb, J, s))) return rc;
+  if ((rc = upload(d_qos, qos_kind, J, s))) return rc;
+  if ((rc = upload(d_seed, rng_seed, size_t(n_tasks), s))) return rc;
+  if ((rc = alloc_out(d_met, sizeof(miso_b200_sim_metrics) * size_t(n_tasks)))) return rc;
+  const size_t jo_n = job_out ? size_t(n_tasks) * size_t(max_jobs) * 6 : 0;
+  if ((rc = alloc_out(d_jo, jo_n * sizeof(int64_t)))) return rc;
+  const size_t log_n = log ? size_t(n_tasks) * size_t(std::max<int64_t>(log_cap, 0)) : 0;
+  if ((rc = alloc_out(d_log, log_n * sizeof(miso_b200_log_record)))) return rc;
+  const size_t stp_n = stp_series ? size_t(n_tasks) * 2 * size_t(std::max<int64_t>(stp_cap, 0)) : 0;
+  if ((rc = alloc_out(d_stp, stp_n * sizeof(double)))) return rc;
+  rc = miso_b200_simulate_batch_ex(
+      ctx, opt, n_tasks, static_cast<const int32_t*>(d_tt.p), static_cast<const uint8_t*>(d_sc.p),
+      static_cast<const int32_t*>(d_off.p), static_cast<const double*>(d_arr.p),
+      static_cast<const double*>(d_base.p), static_cast<const double*>(d_sp.p),
+      static_cast<const uint8_t*>(d_mem.p), static_cast<const int8_t*>(d_qos.p),
+      static_cast<const uint64_t*>(d_seed.p), static_cast<miso_b200_sim_metrics*>(d_met.p),
+      nullptr, static_cast<int64_t*>(d_jo.p), static_cast<miso_b200_log_record*>(d_log.p),
+      log ? log_cap : 0, static_cast<double*>(d_stp.p), stp_series ? stp_cap : 0, flags, s);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(metrics, d_met.p, sizeof(miso_b200_sim_metrics) * size_t(n_tasks),
+                           cudaMemcpyDeviceToHost, s));
+  if (jo_n) CUDA_TRY(cudaMemcpyAsync(job_out, d_jo.p, jo_n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (log_n) CUDA_TRY(cudaMemcpyAsync(log, d_log.p, log_n * sizeof(miso_b200_log_record), cudaMemcpyDeviceToHost, s));
+  if (stp_n) CUDA_TRY(cudaMemcpyAsync(stp_series, d_stp.p, stp_n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
   return MISO_B200_OK;
 }
 

@@ -1161,6 +1161,15 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   }
 
   // ---- finalize (sim.hpp:902-949) ----
+  if (b.job_out) {  // per-job report inputs (sim.hpp:916-929), lanes in parallel
+    int64_t* o = b.job_out + size_t(warp) * size_t(b.max_jobs) * 6;
+    for (int i = lane; i < J; i += 32) {
+      const DJob& j = c.jobs[i];
+      o[6 * i] = (j.flags & kDone) ? j.completion_us : -1;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) o[6 * i + 1 + k] = j.acc[k];
+    }
+  }
   SimMetrics m;
   m.status = c.status;
   m.job_count = J;

@@ -45,6 +45,7 @@ struct SimBatch {
   size_t ws_stride;
   SimMetrics* metrics;
   int64_t* job_jct_us;
+  int64_t* job_out;  // per task: max_jobs x {completion_us (-1 unfinished), acc_us[5]}
   LogRec* log;
   int64_t log_cap;
   double* stp_series;

@@ -60,7 +60,7 @@ lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_do
 lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
     [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
 lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
-    [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
+    [C.c_void_p] * 13 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
 
 
 @dataclass
@@ -198,7 +198,7 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
                                            p(d_arr), p(d_dur),
                                            p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
-                                           p(d_jct), p(d_log), log_cap, p(d_stp), stp_cap,
+                                           p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
                                            1 if jct_only else 0, s))
     torch.cuda.synchronize(dev)
     met = d_met.cpu().numpy().view(METRICS_DTYPE)
