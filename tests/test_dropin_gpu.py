@@ -47,3 +47,16 @@ def test_reference_sim_experiment_tests_against_b200(name):
     assert failed == EXPECTED_FAIL[name], r.stdout[-4000:] + r.stderr[-2000:]
     want = f"{TOTALS[name]} tests, {len(EXPECTED_FAIL[name])} failed"
     assert want in r.stdout, r.stdout[-2000:]
+
+
+def test_experiment_csv_json_byte_identical_to_reference():
+    """run_experiment_in_memory (experiment.hpp:364) on the reference's CPU engine and on the
+    B200 (every trial of a sweep point in one launch): write_csv and summarize().dump(2) text
+    identical, per-row reports (format_report incl. per-job phases and the STP series)
+    identical -- MAE, lambda and checkpoint sweeps, all four policies, drift re-profiling."""
+    b = BIN.parent / "experiment_parity"
+    if not b.exists():
+        pytest.skip("parity binary not built (needs /root/reference at build time)")
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=1200, cwd=b.parent)
+    print(r.stdout)
+    assert r.returncode == 0 and "PARITY OK" in r.stdout, r.stdout + r.stderr
