@@ -336,11 +336,16 @@ def bench_c4(args):
     traces = miso.generate_traces(range(S), 1000, lambda_s=10.0)
 
     def trial_batch():
+        # run_trial_unit's work per seed (experiment.hpp:299-362): nopart, the best-static
+        # search (every feasible catalog entry, one launch), optsta re-run with the chosen
+        # partition (full metrics), miso
         nop = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="nopart", cluster_size=100))
         st = miso.best_static_partition(ctx, traces, cluster_size=100)
+        sta = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="optsta", cluster_size=100),
+                                  static_partitions=[miso.DEFAULT_CATALOG[e] for e, _ in st])
         mis = miso.simulate_batch(ctx, traces, miso.SimOptions(policy="miso", cluster_size=100,
                                                                predictor="noisy"))
-        return nop, st, mis
+        return nop, st, sta, mis
 
     for _ in range(max(1, args.warmup)):
         trial_batch()
@@ -348,12 +353,13 @@ def bench_c4(args):
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        nop, st, mis = trial_batch()
+        nop, st, sta, mis = trial_batch()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
     j_nop = nop.metrics["avg_jct_s"]
-    j_sta = np.array([tab[e] for e, tab in st])
+    j_sta = sta.metrics["avg_jct_s"]
+    assert np.array_equal(j_sta.view(np.uint64), np.array([tab[e] for e, tab in st]).view(np.uint64))
     j_mis = mis.metrics["avg_jct_s"]
     ev = int(mis.metrics["events"].sum())
     cpu = None
@@ -376,7 +382,7 @@ def bench_c4(args):
                  "static_entry_equal": bool(all(e == st[i][0] for i, (e, _) in enumerate(outs)))}
     print(json.dumps({"metric": "cluster-simulation trials/sec (config 4: nopart + optsta(best static) + miso, 100 GPUs x 1000 jobs)",
                       "value": S / dt, "unit": "trials/s", "s_per_step": dt, "seeds": S,
-                      "simulations_per_step": int(S * 2 + sum(np.isfinite(t).sum() for _, t in st)),
+                      "simulations_per_step": int(S * 3 + sum(np.isfinite(t).sum() for _, t in st)),
                       "miso_events_per_seed": ev / S, "steps": args.steps, "warmup": args.warmup,
                       "dtype": "f64", "data": "synthetic (generate_trace seeds 0..S-1)",
                       "median_jct_norm": {"optsta": float(np.median(j_sta / j_nop)),

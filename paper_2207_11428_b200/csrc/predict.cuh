@@ -69,6 +69,30 @@ __device__ __forceinline__ void mt64_first3(uint64_t seed, uint64_t out[3]) {
   out[2] = mt64_twist_draw(x2, x3, x158);
 }
 
+// Two independent streams at once: the 158-step seeding recurrences are serial chains of
+// 64-bit multiplies, so interleaving the two perturbed entries of a column doubles the ILP.
+__device__ __forceinline__ void mt64_first3_x2(uint64_t sa, uint64_t sb, uint64_t ra[3],
+                                               uint64_t rb[3]) {
+  const uint64_t a1 = mt64_seed_step(sa, 1), b1 = mt64_seed_step(sb, 1);
+  const uint64_t a2 = mt64_seed_step(a1, 2), b2 = mt64_seed_step(b1, 2);
+  const uint64_t a3 = mt64_seed_step(a2, 3), b3 = mt64_seed_step(b2, 3);
+  uint64_t xa = a3, xb = b3;
+#pragma unroll 8
+  for (uint32_t i = 4; i <= 155; ++i) {
+    xa = mt64_seed_step(xa, i);
+    xb = mt64_seed_step(xb, i);
+  }
+  const uint64_t a156 = mt64_seed_step(xa, 156), b156 = mt64_seed_step(xb, 156);
+  const uint64_t a157 = mt64_seed_step(a156, 157), b157 = mt64_seed_step(b156, 157);
+  const uint64_t a158 = mt64_seed_step(a157, 158), b158 = mt64_seed_step(b157, 158);
+  ra[0] = mt64_twist_draw(sa, a1, a156);
+  ra[1] = mt64_twist_draw(a1, a2, a157);
+  ra[2] = mt64_twist_draw(a2, a3, a158);
+  rb[0] = mt64_twist_draw(sb, b1, b156);
+  rb[1] = mt64_twist_draw(b1, b2, b157);
+  rb[2] = mt64_twist_draw(b2, b3, b158);
+}
+
 __device__ __forceinline__ double uniform01_of(uint64_t raw) {  // common.hpp:90
   return static_cast<double>(raw >> 11) * 0x1.0p-53;
 }
@@ -77,11 +101,8 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {  // s
   return v < lo ? lo : (hi < v ? hi : v);
 }
 
-// profiles.hpp:193-205
-__device__ __forceinline__ double perturb_speed(double truth, double target_mae, uint64_t entry_seed) {
-  if (target_mae <= 0.0) return truth;
-  uint64_t r[3];
-  mt64_first3(entry_seed, r);
+// profiles.hpp:193-205, given the entry's first three raw draws.
+__device__ __forceinline__ double perturb_with(double truth, double target_mae, const uint64_t r[3]) {
   double u1 = uniform01_of(r[0]);
   const double u2 = uniform01_of(r[1]);
   if (u1 <= 0.0) u1 = 0x1.0p-53;
@@ -98,6 +119,14 @@ __device__ __forceinline__ double perturb_speed(double truth, double target_mae,
   return (1.0 - truth >= truth - kSpeedFloor) ? 1.0 : kSpeedFloor;
 }
 
+// profiles.hpp:193-205
+__device__ __forceinline__ double perturb_speed(double truth, double target_mae, uint64_t entry_seed) {
+  if (target_mae <= 0.0) return truth;
+  uint64_t r[3];
+  mt64_first3(entry_seed, r);
+  return perturb_with(truth, target_mae, r);
+}
+
 struct ModelW {
   double w2[4], w1[4];  // LinearMap weights over (f7, f4, f3, 1)
 };
@@ -110,10 +139,13 @@ __device__ __forceinline__ void predict_column(double f7, double f4, double f3, 
                                                double target_mae, const ModelW& w,
                                                double out5[5]) {
   double v0 = f7, v1 = f4, v2 = f3;
-  if (noisy) {
+  if (noisy && target_mae > 0.0) {  // (target_mae <= 0: perturb_speed returns the truth)
     const uint64_t base = mix_seed(rng_seed, nonce);
-    v1 = perturb_speed(f4, target_mae, mix_seed(base, static_cast<uint64_t>(col) * 8 + 1));
-    v2 = perturb_speed(f3, target_mae, mix_seed(base, static_cast<uint64_t>(col) * 8 + 2));
+    uint64_t ra[3], rb[3];
+    mt64_first3_x2(mix_seed(base, static_cast<uint64_t>(col) * 8 + 1),
+                   mix_seed(base, static_cast<uint64_t>(col) * 8 + 2), ra, rb);
+    v1 = perturb_with(f4, target_mae, ra);
+    v2 = perturb_with(f3, target_mae, rb);
   }
   double mx = v0;  // std::max({a, b, c})
   if (mx < v1) mx = v1;
