@@ -7,6 +7,7 @@
 #include <thread>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -232,7 +233,11 @@ int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
   int rc = ensure_host_scratch(ctx, rows, n);
   if (rc) return rc;
   // Two-stream pipeline: chunk k's H2D overlaps chunk k-1's search and D2H.
-  const uint64_t kChunk = 1u << 17;
+  static uint64_t kChunk = 0;
+  if (!kChunk) {  // MISO_B200_E2E_CHUNK: instances per pipeline chunk (tuning)
+    const char* e = getenv("MISO_B200_E2E_CHUNK");
+    kChunk = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : (1u << 17);
+  }
   int k = 0;
   for (uint64_t i0 = 0; i0 < n; i0 += kChunk, ++k) {
     const uint64_t i1 = std::min(n, i0 + kChunk);
