@@ -121,6 +121,37 @@ lib.miso_b200_generate_traces.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_doub
                                           C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
 
 
+class TraceBatch(list):
+    """A list of Trace views that also keeps the batch's CSR arrays (generate_traces), so
+    simulate_batch / best_static_partition upload them without re-concatenating. Slicing
+    with a step of 1 keeps the CSR form."""
+
+    csr = None  # (offsets int32 (n+1), arrival, duration, speeds5 (J,5), mem u8, qos i8)
+
+    def __getitem__(self, i):
+        r = super().__getitem__(i)
+        if isinstance(i, slice) and self.csr is not None and i.step in (None, 1):
+            lo, hi, _ = i.indices(len(self))
+            off, a, d, sp, mem, qos = self.csr
+            o0, o1 = int(off[lo]), int(off[hi])
+            b = TraceBatch(r)
+            b.csr = (off[lo:hi + 1] - o0, a[o0:o1], d[o0:o1], sp[o0:o1], mem[o0:o1], qos[o0:o1])
+            return b
+        return r
+
+
+def _csr(traces):
+    """(offsets, arrival, duration, speeds5, mem, qos) of a trace list."""
+    if isinstance(traces, TraceBatch) and traces.csr is not None:
+        return traces.csr
+    offs = np.zeros(len(traces) + 1, np.int32)
+    offs[1:] = np.cumsum([t.n for t in traces])
+    cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
+    return (offs, cat(lambda t: t.arrival_s, np.float64), cat(lambda t: t.duration_s, np.float64),
+            cat(lambda t: t.speeds5, np.float64).reshape(-1, 5), cat(lambda t: t.mem_gb, np.uint8),
+            cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8))
+
+
 def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float = 60.0,
                     max_duration_s: float = 7200.0, dist: str = "lognormal", sigma: float = 1.5,
                     fixed_s: float = 600.0, lo_s: float = 60.0, hi_s: float = 7200.0,
@@ -139,7 +170,11 @@ def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float 
                                              kind, sigma, fixed_s, lo_s, hi_s, threads,
                                              a.ctypes.data, d.ctypes.data, sp.ctypes.data,
                                              mem.ctypes.data))
-    return [Trace(a[i], d[i], sp[i], mem[i], None, int(sd[i])) for i in range(n)]
+    out = TraceBatch(Trace(a[i], d[i], sp[i], mem[i], None, int(sd[i])) for i in range(n))
+    offs = (np.arange(n + 1) * job_count).astype(np.int32)
+    out.csr = (offs, a.reshape(-1), d.reshape(-1), sp.reshape(-1, 5), mem.reshape(-1).astype(np.uint8),
+               np.full(n * job_count, -1, np.int8))
+    return out
 
 
 @dataclass
@@ -169,16 +204,10 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     import torch
     dev = torch.device("cuda", ctx.device)
     S = len(traces) if task_trace is None else len(task_trace)
-    offs = np.zeros(len(traces) + 1, np.int32)
-    offs[1:] = np.cumsum([t.n for t in traces])
-    cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
-    arr = cat(lambda t: t.arrival_s, np.float64)
-    dur = cat(lambda t: t.duration_s, np.float64)
-    sp = cat(lambda t: t.speeds5, np.float64)
-    mem = cat(lambda t: t.mem_gb, np.uint8)
-    qos = cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8)
+    offs, arr, dur, sp, mem, qos = _csr(traces)
     if rng_seeds is None:
-        rng_seeds = [traces[i if task_trace is None else task_trace[i]].seed for i in range(S)]
+        tseeds = np.array([t.seed for t in traces], np.uint64)
+        rng_seeds = tseeds if task_trace is None else tseeds[np.asarray(task_trace, np.int64)]
     seeds = np.asarray(rng_seeds, np.uint64)
     T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
     d_offs, d_arr, d_dur, d_sp = T(offs, None), T(arr, None), T(dur, None), T(sp, None)
@@ -301,35 +330,34 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
                       mps_window_s=base.mps_window_s, interference=base.interference,
                       check_invariants=base.check_invariants, max_events=base.max_events)
     from .catalog import GPC, MEM_GB
-    mem_gb = np.array(MEM_GB)
-    gpc = np.array(GPC)
-    largest = np.array([max(k for k in range(5) if c[k] > 0) for c in cat])
-    tasks, parts = [], []
-    for ti, t in enumerate(traces):
-        qos = np.full(t.n, -1) if t.qos_kind is None else np.asarray(t.qos_kind)
-        qg = np.where(qos >= 0, gpc[np.maximum(qos, 0)], 0)
-        ok = (mem_gb[None, :] >= np.asarray(t.mem_gb)[:, None]) & (gpc[None, :] >= qg[:, None])
-        if not ok.any(axis=1).all():
-            raise ValueError(f"trace {ti}: a job fits no slice kind")
-        need = int(ok.argmax(axis=1).max())  # min_slice_for per job, then the largest
-        for e in np.nonzero(largest >= need)[0]:
-            tasks.append((ti, int(e)))
-            parts.append(cat[e])
-    # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs
-    res = simulate_batch(ctx, traces, opts, task_trace=[t for t, _ in tasks], static_partitions=parts,
-                         jct_only=True)
-    out = []
+    catc = np.asarray(cat, np.uint8).reshape(-1, 5)
+    largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
+    # min_slice_for per job (topology.hpp:68-72), then the largest per trace (sim.hpp:1036-1041)
+    offs, _, _, _, mem, qos = _csr(traces)
+    qg = np.where(qos >= 0, np.asarray(GPC)[np.maximum(qos, 0)], 0)
+    ok = (np.asarray(MEM_GB)[None, :] >= mem[:, None].astype(np.int64)) & \
+         (np.asarray(GPC)[None, :] >= qg[:, None])
+    fits = ok.any(axis=1)
+    if not fits.all():
+        j = int(np.argmin(fits))
+        ti = int(np.searchsorted(offs, j, side="right") - 1)
+        raise ValueError(f"trace {ti}: a job fits no slice kind")
+    need = np.maximum.reduceat(ok.argmax(axis=1), offs[:-1]) if len(traces) else np.zeros(0, np.int64)
+    feas = largest[None, :] >= need[:, None]                      # (traces, entries)
+    ti_arr, e_arr = np.nonzero(feas)                               # trace-major, catalog order
     table = np.full((len(traces), len(cat)), np.inf)
-    for i, (ti, e) in enumerate(tasks):
-        table[ti, e] = res.metrics[i]["avg_jct_s"]
+    if len(ti_arr):
+        res = simulate_batch(ctx, traces, opts, task_trace=ti_arr.astype(np.int32),
+                             static_partitions=catc[e_arr], jct_only=True)
+        # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs
+        table[ti_arr, e_arr] = res.metrics["avg_jct_s"]
+    out = []
     for ti in range(len(traces)):
-        best, chosen = np.inf, -1
-        for e in range(len(cat)):  # strict <, first wins (sim.hpp:1058)
-            if table[ti, e] < best:
-                best, chosen = table[ti, e], e
-        if chosen < 0:
+        row = table[ti]
+        chosen = int(np.argmin(row))  # first minimum == strict <, first wins (sim.hpp:1058)
+        if not row[chosen] < np.inf:
             raise ValueError(f"trace {ti}: no static partition can host this trace")
-        out.append((chosen, table[ti]))
+        out.append((chosen, row))
     return out
 
 

@@ -1,5 +1,7 @@
 #!/usr/bin/env python3
-"""One best_static_partition launch over config-4 traces (profiling helper, GPU only)."""
+"""best_static_partition over config-4 traces (profiling/A-B helper, GPU only): one warm-up
+call, then the median of 3 timed calls (host task building + one device launch each)."""
+import statistics
 import sys
 import time
 
@@ -8,10 +10,15 @@ import torch  # noqa: E402
 import paper_2207_11428_b200 as miso  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 ctx = miso.Context(0)
-traces = [miso.generate_trace(s, 1000, lambda_s=10.0) for s in range(S)]
-torch.cuda.synchronize()
-t0 = time.perf_counter()
-st = miso.best_static_partition(ctx, traces, cluster_size=100)
-torch.cuda.synchronize()
-print("static search", S, "traces", time.perf_counter() - t0, "s")
+traces = miso.generate_traces(range(S), 1000, lambda_s=10.0)
+miso.best_static_partition(ctx, traces, cluster_size=100)
+ts = []
+for _ in range(reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    miso.best_static_partition(ctx, traces, cluster_size=100)
+    torch.cuda.synchronize()
+    ts.append(time.perf_counter() - t0)
+print("static search", S, "traces median", round(statistics.median(ts), 4), "s", [round(t, 4) for t in ts])
