@@ -195,53 +195,64 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
                    stp_cap: int = 0, want_jct: bool = False, stream=None,
                    task_trace: Optional[Sequence[int]] = None,
                    static_partitions: Optional[Sequence[Sequence[int]]] = None,
-                   jct_only: bool = False) -> SimResult:
+                   jct_only: bool = False, defer: bool = False):
     """run_simulation for every task at once (device), one warp per task. By default task i
     simulates traces[i]; with task_trace, task t simulates traces[task_trace[t]] (one launch
     can replay a trace under many static partitions). rng_seeds (per task) default to the
     trace's seed (experiment.hpp:305). static_partitions: per-task kind counts (optsta).
-    jct_only: MISO_B200_SIM_JCT_ONLY (no STP series; stp metrics read 0)."""
+    jct_only: MISO_B200_SIM_JCT_ONLY (no STP series; stp metrics read 0).
+    stream: a torch.cuda.Stream for the uploads, the launch and the read-back (default: the
+    current stream). defer=True returns a zero-argument callable that waits for that stream
+    and returns the SimResult, so launches on different streams (and different Contexts --
+    each owns one simulation workspace) run concurrently."""
     import torch
     dev = torch.device("cuda", ctx.device)
+    st_obj = stream if stream is not None else torch.cuda.current_stream(dev)
     S = len(traces) if task_trace is None else len(task_trace)
     offs, arr, dur, sp, mem, qos = _csr(traces)
     if rng_seeds is None:
         tseeds = np.array([t.seed for t in traces], np.uint64)
         rng_seeds = tseeds if task_trace is None else tseeds[np.asarray(task_trace, np.int64)]
     seeds = np.asarray(rng_seeds, np.uint64)
-    T = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
-    d_offs, d_arr, d_dur, d_sp = T(offs, None), T(arr, None), T(dur, None), T(sp, None)
-    d_mem, d_qos, d_seed = T(mem, None), T(qos, None), T(seeds.view(np.int64), None)
-    d_tt = None if task_trace is None else T(np.asarray(task_trace, np.int32), None)
     if opts.policy == "optsta" and static_partitions is None:
         raise ValueError("optsta requires a static partition")  # sim.hpp:208-209
-    d_sc = None if static_partitions is None else \
-        T(np.asarray(static_partitions, np.uint8).reshape(S, 5), None)
-    d_met = torch.empty(S * METRICS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    d_jct = torch.empty(int(offs[-1]), dtype=torch.int64, device=dev) if want_jct else None
-    d_log = torch.empty(S * log_cap * 32, dtype=torch.uint8, device=dev) if log_cap else None
-    d_stp = torch.empty(S * stp_cap * 2, dtype=torch.float64, device=dev) if stp_cap else None
-    s = stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
-    o = opts.to_c()
-    p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
-                                           p(d_arr), p(d_dur),
-                                           p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
-                                           p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
-                                           1 if jct_only else 0, s))
-    torch.cuda.synchronize(dev)
-    met = d_met.cpu().numpy().view(METRICS_DTYPE)
-    res = SimResult(met, traces=list(traces))
-    if want_jct:
-        j = d_jct.cpu().numpy()
-        res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(len(traces))]
-    if log_cap:
-        lg = d_log.cpu().numpy().view(LOG_DTYPE).reshape(S, log_cap)
-        res.logs = [lg[i, : min(log_cap, int(met[i]["log_records"]))] for i in range(S)]
-    if stp_cap:
-        st = d_stp.cpu().numpy().reshape(S, stp_cap, 2)
-        res.stp = [st[i, : min(stp_cap, int(met[i]["stp_points"]))] for i in range(S)]
-    return res
+    with torch.cuda.stream(st_obj):
+        T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev, non_blocking=False)  # noqa: E731
+        d_offs, d_arr, d_dur, d_sp = T(offs), T(arr), T(dur), T(sp)
+        d_mem, d_qos, d_seed = T(mem), T(qos), T(seeds.view(np.int64))
+        d_tt = None if task_trace is None else T(np.asarray(task_trace, np.int32))
+        d_sc = None if static_partitions is None else \
+            T(np.asarray(static_partitions, np.uint8).reshape(S, 5))
+        d_met = torch.empty(S * METRICS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        d_jct = torch.empty(int(offs[-1]), dtype=torch.int64, device=dev) if want_jct else None
+        d_log = torch.empty(S * log_cap * 32, dtype=torch.uint8, device=dev) if log_cap else None
+        d_stp = torch.empty(S * stp_cap * 2, dtype=torch.float64, device=dev) if stp_cap else None
+        o = opts.to_c()
+        p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+                                               p(d_arr), p(d_dur),
+                                               p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
+                                               p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
+                                               1 if jct_only else 0, st_obj.cuda_stream))
+    keep = (d_offs, d_arr, d_dur, d_sp, d_mem, d_qos, d_seed, d_tt, d_sc)  # alive until done
+
+    def finish() -> SimResult:
+        st_obj.synchronize()
+        _ = keep  # inputs stay referenced until the stream has finished with them
+        met = d_met.cpu().numpy().view(METRICS_DTYPE)
+        res = SimResult(met, traces=list(traces))
+        if want_jct:
+            j = d_jct.cpu().numpy()
+            res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(len(traces))]
+        if log_cap:
+            lg = d_log.cpu().numpy().view(LOG_DTYPE).reshape(S, log_cap)
+            res.logs = [lg[i, : min(log_cap, int(met[i]["log_records"]))] for i in range(S)]
+        if stp_cap:
+            stp = d_stp.cpu().numpy().reshape(S, stp_cap, 2)
+            res.stp = [stp[i, : min(stp_cap, int(met[i]["stp_points"]))] for i in range(S)]
+        return res
+
+    return finish if defer else finish()
 
 
 def fmt_g(v: float) -> str:
@@ -315,7 +326,7 @@ def min_kind(mem_gb: int, qos_kind=None):
 
 
 def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: int,
-                          overheads: Optional[SimOptions] = None, catalog=None):
+                          overheads: Optional[SimOptions] = None, catalog=None, stream=None):
     """best_static_partition (sim.hpp:1031-1066) for many traces in ONE launch: every
     (trace, candidate partition) pair is an independent optsta simulation (one warp each).
     Returns per trace (chosen catalog index, table of avg JCT per entry; inf = skipped or
@@ -348,7 +359,7 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
     table = np.full((len(traces), len(cat)), np.inf)
     if len(ti_arr):
         res = simulate_batch(ctx, traces, opts, task_trace=ti_arr.astype(np.int32),
-                             static_partitions=catc[e_arr], jct_only=True)
+                             static_partitions=catc[e_arr], jct_only=True, stream=stream)
         # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs
         table[ti_arr, e_arr] = res.metrics["avg_jct_s"]
     out = []
