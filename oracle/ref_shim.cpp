@@ -7,9 +7,11 @@
 //
 // Each entry point names the reference call it drives.
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -403,6 +405,34 @@ int ref_trial(uint64_t seed, int job_count, double lambda_s, int cluster_size, d
   out[1] = miso::run_simulation(trace, cluster_size, miso::Policy::optsta, o, ps, st.chosen).avg_jct_s;
   out[2] = miso::run_simulation(trace, cluster_size, miso::Policy::miso, o, ps).avg_jct_s;
   return catalog_index(miso::default_catalog(), st.chosen);
+}
+
+// save_trace (workload.hpp:149-170) text of generate_trace({job_count, lambda_s, seed}).
+// Returns the length (the text is truncated to cap).
+size_t ref_trace_text(uint64_t seed, int job_count, double lambda_s, char* buf, size_t cap) {
+  miso::TraceSpec spec;
+  spec.job_count = job_count;
+  spec.lambda_s = lambda_s;
+  spec.seed = seed;
+  std::ostringstream o;
+  miso::save_trace(miso::generate_trace(spec), o);
+  const std::string t = o.str();
+  std::memcpy(buf, t.data(), std::min(cap, t.size()));
+  return t.size();
+}
+
+// load_trace (workload.hpp:172-243) of `text`: 0 if it parses (job_count written), else the
+// ParseError line and its what() text in msg.
+int ref_load_trace(const char* text, int* job_count, char* msg, size_t cap) {
+  std::istringstream in{std::string(text)};
+  try {
+    auto t = miso::load_trace(in);
+    *job_count = static_cast<int>(t.jobs.size());
+    return 0;
+  } catch (const miso::ParseError& e) {
+    std::snprintf(msg, cap, "%s", e.what());
+    return e.line() > 0 ? e.line() : -1;
+  }
 }
 
 // Raw std::mt19937_64 draws of DetRng(seed) (common.hpp:85-119), for fixture generators.

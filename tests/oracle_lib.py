@@ -175,6 +175,26 @@ class Ref:
         self.lib.ref_rng_raw(seed, n, out)
         return out
 
+    def trace_text(self, seed: int, job_count: int, lambda_s: float) -> str:
+        """save_trace text of the reference's generate_trace (ref_trace_text)."""
+        f = self.lib.ref_trace_text
+        f.restype = C.c_size_t
+        f.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_char_p, C.c_size_t]
+        n = f(seed, job_count, lambda_s, None, 0)
+        buf = C.create_string_buffer(n + 1)
+        f(seed, job_count, lambda_s, buf, n)
+        return buf.raw[:n].decode()
+
+    def load_trace(self, text: str):
+        """The reference's load_trace on `text`: (0, job_count, "") or (line, 0, what())."""
+        f = self.lib.ref_load_trace
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]
+        jc = C.c_int(0)
+        msg = C.create_string_buffer(512)
+        r = f(text.encode(), C.byref(jc), msg, 512)
+        return r, jc.value, msg.value.decode()
+
     def c1_time(self, reps: int, seed=7, job_count=3, interference=0.8, target_mae=0.017):
         """Seconds for `reps` config-1 decisions on this thread (ref_c1_time) and the sum of
         their objectives (nonce 1..reps)."""
