@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simulate_kernel -c 1 -o gpurun_out/sim_miso -f python tools/sim_one_policy.py miso 1024 > gpurun_out/ncu_sim.log 2>&1
