@@ -238,7 +238,7 @@ def bench_c3(args):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib
     threads = oracle_lib.host_threads()
-    ref = oracle_lib.Ref() if oracle_lib.have_ref() else None
+    ref = oracle_lib.Ref() if oracle_lib.have_ref() and not args.no_cpu_baseline else None
     cpu = None
     if ref is not None:
         k = 7 * 100_000
