@@ -433,13 +433,18 @@ def bench_c5(args):
     from paper_2207_11428_b200.dist import gather_to_rank0, shard_range
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = os.environ.get("MISO_B200_DIST_BACKEND", "nccl")
+    coll_dev = torch.device("cpu") if backend == "gloo" else dev
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     ctx = miso.Context(local)
     chunks, per_chunk, S = args.c5_chunks, 1_000_000, args.c5_seeds
     c_lo, c_hi = shard_range(chunks, rank, world)
@@ -493,12 +498,12 @@ def bench_c5(args):
         rows[i0:i0 + len(tb), 2] = mis.metrics["avg_jct_s"]
     torch.cuda.synchronize()
     trial_s = time.perf_counter() - t0
-    t = torch.tensor([search_ms, trial_s, float(feasible)], dtype=torch.float64, device=dev)
+    t = torch.tensor([search_ms, trial_s, float(feasible)], dtype=torch.float64, device=coll_dev)
     if dist is not None:
         dist.all_reduce(t[:2], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[2:], op=dist.ReduceOp.SUM)
     search_ms, trial_s, feasible = t.tolist()
-    allrows = gather_to_rank0(rows.reshape(-1), S * 3, rank, world, device=dev if world > 1 else None)
+    allrows = gather_to_rank0(rows.reshape(-1), S * 3, rank, world, device=coll_dev if world > 1 else None)
     if rank == 0:
         r = allrows.reshape(S, 3)
         print(json.dumps({
@@ -554,11 +559,19 @@ def main():
         return
 
     import torch
+    # one process per GPU; MISO_B200_DIST_BACKEND=gloo (with local % device_count) lets the
+    # multi-rank path be exercised on a single-GPU box
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    backend = os.environ.get("MISO_B200_DIST_BACKEND", "nccl")
+    coll_dev = torch.device("cpu") if backend == "gloo" else torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if dist is not None:
@@ -622,12 +635,21 @@ def main():
         host_free(p)
 
     # max over ranks
-    t = torch.tensor([total_ms, kern_ms, e2e_s], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms, kern_ms, e2e_s], dtype=torch.float64, device=coll_dev)
+    gather = None
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        stats = torch.tensor([float((d_c < 111).sum()), float(d_obj.sum().item())],
-                             dtype=torch.float64, device="cuda")
-        dist.all_reduce(stats)  # final statistics gather (feasible count, objective checksum)
+        # final result gather (untimed): every rank's decisions and objectives to rank 0 in
+        # global instance order (dist.gather_to_rank0: all_gather of equal shards, byte-exact)
+        from paper_2207_11428_b200.dist import gather_to_rank0
+        g0 = time.perf_counter()
+        all_c = gather_to_rank0(d_c, world * n, rank, world, device=coll_dev)
+        all_o = gather_to_rank0(d_obj.cpu().numpy(), world * n, rank, world, device=coll_dev)
+        g_s = time.perf_counter() - g0
+        if rank == 0:
+            assert np.array_equal(all_c[:n], d_c) and np.array_equal(all_o[:n].view(np.uint64), d_obj.cpu().numpy().view(np.uint64))
+            gather = {"instances": int(len(all_c)), "bytes": int(all_c.nbytes + all_o.nbytes),
+                      "feasible": int((all_c < 111).sum()), "s": g_s, "backend": backend}
     total_ms, kern_ms, e2e_s = t.tolist()
 
     if rank == 0:
@@ -652,11 +674,13 @@ def main():
                          "kernel_ms_note": "timed region / K (K back-to-back launches, one event pair)",
                          "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
             "e2e": {"value": world * n * E / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": nb_s + nb_o, "d2h_bytes_per_step": n * 9,
+                    "h2d_bytes_per_step": world * (nb_s + nb_o), "d2h_bytes_per_step": world * n * 9,
                     "api": "miso_b200_optimize_batch_host (pinned host buffers)", "steps": E},
             "clocks": clk,
             "gpu_launches": K,
         }
+        if gather is not None:
+            line["result_gather"] = gather
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference_rate(speeds, offs, m)
         print(json.dumps(line), flush=True)
