@@ -187,6 +187,7 @@ typedef struct {
 #define MISO_B200_LOG_SHRINK 11
 #define MISO_B200_LOG_ADMIT_SLOT 12 /* optsta admit: x = slot */
 #define MISO_B200_LOG_MIGRATE 13    /* optsta migration: x = slice kind, a = slot */
+#define MISO_B200_LOG_SPAWN 14      /* multi-instance clone: job = clone, a = parent job */
 
 /* generate_trace (workload.hpp:97-114) on the host: dist 0 lognormal(sigma), 1 fixed(fixed_s),
  * 2 uniform(lo_s, hi_s). Arrays of job_count; speeds5 kind order 1g..7g. */
@@ -223,26 +224,35 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              miso_b200_log_record* log, int64_t log_cap, double* stp_series,
                              int64_t stp_cap, void* stream);
 
-/* miso_b200_simulate_batch with flags and per-job outputs. MISO_B200_SIM_JCT_ONLY: the tasks'
- * consumer needs only the job-completion metrics (avg_jct_s, jct_sum_s, makespan, the time
- * fractions, counters): the STP series (refresh_stp, sim.hpp:353-361) is not maintained,
- * stp_time_avg/stp_points read 0 and stp_series must be NULL. Every other field, the event
- * order and the event log are unchanged (STP never feeds back into decisions).
- * best_static_partition (sim.hpp:1031-1066) reads only avg_jct_s of its candidate runs.
- * job_out (optional, any task_trace): per task max_jobs x 6 int64 -- the job's completion time
- * in us (-1 if it never finished) and its per-phase accumulated us (queued, mps, checkpoint,
- * running, idle): the inputs of MetricsReport::per_job (sim.hpp:916-929); max_jobs = the
- * longest trace of the batch. */
+/* miso_b200_simulate_batch with multi-instance jobs, flags and per-job outputs.
+ * instances (optional, per trace job): JobProfile::instance_count (>= 1; NULL = all 1). A job
+ * with k > 1 spawns k - 1 clones "id#1".."id#(k-1)" at its first admission (nopart, optsta) or
+ * estimate caching (miso, oracle), exactly as SimEngine::spawn_instances (sim.hpp:432-455);
+ * the metrics then count them (job_count = trace jobs + clones spawned).
+ * MISO_B200_SIM_JCT_ONLY: the tasks' consumer needs only the job-completion metrics (avg_jct_s,
+ * jct_sum_s, makespan, the time fractions, counters): the STP series (refresh_stp,
+ * sim.hpp:353-361) is not maintained, stp_time_avg/stp_points read 0 and stp_series must be
+ * NULL. Every other field, the event order and the event log are unchanged (STP never feeds
+ * back into decisions). best_static_partition (sim.hpp:1031-1066) reads only avg_jct_s of its
+ * candidate runs.
+ * job_out (optional, any task_trace): per task max_jobs x MISO_B200_JOB_OUT_FIELDS int64 --
+ * the job's completion time in us (-1 if it never finished), its per-phase accumulated us
+ * (queued, mps, checkpoint, running, idle), its parent job index (-1 for trace jobs) and clone
+ * ordinal k: the inputs of MetricsReport::per_job (sim.hpp:916-929). Jobs are in SimEngine
+ * order (trace jobs, then clones in spawn order); max_jobs = the largest per-trace sum of
+ * instance counts of the batch. */
 #define MISO_B200_SIM_JCT_ONLY 1u
+#define MISO_B200_JOB_OUT_FIELDS 8
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
                                 const int32_t* task_trace, const uint8_t* static_counts,
                                 const int32_t* job_offsets, const double* arrival_s,
                                 const double* base_s, const double* speeds5,
                                 const uint8_t* mem_gb, const int8_t* qos_kind,
-                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
-                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
-                                int64_t log_cap, double* stp_series, int64_t stp_cap,
-                                unsigned flags, void* stream);
+                                const uint8_t* instances, const uint64_t* rng_seed,
+                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
+                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
+                                double* stp_series, int64_t stp_cap, unsigned flags,
+                                void* stream);
 
 /* The same with HOST pointers (synchronous): inputs are copied to the device, results back.
  * n_traces = entries of job_offsets minus one. The C++ binding include/miso_b200_sim.hpp builds
@@ -252,9 +262,9 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
                                   const uint8_t* static_counts, const int32_t* job_offsets,
                                   const double* arrival_s, const double* base_s,
                                   const double* speeds5, const uint8_t* mem_gb,
-                                  const int8_t* qos_kind, const uint64_t* rng_seed,
-                                  miso_b200_sim_metrics* metrics, int64_t* job_out,
-                                  miso_b200_log_record* log, int64_t log_cap,
+                                  const int8_t* qos_kind, const uint8_t* instances,
+                                  const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                  int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
                                   double* stp_series, int64_t stp_cap, unsigned flags);
 
 /* Pinned host memory for the *_host paths. */

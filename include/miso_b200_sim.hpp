@@ -17,9 +17,9 @@
 // options.event_log in the reference's format (sim.hpp:365-367). Errors: std::invalid_argument
 // for bad options/traces (validated with the reference's own validators, in its order),
 // SimInvariantError for engine failures, InfeasibleError from the static search.
-// Not supported by the device engine (std::invalid_argument): multi-instance jobs
-// (JobProfile::instance_count > 1, API-only in the reference) and a caller-fitted
-// small-slice model (SimOptions::small_slice_model; the shared default model is used).
+// Multi-instance jobs (JobProfile::instance_count > 1) spawn their clones on the device as in
+// SimEngine::spawn_instances. Not supported (std::invalid_argument): a caller-fitted small-slice
+// model (SimOptions::small_slice_model; the shared default model is used).
 #pragma once
 
 #include <algorithm>
@@ -42,11 +42,12 @@ namespace detail {
 struct TraceArrays {
   std::vector<int32_t> offsets{0};
   std::vector<double> arrival, base, speeds;
-  std::vector<uint8_t> mem;
+  std::vector<uint8_t> mem, inst;
   std::vector<int8_t> qos;
 
   void add(const JobTrace& t) {
     for (const TraceJob& j : t.jobs) {
+      inst.push_back(static_cast<uint8_t>(std::clamp(j.profile.instance_count, 1, 255)));
       arrival.push_back(j.arrival_s);
       base.push_back(j.profile.base_duration_s);
       for (int k = 0; k < 5; ++k) speeds.push_back(j.profile.speed_table.v[k]);
@@ -77,8 +78,8 @@ inline void validate(const JobTrace& trace, const SimOptions& opt) {
     if (i == 0 && a != 0) throw std::invalid_argument("first arrival must be at t=0");
     if (a < prev) throw std::invalid_argument("arrival times must be non-decreasing");
     prev = a;
-    if (t.profile.instance_count > 1)
-      throw std::invalid_argument("miso_b200: multi-instance jobs are not supported by the device engine");
+    if (t.profile.instance_count > 255)
+      throw std::invalid_argument("miso_b200: instance_count above 255");
   }
   if (opt.small_slice_model.fitted)
     throw std::invalid_argument("miso_b200: the device engine uses the shared default small-slice model");
@@ -121,11 +122,27 @@ inline PartitionConfig unpack_part(uint32_t a) {
   return PartitionConfig::from_counts(c);
 }
 
+// Job ids in SimEngine order: the trace's, then clones "parent#k" in spawn order (job_out
+// carries each clone's parent and k).
+inline std::vector<std::string> job_ids(const JobTrace& trace, const int64_t* job_out, int n) {
+  std::vector<std::string> ids;
+  ids.reserve(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    if (static_cast<size_t>(i) < trace.jobs.size()) {
+      ids.push_back(trace.jobs[static_cast<size_t>(i)].profile.job_id);
+    } else {
+      const int64_t* o = job_out + size_t(MISO_B200_JOB_OUT_FIELDS) * static_cast<size_t>(i);
+      ids.push_back(ids[static_cast<size_t>(o[6])] + "#" + std::to_string(o[7]));
+    }
+  }
+  return ids;
+}
+
 // The reference's event-log text (sim.hpp:365-367 and its log() call sites) from the device's
 // compact records.
-inline void render_log(const JobTrace& trace, const miso_b200_log_record* r, int64_t n,
-                       std::ostream& out) {
-  auto jid = [&](int j) -> const std::string& { return trace.jobs[static_cast<size_t>(j)].profile.job_id; };
+inline void render_log(const std::vector<std::string>& ids, const miso_b200_log_record* r,
+                       int64_t n, std::ostream& out) {
+  auto jid = [&](int j) -> const std::string& { return ids[static_cast<size_t>(j)]; };
   for (int64_t i = 0; i < n; ++i) {
     const miso_b200_log_record& e = r[i];
     const int g = e.gpu;
@@ -165,6 +182,9 @@ inline void render_log(const JobTrace& trace, const miso_b200_log_record* r, int
         out << "migrate job=" << jid(e.job) << " gpu=" << g << " slot=" << e.a
             << " slice=" << kind_name(e.x);
         break;
+      case MISO_B200_LOG_SPAWN:
+        out << "spawn job=" << jid(e.job) << " parent=" << jid(static_cast<int>(e.a));
+        break;
       default: out << "?kind=" << int(e.kind); break;
     }
     out << '\n';
@@ -174,7 +194,8 @@ inline void render_log(const JobTrace& trace, const miso_b200_log_record* r, int
 // finalize (sim.hpp:902-949) from the device's scalars and per-job accumulators.
 inline MetricsReport make_report(const JobTrace& trace, Policy policy,
                                  const miso_b200_sim_metrics& m, const int64_t* job_out,
-                                 const double* stp, int64_t stp_n) {
+                                 const std::vector<std::string>* ids, const double* stp,
+                                 int64_t stp_n) {
   MetricsReport r;
   r.policy = policy_label(policy);
   r.seed = trace.spec.seed;
@@ -193,12 +214,16 @@ inline MetricsReport make_report(const JobTrace& trace, Policy policy,
   r.run_frac = m.run_frac;
   r.idle_frac = m.idle_frac;
   if (job_out) {
-    r.per_job.reserve(trace.jobs.size());
-    for (size_t i = 0; i < trace.jobs.size(); ++i) {
-      const int64_t* o = job_out + 6 * i;
+    r.per_job.reserve(static_cast<size_t>(m.job_count));
+    std::vector<int64_t> arr_us(static_cast<size_t>(m.job_count));
+    for (int i = 0; i < m.job_count; ++i) {
+      const int64_t* o = job_out + size_t(MISO_B200_JOB_OUT_FIELDS) * static_cast<size_t>(i);
+      arr_us[static_cast<size_t>(i)] =
+          o[6] < 0 ? ::miso::detail::us_from_s(trace.jobs[static_cast<size_t>(i)].arrival_s)
+                   : arr_us[static_cast<size_t>(o[6])];  // clones keep the parent's arrival
       JobMetrics jm;
-      jm.job_id = trace.jobs[i].profile.job_id;
-      const int64_t arr = ::miso::detail::us_from_s(trace.jobs[i].arrival_s);
+      jm.job_id = (*ids)[static_cast<size_t>(i)];
+      const int64_t arr = arr_us[static_cast<size_t>(i)];
       jm.arrival_s = ::miso::detail::s_from_us(arr);
       jm.queue_s = ::miso::detail::s_from_us(o[1]);
       jm.mps_s = ::miso::detail::s_from_us(o[2]);
@@ -245,14 +270,16 @@ inline std::vector<MetricsReport> run_simulation_batch(
     if (rng_seeds) seeds[i] = (*rng_seeds)[i];
     if (optsta)
       for (int k = 0; k < 5; ++k) sc.push_back(oi.static_partition->counts()[static_cast<size_t>(k)]);
-    max_jobs = std::max(max_jobs, static_cast<int>(traces[i]->jobs.size()));
+    int cap = 0;
+    for (const TraceJob& j : traces[i]->jobs) cap += std::max(1, j.profile.instance_count);
+    max_jobs = std::max(max_jobs, cap);
   }
   const miso_b200_sim_options c = detail::to_c(options);
   Device& d = Device::get();
   std::lock_guard<std::mutex> lock(d.mu());
   d.use_catalog(options.catalog);
   std::vector<miso_b200_sim_metrics> met(n);
-  std::vector<int64_t> job_out(full ? n * size_t(max_jobs) * 6 : 0);
+  std::vector<int64_t> job_out(full ? n * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : 0);
   const bool want_log = full && options.event_log != nullptr;
   int64_t log_cap = want_log ? 64 * int64_t(max_jobs) + 1024 : 0;
   int64_t stp_cap = full ? 16 * int64_t(max_jobs) + 64 : 0;
@@ -264,7 +291,7 @@ inline std::vector<MetricsReport> run_simulation_batch(
     Device::check(miso_b200_simulate_batch_host(
         d.ctx(), &c, static_cast<int>(n), static_cast<int>(n), nullptr, optsta ? sc.data() : nullptr,
         ta.offsets.data(), ta.arrival.data(), ta.base.data(), ta.speeds.data(), ta.mem.data(),
-        ta.qos.data(), seeds.data(), met.data(), full ? job_out.data() : nullptr,
+        ta.qos.data(), ta.inst.data(), seeds.data(), met.data(), full ? job_out.data() : nullptr,
         want_log ? log.data() : nullptr, log_cap, full ? stp.data() : nullptr, stp_cap,
         full ? 0u : MISO_B200_SIM_JCT_ONLY));
     int64_t need_log = 0, need_stp = 0;
@@ -279,12 +306,14 @@ inline std::vector<MetricsReport> run_simulation_batch(
   out.reserve(n);
   for (size_t i = 0; i < n; ++i) {
     if (met[i].status) detail::throw_status(met[i].status);
-    out.push_back(detail::make_report(
-        *traces[i], options.policy, met[i], full ? job_out.data() + i * size_t(max_jobs) * 6 : nullptr,
-        full ? stp.data() + i * 2 * size_t(stp_cap) : nullptr,
-        full ? std::min<int64_t>(met[i].stp_points, stp_cap) : 0));
+    const int64_t* jo = full ? job_out.data() + i * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : nullptr;
+    std::vector<std::string> ids;
+    if (full) ids = detail::job_ids(*traces[i], jo, met[i].job_count);
+    out.push_back(detail::make_report(*traces[i], options.policy, met[i], jo, full ? &ids : nullptr,
+                                      full ? stp.data() + i * 2 * size_t(stp_cap) : nullptr,
+                                      full ? std::min<int64_t>(met[i].stp_points, stp_cap) : 0));
     if (want_log)
-      detail::render_log(*traces[i], log.data() + i * size_t(log_cap),
+      detail::render_log(ids, log.data() + i * size_t(log_cap),
                          std::min<int64_t>(met[i].log_records, log_cap), *options.event_log);
   }
   return out;

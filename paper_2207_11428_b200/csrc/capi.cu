@@ -444,9 +444,9 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                              miso_b200_log_record* log, int64_t log_cap, double* stp_series,
                              int64_t stp_cap, void* stream) {
   return miso_b200_simulate_batch_ex(ctx, opt, n_seeds, task_trace, static_counts, job_offsets,
-                                     arrival_s, base_s, speeds5, mem_gb, qos_kind, rng_seed,
-                                     metrics, job_jct_us, nullptr, log, log_cap, stp_series,
-                                     stp_cap, 0u, stream);
+                                     arrival_s, base_s, speeds5, mem_gb, qos_kind, nullptr,
+                                     rng_seed, metrics, job_jct_us, nullptr, log, log_cap,
+                                     stp_series, stp_cap, 0u, stream);
 }
 
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
@@ -454,10 +454,11 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
                                 const int32_t* job_offsets, const double* arrival_s,
                                 const double* base_s, const double* speeds5,
                                 const uint8_t* mem_gb, const int8_t* qos_kind,
-                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
-                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
-                                int64_t log_cap, double* stp_series, int64_t stp_cap,
-                                unsigned flags, void* stream) {
+                                const uint8_t* instances, const uint64_t* rng_seed,
+                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
+                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
+                                double* stp_series, int64_t stp_cap, unsigned flags,
+                                void* stream) {
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (flags & ~MISO_B200_SIM_JCT_ONLY) return fail(MISO_B200_E_INVALID, "unknown flags");
   if ((flags & MISO_B200_SIM_JCT_ONLY) && stp_series)
@@ -506,10 +507,20 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
         return fail(MISO_B200_E_INVALID, "static partition of task " + std::to_string(i) + " is not feasible");
   }
   CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<uint8_t> inst;
+  if (instances && offs[size_t(n_traces)] > offs[0]) {  // capacity includes every clone
+    inst.resize(size_t(offs[size_t(n_traces)]));
+    CUDA_TRY(cudaMemcpyAsync(inst.data(), instances, inst.size(), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
   int max_jobs = 0;
   for (int i = 0; i < n_traces; ++i) {
-    const int J = offs[i + 1] - offs[i];
+    int J = offs[i + 1] - offs[i];
     if (J < 1) return fail(MISO_B200_E_INVALID, "trace has no jobs");  // sim.hpp:210
+    for (int q = offs[i]; !inst.empty() && q < offs[i + 1]; ++q) {
+      if (inst[size_t(q)] < 1) return fail(MISO_B200_E_INVALID, "instance count must be >= 1");
+      J += inst[size_t(q)] - 1;
+    }
     max_jobs = std::max(max_jobs, J);
   }
   if (!ctx->lut_valid) {
@@ -552,6 +563,7 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
   b.base_s = base_s;
   b.speeds5 = speeds5;
   b.mem_gb = mem_gb;
+  b.instances = instances;
   b.qos_kind = qos_kind;
   b.rng_seed = rng_seed;
   b.spare_lut = ctx->d_spare_lut;
@@ -596,9 +608,9 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
                                   const uint8_t* static_counts, const int32_t* job_offsets,
                                   const double* arrival_s, const double* base_s,
                                   const double* speeds5, const uint8_t* mem_gb,
-                                  const int8_t* qos_kind, const uint64_t* rng_seed,
-                                  miso_b200_sim_metrics* metrics, int64_t* job_out,
-                                  miso_b200_log_record* log, int64_t log_cap,
+                                  const int8_t* qos_kind, const uint8_t* instances,
+                                  const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                  int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
                                   double* stp_series, int64_t stp_cap, unsigned flags) {
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (n_tasks < 0 || n_traces < 0) return fail(MISO_B200_E_INVALID, "negative count");
@@ -613,12 +625,20 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
     for (int t = 0; t < n_tasks; ++t)
       if (task_trace[t] < 0 || task_trace[t] >= n_traces) return fail(MISO_B200_E_INVALID, "task_trace out of range");
   int max_jobs = 0;
-  for (int i = 0; i < n_traces; ++i) max_jobs = std::max(max_jobs, job_offsets[i + 1] - job_offsets[i]);
+  for (int i = 0; i < n_traces; ++i) {
+    int Jt = job_offsets[i + 1] - job_offsets[i];
+    for (int q = job_offsets[i]; instances && q < job_offsets[i + 1]; ++q) {
+      if (instances[q] < 1) return fail(MISO_B200_E_INVALID, "instance count must be >= 1");
+      Jt += instances[q] - 1;
+    }
+    max_jobs = std::max(max_jobs, Jt);
+  }
   const size_t J = size_t(job_offsets[n_traces]);
   DeviceGuard g(ctx->device);
   if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
   cudaStream_t s = ctx->streams[0];
-  DevBuf d_tt, d_sc, d_off, d_arr, d_base, d_sp, d_mem, d_qos, d_seed, d_met, d_jo, d_log, d_stp;
+  DevBuf d_tt, d_sc, d_off, d_arr, d_base, d_sp, d_mem, d_qos, d_inst, d_seed, d_met, d_jo, d_log,
+      d_stp;
   int rc;
   if ((rc = upload(d_tt, task_trace, task_trace ? size_t(n_tasks) : 0, s))) return rc;
   if ((rc = upload(d_sc, static_counts, static_counts ? size_t(n_tasks) * 5 : 0, s))) return rc;
@@ -628,9 +648,10 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if ((rc = upload(d_sp, speeds5, J * 5, s))) return rc;
   if ((rc = upload(d_mem, mem_gb, J, s))) return rc;
   if ((rc = upload(d_qos, qos_kind, J, s))) return rc;
+  if ((rc = upload(d_inst, instances, instances ? J : 0, s))) return rc;
   if ((rc = upload(d_seed, rng_seed, size_t(n_tasks), s))) return rc;
   if ((rc = alloc_out(d_met, sizeof(miso_b200_sim_metrics) * size_t(n_tasks)))) return rc;
-  const size_t jo_n = job_out ? size_t(n_tasks) * size_t(max_jobs) * 6 : 0;
+  const size_t jo_n = job_out ? size_t(n_tasks) * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : 0;
   if ((rc = alloc_out(d_jo, jo_n * sizeof(int64_t)))) return rc;
   const size_t log_n = log ? size_t(n_tasks) * size_t(std::max<int64_t>(log_cap, 0)) : 0;
   if ((rc = alloc_out(d_log, log_n * sizeof(miso_b200_log_record)))) return rc;
@@ -641,7 +662,8 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
       static_cast<const int32_t*>(d_off.p), static_cast<const double*>(d_arr.p),
       static_cast<const double*>(d_base.p), static_cast<const double*>(d_sp.p),
       static_cast<const uint8_t*>(d_mem.p), static_cast<const int8_t*>(d_qos.p),
-      static_cast<const uint64_t*>(d_seed.p), static_cast<miso_b200_sim_metrics*>(d_met.p),
+      static_cast<const uint8_t*>(d_inst.p), static_cast<const uint64_t*>(d_seed.p),
+      static_cast<miso_b200_sim_metrics*>(d_met.p),
       nullptr, static_cast<int64_t*>(d_jo.p), static_cast<miso_b200_log_record*>(d_log.p),
       log ? log_cap : 0, static_cast<double*>(d_stp.p), stp_series ? stp_cap : 0, flags, s);
   if (rc) return rc;

@@ -40,7 +40,7 @@ enum Phase : uint8_t { kQueued = 0, kMps = 1, kCkpt = 2, kRunning = 3, kIdle = 4
 enum Mode : uint8_t { kGpuIdle = 0, kGpuMig = 1, kGpuMps = 2, kGpuReconfig = 3 };
 enum EvKind : uint32_t { kEvArrival = 0, kEvMpsEnd = 1, kEvReconfigDone = 2, kEvCkptDone = 3,
                          kEvCompletion = 4 };
-enum JobFlag : uint8_t { kRunState = 1, kDone = 2, kHasEst = 4 };
+enum JobFlag : uint8_t { kRunState = 1, kDone = 2, kHasEst = 4, kSpawned = 8 };
 
 constexpr int64_t kNoEvent = INT64_MAX;
 
@@ -54,8 +54,10 @@ struct DJob {
   int16_t gpu;
   uint8_t phase, slice, mem, min_kind, flags;
   int8_t qos;
-  int8_t slot;  // optsta slot index on its GPU
-  uint8_t pad[5];
+  int8_t slot;      // optsta slot index on its GPU
+  uint8_t inst;     // JobProfile::instance_count (clones: 1)
+  int16_t clone_k;  // clones: k of "parent#k"; trace jobs: 0
+  int32_t parent;   // clones: parent job index; trace jobs: -1
 };
 
 struct DGpu {
@@ -102,7 +104,8 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   int W;                // words per freemask row
   LogRec* log;
   int64_t log_cap, log_n;
-  int J, G;
+  int J, G;             // J: job capacity (trace jobs + every possible clone)
+  int J_used;           // trace jobs + clones spawned so far (jobs_.size() in the reference)
   int qhead, qtail;
   int64_t now;
   uint64_t seq;
@@ -411,11 +414,67 @@ __device__ void start_running(Ctx& c, int ji, int s) {
   log_rec(c, kLogStart, j.gpu, ji, static_cast<uint8_t>(s), 0, 0, r);
 }
 
-// sim.hpp:457-461 (spawn_instances is a no-op for instance_count == 1, the only supported)
-__device__ __forceinline__ void cache_estimates(DJob& j, const double* est) {
+// sim.hpp:432-455: a multi-instance job's clones are appended at its first admission (nopart,
+// optsta) or estimate caching (miso, oracle): copies of the profile ("parent#k"), the parent's
+// arrival as FCFS position and JCT baseline, the parent's estimates, queued in FCFS order
+// (arrival_us, index == entry_seq). The STP window grows to the clone's index; jobs in between
+// that have not arrived yet contribute +0.0 (exact).
+__device__ void spawn_instances(Ctx& c, int pi) {
+  DJob& par = c.jobs[pi];
+  if ((par.flags & kSpawned) || par.inst <= 1) return;
+  par.flags |= kSpawned;
+  for (int k = 1; k < par.inst; ++k) {
+    const int ci = c.J_used;
+    if (ci >= c.J) {  // capacity is the trace's instance total; cannot happen
+      fail(c, MISO_B200_SIM_INVARIANT);
+      return;
+    }
+    DJob& j = c.jobs[ci];
+    j.base = par.base;
+    j.remaining = par.base;
+    j.consumed = 0;
+    j.rate = 0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      j.truth[q] = par.truth[q];
+      j.est[q] = par.est[q];
+      j.acc[q] = 0;
+    }
+    j.arrival_us = par.arrival_us;
+    j.last_update_us = par.arrival_us;
+    j.first_progress_us = -1;
+    j.completion_us = -1;
+    j.epoch = 0;
+    j.gpu = -1;
+    j.phase = kQueued;
+    j.slice = 4;
+    j.mem = par.mem;
+    j.min_kind = par.min_kind;
+    j.qos = par.qos;
+    j.flags = static_cast<uint8_t>((par.flags & kHasEst) | kSpawned);
+    j.slot = -1;
+    j.inst = 1;
+    j.clone_k = static_cast<int16_t>(k);
+    j.parent = pi;
+    __syncwarp();
+    c.J_used = ci + 1;
+    sync_jst(c, ci, j);
+    if (ci + 1 > c.n_arrived) {
+      if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;
+      c.n_arrived = ci + 1;
+    }
+    log_rec(c, kLogSpawn, -1, ci, 0, static_cast<uint32_t>(pi), 0, 0);
+    enqueue(c, ci);
+  }
+}
+
+// sim.hpp:457-461
+__device__ void cache_estimates(Ctx& c, int ji, const double* est) {
+  DJob& j = c.jobs[ji];
 #pragma unroll
   for (int k = 0; k < 5; ++k) j.est[k] = est[k];
   j.flags |= kHasEst;
+  spawn_instances(c, ji);
 }
 
 // sim.hpp:670-680 with simulate_mps_rates / interp_speed (profiles.hpp:391-431)
@@ -501,8 +560,8 @@ __device__ void finish_profiling(Ctx& c, int gi) {
   const int n = g.nroster;
   if (!c.p->noisy) {
     for (int i = 0; i < n; ++i) {
-      DJob& j = c.jobs[g.roster[i]];
-      cache_estimates(j, j.truth);
+      const int ji = g.roster[i];
+      cache_estimates(c, ji, c.jobs[ji].truth);
     }
   } else {
     const uint64_t nonce = ++c.nonce;
@@ -518,7 +577,7 @@ __device__ void finish_profiling(Ctx& c, int gi) {
       double ei[5];
 #pragma unroll
       for (int k = 0; k < 5; ++k) ei[k] = __shfl_sync(0xffffffffu, e[k], i);
-      cache_estimates(c.jobs[g.roster[i]], ei);
+      cache_estimates(c, g.roster[i], ei);
     }
   }
   reopt_and_apply(c, gi, true);
@@ -623,8 +682,8 @@ __device__ void settle_admissions(Ctx& c, int gi) {
   DGpu& g = c.gpus[gi];
   if (c.p->policy == MISO_B200_POLICY_ORACLE)
     for (int i = 0; i < g.nroster; ++i) {
-      DJob& j = c.jobs[g.roster[i]];
-      if (!(j.flags & kHasEst)) cache_estimates(j, j.truth);
+      const int ji = g.roster[i];
+      if (!(c.jobs[ji].flags & kHasEst)) cache_estimates(c, ji, c.jobs[ji].truth);
     }
   bool all_est = true;
   for (int i = 0; i < g.nroster; ++i) all_est = all_est && (c.jobs[g.roster[i]].flags & kHasEst);
@@ -721,6 +780,7 @@ __device__ bool admit_optsta(Ctx& c, int ji) {
   jm.slot = static_cast<int8_t>(bi);
   log_rec(c, kLogAdmitSlot, bg, ji, static_cast<uint8_t>(bi), 0, 0, 0);
   start_running(c, ji, g.slot_kind[bi]);
+  spawn_instances(c, ji);
   return true;
 }
 
@@ -745,6 +805,7 @@ __device__ bool admit_nopart(Ctx& c, int ji) {
   c.jobs[ji].gpu = static_cast<int16_t>(b);
   log_rec(c, kLogAdmit, b, ji, 0, 0, 0, 0);
   start_running(c, ji, 4);
+  spawn_instances(c, ji);
   return true;
 }
 
@@ -1010,7 +1071,14 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   const int lane = lane_id();
   const int tr = b.task_trace ? b.task_trace[warp] : warp;  // task -> trace
   const int J0 = b.job_offsets[tr];
-  const int J = b.job_offsets[tr + 1] - J0;
+  const int JT = b.job_offsets[tr + 1] - J0;  // trace jobs
+  // capacity: every job's instance_count (sim.hpp:242); clones occupy [JT, J)
+  int extra = 0;
+  if (b.instances)
+    for (int i = lane_id(); i < JT; i += 32) extra += b.instances[J0 + i] > 1 ? b.instances[J0 + i] - 1 : 0;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) extra += __shfl_xor_sync(0xffffffffu, extra, off);
+  const int J = JT + extra;
   const int G = prm.cluster_size;
   unsigned char* ws = b.workspace + size_t(warp) * b.ws_stride;
   Ctx c;
@@ -1037,6 +1105,7 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.stp_series = b.stp_series ? b.stp_series + size_t(warp) * 2 * b.stp_cap : nullptr;
   c.stp_cap = b.stp_cap;
   c.J = J;
+  c.J_used = JT;
   c.G = G;
   c.qhead = c.qtail = 0;
   c.now = 0;
@@ -1058,7 +1127,7 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.w = w;
 
   // ---- init_jobs / init_gpus (sim.hpp:240-276), lanes in parallel ----
-  for (int i = lane; i < J; i += 32) {
+  for (int i = lane; i < JT; i += 32) {
     DJob& j = c.jobs[i];
     const int64_t a = us_from_s(b.arrival_s[J0 + i]);
     j.remaining = b.base_s[J0 + i];
@@ -1088,6 +1157,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     j.min_kind = static_cast<uint8_t>(mk < 0 ? 0xFF : mk);
     j.flags = 0;
     j.slot = -1;
+    j.inst = b.instances ? b.instances[J0 + i] : 1;
+    j.clone_k = 0;
+    j.parent = -1;
     c.jst[i] = kQueued | (4 << 3);
     Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
     s.t = a;
@@ -1122,6 +1194,10 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     }
     c.slots[J + gi].t = kNoEvent;
   }
+  for (int i = JT + lane; i < J; i += 32) {  // clone slots: no event, not arrived
+    c.slots[i].t = kNoEvent;
+    c.jst[i] = kQueued | (4 << 3);
+  }
   for (int i = lane; i < J; i += 32) c.rate_eff[i] = 0.0;
   for (int wi = lane; wi < 5 * c.W; wi += 32) {  // optsta: every GPU starts with all slots free
     const int k = wi / c.W, w = wi % c.W;
@@ -1134,9 +1210,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     c.freemask[wi] = v;
   }
   __syncwarp();
-  c.seq = static_cast<uint64_t>(J);
+  c.seq = static_cast<uint64_t>(JT);  // one arrival event per trace job (sim.hpp:219)
   bool bad_job = false;
-  for (int i = 0; i < J; ++i) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
+  for (int i = 0; i < JT; ++i) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
 
   // ---- event loop (sim.hpp:221-233) ----
   if (bad_job && (prm.policy == MISO_B200_POLICY_MISO || prm.policy == MISO_B200_POLICY_ORACLE))
@@ -1161,20 +1237,24 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   }
 
   // ---- finalize (sim.hpp:902-949) ----
+  const int JU = c.J_used;  // jobs_.size(): trace jobs + spawned clones (sim.hpp:903-913)
   if (b.job_out) {  // per-job report inputs (sim.hpp:916-929), lanes in parallel
-    int64_t* o = b.job_out + size_t(warp) * size_t(b.max_jobs) * 6;
-    for (int i = lane; i < J; i += 32) {
+    int64_t* o = b.job_out + size_t(warp) * size_t(b.max_jobs) * kJobOutFields;
+    for (int i = lane; i < JU; i += 32) {
       const DJob& j = c.jobs[i];
-      o[6 * i] = (j.flags & kDone) ? j.completion_us : -1;
+      int64_t* r = o + size_t(kJobOutFields) * i;
+      r[0] = (j.flags & kDone) ? j.completion_us : -1;
 #pragma unroll
-      for (int k = 0; k < 5; ++k) o[6 * i + 1 + k] = j.acc[k];
+      for (int k = 0; k < 5; ++k) r[1 + k] = j.acc[k];
+      r[6] = j.parent;
+      r[7] = j.clone_k;
     }
   }
   SimMetrics m;
   m.status = c.status;
-  m.job_count = J;
+  m.job_count = JU;
   m.completed_count = c.done_count;
-  m.completed = c.done_count == J;
+  m.completed = c.done_count == JU;
   m.repartitions = c.repartitions;
   m.migrations = c.migrations;
   m.mps_sessions = c.mps_sessions;
@@ -1183,9 +1263,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   m.stp_points = c.stp_points;
   double totals[5] = {0, 0, 0, 0, 0};
   double jct_sum = 0;
-  for (int i = 0; i < J; ++i) {
+  for (int i = 0; i < JU; ++i) {
     const DJob& j = c.jobs[i];
-    if (b.job_jct_us && !b.task_trace && lane == 0) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
+    if (b.job_jct_us && !b.task_trace && lane == 0 && i < JT) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
     if (!(j.flags & kDone)) continue;
     jct_sum += s_from_us(j.completion_us - j.arrival_us);
 #pragma unroll
@@ -1204,7 +1284,7 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   m.makespan_s = inf;
   m.stp_time_avg = 0;
   if (m.completed) {
-    m.avg_jct_s = jct_sum / static_cast<double>(J);
+    m.avg_jct_s = jct_sum / static_cast<double>(JU);
     m.makespan_s = s_from_us(c.last_completion - c.first_progress);
     if (c.last_completion > c.first_progress)
       m.stp_time_avg = c.stp_integral / s_from_us(c.last_completion - c.first_progress);

@@ -18,7 +18,11 @@ enum LogKind : uint8_t {
   kLogPartition = MISO_B200_LOG_PARTITION, kLogAssign = MISO_B200_LOG_ASSIGN,
   kLogComplete = MISO_B200_LOG_COMPLETE, kLogShrink = MISO_B200_LOG_SHRINK,
   kLogAdmitSlot = MISO_B200_LOG_ADMIT_SLOT, kLogMigrate = MISO_B200_LOG_MIGRATE,
+  kLogSpawn = MISO_B200_LOG_SPAWN,
 };
+
+// job_out record per job: completion_us, acc_us[5], parent (-1), clone ordinal k
+constexpr int kJobOutFields = 8;
 
 struct SimParams {
   int policy, cluster_size, noisy, check_invariants;
@@ -38,6 +42,7 @@ struct SimBatch {
   const double* base_s;
   const double* speeds5;
   const uint8_t* mem_gb;
+  const uint8_t* instances;     // per trace job, JobProfile::instance_count (nullable: all 1)
   const int8_t* qos_kind;
   const uint64_t* rng_seed;
   const int8_t* spare_lut;

@@ -60,7 +60,7 @@ lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_do
 lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
     [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
 lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
-    [C.c_void_p] * 13 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
+    [C.c_void_p] * 14 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
 
 
 @dataclass
@@ -95,6 +95,7 @@ class Trace:
     mem_gb: np.ndarray
     qos_kind: Optional[np.ndarray] = None
     seed: int = 0
+    instances: Optional[np.ndarray] = None  # JobProfile::instance_count (None: all 1)
 
     @property
     def n(self) -> int:
@@ -126,22 +127,23 @@ class TraceBatch(list):
     simulate_batch / best_static_partition upload them without re-concatenating. Slicing
     with a step of 1 keeps the CSR form."""
 
-    csr = None  # (offsets int32 (n+1), arrival, duration, speeds5 (J,5), mem u8, qos i8)
+    csr = None  # (offsets int32 (n+1), arrival, duration, speeds5 (J,5), mem u8, qos i8, inst u8|None)
 
     def __getitem__(self, i):
         r = super().__getitem__(i)
         if isinstance(i, slice) and self.csr is not None and i.step in (None, 1):
             lo, hi, _ = i.indices(len(self))
-            off, a, d, sp, mem, qos = self.csr
+            off, a, d, sp, mem, qos, inst = self.csr
             o0, o1 = int(off[lo]), int(off[hi])
             b = TraceBatch(r)
-            b.csr = (off[lo:hi + 1] - o0, a[o0:o1], d[o0:o1], sp[o0:o1], mem[o0:o1], qos[o0:o1])
+            b.csr = (off[lo:hi + 1] - o0, a[o0:o1], d[o0:o1], sp[o0:o1], mem[o0:o1], qos[o0:o1],
+                     None if inst is None else inst[o0:o1])
             return b
         return r
 
 
 def _csr(traces):
-    """(offsets, arrival, duration, speeds5, mem, qos) of a trace list."""
+    """(offsets, arrival, duration, speeds5, mem, qos, instances or None) of a trace list."""
     if isinstance(traces, TraceBatch) and traces.csr is not None:
         return traces.csr
     offs = np.zeros(len(traces) + 1, np.int32)
@@ -149,7 +151,9 @@ def _csr(traces):
     cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
     return (offs, cat(lambda t: t.arrival_s, np.float64), cat(lambda t: t.duration_s, np.float64),
             cat(lambda t: t.speeds5, np.float64).reshape(-1, 5), cat(lambda t: t.mem_gb, np.uint8),
-            cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8))
+            cat(lambda t: (t.qos_kind if t.qos_kind is not None else np.full(t.n, -1)), np.int8),
+            None if all(t.instances is None for t in traces) else
+            cat(lambda t: (t.instances if t.instances is not None else np.ones(t.n)), np.uint8))
 
 
 def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float = 60.0,
@@ -173,7 +177,7 @@ def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float 
     out = TraceBatch(Trace(a[i], d[i], sp[i], mem[i], None, int(sd[i])) for i in range(n))
     offs = (np.arange(n + 1) * job_count).astype(np.int32)
     out.csr = (offs, a.reshape(-1), d.reshape(-1), sp.reshape(-1, 5), mem.reshape(-1).astype(np.uint8),
-               np.full(n * job_count, -1, np.int8))
+               np.full(n * job_count, -1, np.int8), None)
     return out
 
 
@@ -209,7 +213,9 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     dev = torch.device("cuda", ctx.device)
     st_obj = stream if stream is not None else torch.cuda.current_stream(dev)
     S = len(traces) if task_trace is None else len(task_trace)
-    offs, arr, dur, sp, mem, qos = _csr(traces)
+    offs, arr, dur, sp, mem, qos, inst = _csr(traces)
+    if inst is not None and (np.asarray(inst) < 1).any():
+        raise ValueError("instance count must be >= 1")
     if rng_seeds is None:
         tseeds = np.array([t.seed for t in traces], np.uint64)
         rng_seeds = tseeds if task_trace is None else tseeds[np.asarray(task_trace, np.int64)]
@@ -221,6 +227,7 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         d_offs, d_arr, d_dur, d_sp = T(offs), T(arr), T(dur), T(sp)
         d_mem, d_qos, d_seed = T(mem), T(qos), T(seeds.view(np.int64))
         d_tt = None if task_trace is None else T(np.asarray(task_trace, np.int32))
+        d_inst = None if inst is None else T(np.asarray(inst, np.uint8))
         d_sc = None if static_partitions is None else \
             T(np.asarray(static_partitions, np.uint8).reshape(S, 5))
         d_met = torch.empty(S * METRICS_DTYPE.itemsize, dtype=torch.uint8, device=dev)
@@ -231,10 +238,10 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
                                                p(d_arr), p(d_dur),
-                                               p(d_sp), p(d_mem), p(d_qos), p(d_seed), p(d_met),
+                                               p(d_sp), p(d_mem), p(d_qos), p(d_inst), p(d_seed), p(d_met),
                                                p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
                                                1 if jct_only else 0, st_obj.cuda_stream))
-    keep = (d_offs, d_arr, d_dur, d_sp, d_mem, d_qos, d_seed, d_tt, d_sc)  # alive until done
+    keep = (d_offs, d_arr, d_dur, d_sp, d_mem, d_qos, d_seed, d_tt, d_sc, d_inst)  # alive until done
 
     def finish() -> SimResult:
         st_obj.synchronize()
@@ -308,6 +315,8 @@ def render_log(records: np.ndarray, job_ids=None) -> str:
             line = f"admit gpu={g} job={jid(j)} slot={int(r['x'])}"
         elif k == 13:
             line = f"migrate job={jid(j)} gpu={g} slot={a} slice={KIND_NAMES[int(r['x'])]}"
+        elif k == 14:
+            line = f"spawn job={jid(j)} parent={jid(a)}"
         else:
             line = f"?kind={k}"
         out.append(f"{t} {line}\n")
@@ -344,7 +353,7 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
     catc = np.asarray(cat, np.uint8).reshape(-1, 5)
     largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
     # min_slice_for per job (topology.hpp:68-72), then the largest per trace (sim.hpp:1036-1041)
-    offs, _, _, _, mem, qos = _csr(traces)
+    offs, _, _, _, mem, qos, _ = _csr(traces)
     qg = np.where(qos >= 0, np.asarray(GPC)[np.maximum(qos, 0)], 0)
     ok = (np.asarray(MEM_GB)[None, :] >= mem[:, None].astype(np.int64)) & \
          (np.asarray(GPC)[None, :] >= qg[:, None])

@@ -24,14 +24,8 @@ def test_reference_optimizer_tests_against_b200():
 
 # The reference's simulator, experiment and acceptance test files, compiled unmodified with
 # run_simulation / best_static_partition / run_experiment_in_memory routed to the B200 binding
-# (tools/dropin/prelude_sim.hpp). The only expected failures are the two tests that stress
-# multi-instance clone spawning (JobProfile::instance_count > 1, API-only in the reference and
-# never produced by generate_trace), which the device engine rejects with std::invalid_argument.
-EXPECTED_FAIL = {
-    "sim": {"SimEngine.MultiInstanceJobsSpawnClones"},
-    "experiment": set(),
-    "acceptance": {"Acceptance.AccountingInvariants"},
-}
+# (tools/dropin/prelude_sim.hpp): every test passes, multi-instance clone spawning included.
+EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set()}
 TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9}
 
 
@@ -60,3 +54,15 @@ def test_experiment_csv_json_byte_identical_to_reference():
     r = subprocess.run([str(b)], capture_output=True, text=True, timeout=1200, cwd=b.parent)
     print(r.stdout)
     assert r.returncode == 0 and "PARITY OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_simulator_reports_and_logs_byte_identical_with_clones():
+    """run_simulation (sim.hpp:976) on the reference's CPU engine and through the B200 binding:
+    format_report text and event-log text identical for every policy on traces with
+    multi-instance jobs (clones), QoS floors and 2-4 GPUs; best_static_partition's choice equal."""
+    b = BIN.parent / "sim_parity"
+    if not b.exists():
+        pytest.skip("parity binary not built (needs /root/reference at build time)")
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=1200, cwd=b.parent)
+    print(r.stdout[-3000:])
+    assert r.returncode == 0 and "SIM PARITY OK" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
