@@ -204,6 +204,16 @@ int miso_b200_generate_traces(const uint64_t* seeds, int n_traces, int job_count
                               double lo_s, double hi_s, int threads, double* arrival_s,
                               double* duration_s, double* speeds5, int* mem_gb);
 
+/* generate_trace for n_traces seeds ON THE DEVICE (one warp per trace; DEVICE pointers,
+ * stream-ordered): the same outputs as miso_b200_generate_traces, bit for bit (the reference's
+ * libm calls -- exp, pow, log1p, log, cos -- are restated from glibc 2.39's FMA variants,
+ * csrc/glibc_math*.cuh). Same validation and layout (trace r at offset r*job_count). */
+int miso_b200_generate_traces_device(miso_b200_ctx* ctx, const uint64_t* seeds, int n_traces,
+                                     int job_count, double lambda_s, double max_duration_s,
+                                     int dist, double sigma, double fixed_s, double lo_s,
+                                     double hi_s, double* arrival_s, double* duration_s,
+                                     double* speeds5, int* mem_gb, void* stream);
+
 /* run_simulation (sim.hpp:976-979) for n_seeds independent tasks at once, one warp per task,
  * DEVICE pointers. Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r owns
  * jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in

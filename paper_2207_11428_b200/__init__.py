@@ -20,7 +20,7 @@ from ._native import (  # noqa: F401
     lib_path,
 )
 from .catalog import DEFAULT_CATALOG, partition_name  # noqa: F401
-from .sim import (SimOptions, Trace, best_static_partition, generate_trace, generate_traces, render_log,  # noqa: F401
+from .sim import (SimOptions, Trace, best_static_partition, generate_trace, generate_traces, generate_traces_device, render_log,  # noqa: F401
                   simulate_batch)
 
 __all__ = [

@@ -433,6 +433,31 @@ int miso_b200_generate_traces(const uint64_t* seeds, int n_traces, int job_count
   return MISO_B200_OK;
 }
 
+int miso_b200_generate_traces_device(miso_b200_ctx* ctx, const uint64_t* seeds, int n_traces,
+                                     int job_count, double lambda_s, double max_duration_s,
+                                     int dist, double sigma, double fixed_s, double lo_s,
+                                     double hi_s, double* arrival_s, double* duration_s,
+                                     double* speeds5, int* mem_gb, void* stream) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (n_traces < 0) return fail(MISO_B200_E_INVALID, "n_traces < 0");
+  // validate_trace_spec (workload.hpp:37-46), as miso_b200_generate_trace
+  if (job_count < 1) return fail(MISO_B200_E_INVALID, "job_count must be >= 1");
+  if (!(lambda_s > 0)) return fail(MISO_B200_E_INVALID, "lambda_s must be positive");
+  if (!(max_duration_s > 0)) return fail(MISO_B200_E_INVALID, "max_duration_s must be positive");
+  if (dist < 0 || dist > 2) return fail(MISO_B200_E_INVALID, "unknown duration distribution");
+  if (dist == 0 && !(sigma > 0)) return fail(MISO_B200_E_INVALID, "lognormal sigma must be positive");
+  if (dist == 2 && !(lo_s > 0 && lo_s <= hi_s))
+    return fail(MISO_B200_E_INVALID, "uniform bounds must satisfy 0 < lo_s <= hi_s");
+  if (n_traces == 0) return MISO_B200_OK;
+  if (!seeds || !arrival_s || !duration_s || !speeds5 || !mem_gb) return fail(MISO_B200_E_INVALID, "null buffer");
+  DeviceGuard g(ctx->device);
+  const double mu = std::log(max_duration_s) - 1.2815515655446004 * sigma;  // kZ90, workload.hpp:75
+  CUDA_TRY(launch_generate_traces(seeds, n_traces, job_count, lambda_s, max_duration_s, dist, sigma,
+                                  fixed_s, lo_s, hi_s, mu, arrival_s, duration_s, speeds5, mem_gb,
+                                  static_cast<cudaStream_t>(stream)));
+  return MISO_B200_OK;
+}
+
 static int64_t us_from_s_host(double s) { return static_cast<int64_t>(std::llround(s * 1e6)); }
 
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,

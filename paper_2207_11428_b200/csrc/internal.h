@@ -38,6 +38,14 @@ struct DecideOneOut {
 };
 cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream);
 
+// Device: generate_trace for n seeds, one warp per trace (trace_kernel.cu). mu = the
+// lognormal's log(max_duration_s) - kZ90 * sigma, computed on the host as the reference does.
+cudaError_t launch_generate_traces(const uint64_t* seeds, int n, int job_count, double lambda_s,
+                                   double max_duration_s, int dist, double sigma, double fixed_s,
+                                   double lo_s, double hi_s, double mu, double* arrival_s,
+                                   double* duration_s, double* speeds5, int* mem_gb,
+                                   cudaStream_t stream);
+
 // Host: generate_trace (workload.hpp:97-114); dist_kind 0 lognormal, 1 fixed, 2 uniform.
 void host_generate_trace(uint64_t seed, int job_count, double lambda_s, double max_duration_s,
                          int dist_kind, double sigma, double fixed_s, double lo_s, double hi_s,

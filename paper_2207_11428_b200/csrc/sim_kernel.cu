@@ -1250,7 +1250,7 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
       r[7] = j.clone_k;
     }
   }
-  SimMetrics m;
+  SimMetrics m{};  // value-initialised: the padding bytes are deterministic too
   m.status = c.status;
   m.job_count = JU;
   m.completed_count = c.done_count;

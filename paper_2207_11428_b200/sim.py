@@ -142,9 +142,47 @@ class TraceBatch(list):
         return r
 
 
+class DeviceTraceBatch:
+    """Traces resident on the device (generate_traces_device): equal-length traces as CUDA
+    tensors, accepted by simulate_batch / best_static_partition without a host round trip."""
+
+    def __init__(self, seeds, arrival_s, duration_s, speeds5, mem_gb):
+        self.seeds = np.ascontiguousarray(seeds, np.uint64)
+        self.arrival_s, self.duration_s, self.speeds5, self.mem_gb = arrival_s, duration_s, speeds5, mem_gb
+        self.n, self.job_count = arrival_s.shape
+
+    def __len__(self):
+        return self.n
+
+    def __getitem__(self, i):
+        if not isinstance(i, slice) or i.step not in (None, 1):
+            raise TypeError("DeviceTraceBatch supports contiguous slices only")
+        lo, hi, _ = i.indices(self.n)
+        return DeviceTraceBatch(self.seeds[lo:hi], self.arrival_s[lo:hi], self.duration_s[lo:hi],
+                                self.speeds5[lo:hi], self.mem_gb[lo:hi])
+
+    @property
+    def csr(self):
+        import torch
+        dev = self.arrival_s.device
+        offs = torch.arange(self.n + 1, dtype=torch.int32, device=dev) * self.job_count
+        return (offs, self.arrival_s.reshape(-1), self.duration_s.reshape(-1),
+                self.speeds5.reshape(-1, 5), self.mem_gb.reshape(-1).to(torch.uint8),
+                torch.full((self.n * self.job_count,), -1, dtype=torch.int8, device=dev), None)
+
+    def to_host(self) -> "TraceBatch":
+        a, d = self.arrival_s.cpu().numpy(), self.duration_s.cpu().numpy()
+        sp, mem = self.speeds5.cpu().numpy(), self.mem_gb.cpu().numpy()
+        out = TraceBatch(Trace(a[i], d[i], sp[i], mem[i], None, int(self.seeds[i])) for i in range(self.n))
+        out.csr = (np.arange(self.n + 1, dtype=np.int32) * self.job_count, a.reshape(-1), d.reshape(-1),
+                   sp.reshape(-1, 5), mem.reshape(-1).astype(np.uint8),
+                   np.full(self.n * self.job_count, -1, np.int8), None)
+        return out
+
+
 def _csr(traces):
     """(offsets, arrival, duration, speeds5, mem, qos, instances or None) of a trace list."""
-    if isinstance(traces, TraceBatch) and traces.csr is not None:
+    if isinstance(traces, (TraceBatch, DeviceTraceBatch)) and traces.csr is not None:
         return traces.csr
     offs = np.zeros(len(traces) + 1, np.int32)
     offs[1:] = np.cumsum([t.n for t in traces])
@@ -179,6 +217,35 @@ def generate_traces(seeds: Sequence[int], job_count: int = 100, lambda_s: float 
     out.csr = (offs, a.reshape(-1), d.reshape(-1), sp.reshape(-1, 5), mem.reshape(-1).astype(np.uint8),
                np.full(n * job_count, -1, np.int8), None)
     return out
+
+
+lib.miso_b200_generate_traces_device.argtypes = [
+    C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double,
+    C.c_double, C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+
+
+def generate_traces_device(ctx: Context, seeds, job_count: int = 100, lambda_s: float = 60.0,
+                           max_duration_s: float = 7200.0, dist: str = "lognormal",
+                           sigma: float = 1.5, fixed_s: float = 600.0, lo_s: float = 60.0,
+                           hi_s: float = 7200.0, stream=None):
+    """generate_trace for many seeds ON THE DEVICE (miso_b200_generate_traces_device, one warp
+    per trace), bit-identical to generate_traces. Returns a DeviceTraceBatch (CUDA tensors
+    arrival_s (n, J), duration_s (n, J), speeds5 (n, J, 5), mem_gb (n, J) int32)."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    kind = {"lognormal": 0, "fixed": 1, "uniform": 2}[dist]
+    sd = torch.as_tensor(np.ascontiguousarray(seeds, np.uint64).view(np.int64), device=dev)
+    n = sd.numel()
+    a = torch.empty((n, job_count), dtype=torch.float64, device=dev)
+    d = torch.empty((n, job_count), dtype=torch.float64, device=dev)
+    sp = torch.empty((n, job_count, 5), dtype=torch.float64, device=dev)
+    mem = torch.empty((n, job_count), dtype=torch.int32, device=dev)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    _check(lib.miso_b200_generate_traces_device(ctx._h, sd.data_ptr(), n, job_count, lambda_s,
+                                                max_duration_s, kind, sigma, fixed_s, lo_s, hi_s,
+                                                a.data_ptr(), d.data_ptr(), sp.data_ptr(),
+                                                mem.data_ptr(), st.cuda_stream))
+    return DeviceTraceBatch(np.ascontiguousarray(seeds, np.uint64), a, d, sp, mem)
 
 
 @dataclass
@@ -217,13 +284,15 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     if inst is not None and (np.asarray(inst) < 1).any():
         raise ValueError("instance count must be >= 1")
     if rng_seeds is None:
-        tseeds = np.array([t.seed for t in traces], np.uint64)
+        tseeds = traces.seeds if isinstance(traces, DeviceTraceBatch) else \
+            np.array([t.seed for t in traces], np.uint64)
         rng_seeds = tseeds if task_trace is None else tseeds[np.asarray(task_trace, np.int64)]
     seeds = np.asarray(rng_seeds, np.uint64)
     if opts.policy == "optsta" and static_partitions is None:
         raise ValueError("optsta requires a static partition")  # sim.hpp:208-209
     with torch.cuda.stream(st_obj):
-        T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev, non_blocking=False)  # noqa: E731
+        T = lambda x: x.to(dev) if isinstance(x, torch.Tensor) else \
+            torch.from_numpy(np.ascontiguousarray(x)).to(dev, non_blocking=False)  # noqa: E731
         d_offs, d_arr, d_dur, d_sp = T(offs), T(arr), T(dur), T(sp)
         d_mem, d_qos, d_seed = T(mem), T(qos), T(seeds.view(np.int64))
         d_tt = None if task_trace is None else T(np.asarray(task_trace, np.int32))
@@ -247,10 +316,11 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         st_obj.synchronize()
         _ = keep  # inputs stay referenced until the stream has finished with them
         met = d_met.cpu().numpy().view(METRICS_DTYPE)
-        res = SimResult(met, traces=list(traces))
+        res = SimResult(met, traces=[] if isinstance(traces, DeviceTraceBatch) else list(traces))
         if want_jct:
             j = d_jct.cpu().numpy()
-            res.job_jct_us = [j[offs[i]:offs[i + 1]] for i in range(len(traces))]
+            offs_h = offs.cpu().numpy() if hasattr(offs, "cpu") else offs
+            res.job_jct_us = [j[offs_h[i]:offs_h[i + 1]] for i in range(len(traces))]
         if log_cap:
             lg = d_log.cpu().numpy().view(LOG_DTYPE).reshape(S, log_cap)
             res.logs = [lg[i, : min(log_cap, int(met[i]["log_records"]))] for i in range(S)]
@@ -354,6 +424,8 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
     largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
     # min_slice_for per job (topology.hpp:68-72), then the largest per trace (sim.hpp:1036-1041)
     offs, _, _, _, mem, qos, _ = _csr(traces)
+    if hasattr(mem, "cpu"):  # device-resident batch: the feasibility pass runs on host copies
+        offs, mem, qos = offs.cpu().numpy(), mem.cpu().numpy(), qos.cpu().numpy()
     qg = np.where(qos >= 0, np.asarray(GPC)[np.maximum(qos, 0)], 0)
     ok = (np.asarray(MEM_GB)[None, :] >= mem[:, None].astype(np.int64)) & \
          (np.asarray(GPC)[None, :] >= qg[:, None])

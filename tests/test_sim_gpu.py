@@ -176,3 +176,46 @@ def test_best_static_partition_matches_reference(ctx, ref):
         assert np.array_equal(np.isinf(table), np.isinf(wt))
         fin = ~np.isinf(wt)
         assert np.array_equal(table[fin].view(np.uint64), wt[fin].view(np.uint64))
+
+
+@pytest.mark.parametrize("spec", [
+    dict(job_count=1000, lambda_s=10.0),                       # config 4
+    dict(job_count=257, lambda_s=60.0, sigma=0.7),
+    dict(job_count=1, lambda_s=5.0),
+    dict(job_count=333, lambda_s=0.5, dist="fixed", fixed_s=1234.5),
+    dict(job_count=500, lambda_s=30.0, dist="uniform", lo_s=60.0, hi_s=4000.0),
+    dict(job_count=90, lambda_s=30.0, max_duration_s=900.0, sigma=3.0),
+])
+def test_device_trace_generation_bit_exact(ctx, spec):
+    """generate_trace on the device (one warp per trace; glibc exp/pow/log1p/log/cos restated
+    from the FMA variants) == the host generator (itself bit-identical to the reference's)."""
+    import torch
+    import paper_2207_11428_b200 as m
+    seeds = [0, 1, 7, 99, 2**40 + 3, 2**63 + 11] + list(range(1000, 1058))
+    db = m.generate_traces_device(ctx, seeds, **spec)
+    a, d, sp, mem = db.arrival_s, db.duration_s, db.speeds5, db.mem_gb
+    torch.cuda.synchronize()
+    host = m.generate_traces(seeds, **spec)
+    for i, t in enumerate(host):
+        assert np.array_equal(a[i].cpu().numpy().view(np.uint64), t.arrival_s.view(np.uint64)), (spec, i, "arrival")
+        assert np.array_equal(d[i].cpu().numpy().view(np.uint64), t.duration_s.view(np.uint64)), (spec, i, "duration")
+        assert np.array_equal(sp[i].cpu().numpy().view(np.uint64), t.speeds5.view(np.uint64)), (spec, i, "speeds")
+        assert np.array_equal(mem[i].cpu().numpy(), t.mem_gb), (spec, i, "mem")
+
+
+def test_device_trace_batch_feeds_the_simulator(ctx):
+    """A device-resident trace batch goes straight into simulate_batch / best_static_partition:
+    same metrics (bits) as the host traces."""
+    import paper_2207_11428_b200 as m
+    seeds = list(range(40))
+    db = m.generate_traces_device(ctx, seeds, 300, lambda_s=20.0)
+    hb = m.generate_traces(seeds, 300, lambda_s=20.0)
+    for pol in ("nopart", "miso"):
+        o = m.SimOptions(policy=pol, cluster_size=16, predictor="noisy")
+        a = m.simulate_batch(ctx, db, o).metrics
+        b = m.simulate_batch(ctx, hb, o).metrics
+        assert a.tobytes() == b.tobytes(), pol
+    sa = m.best_static_partition(ctx, db, cluster_size=16)
+    sb = m.best_static_partition(ctx, hb, cluster_size=16)
+    assert [e for e, _ in sa] == [e for e, _ in sb]
+    assert all(np.array_equal(x.view(np.uint64), y.view(np.uint64)) for (_, x), (_, y) in zip(sa, sb))
