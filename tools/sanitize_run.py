@@ -1,0 +1,40 @@
+#!/usr/bin/env python3
+"""Small invocations of every kernel, for compute-sanitizer (memcheck / racecheck / synccheck).
+GPU only. Exercises: the search pipe kernel (aligned) and tile kernel (misaligned base), the
+predictor, the fused decide kernel, the single-roster latency kernel, the simulator (every
+policy, clones, optsta), and the device trace generator."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+sys.path.insert(0, "tests")
+import paper_2207_11428_b200 as m  # noqa: E402
+from oracle_lib import Oracle  # noqa: E402
+
+ctx = m.Context(0)
+orc = Oracle()
+s, f = orc.gen_mixes(5, 5000)
+cand, obj = ctx.optimize_batch(torch.from_numpy(s).cuda(), torch.from_numpy(f.astype(np.int32)).cuda())
+buf = torch.zeros(len(s) + 1, dtype=torch.float64, device="cuda")
+buf[1:] = torch.from_numpy(s).cuda()
+ctx.optimize_batch(buf[1:], torch.from_numpy(f.astype(np.int32)).cuda())      # misaligned -> tile kernel
+ctx.optimize_batch(s, f)                                                        # host pipeline
+t, _ = orc.gen_profiles(3, 700)
+ctx.predict_batch(t, 7, 1, 42, 1, 0.017)
+mem = np.full(700, 5, np.uint8); qos = np.full(700, -1, np.int8)
+offs = np.arange(0, 701, 7).astype(np.uint32)
+ctx.decide_batch(t, mem, qos, offs, np.arange(1, 101, dtype=np.uint64), 7, 1, 0.017)
+tr = m.generate_trace(7, 3)
+ctx.decide([(f"j{i}", (tr.speeds5[i, 4], tr.speeds5[i, 3], tr.speeds5[i, 2]), int(tr.mem_gb[i]), None) for i in range(3)], 1, 7)
+traces = m.generate_traces(range(6), 60, lambda_s=20.0)
+traces[2].instances = np.array([1] * 10 + [3] + [1] * 49, np.uint8)
+for pol in ("nopart", "oracle", "miso"):
+    m.simulate_batch(ctx, list(traces), m.SimOptions(policy=pol, cluster_size=4, predictor="noisy"),
+                     log_cap=4000, stp_cap=2000, want_jct=True)
+m.best_static_partition(ctx, list(traces), cluster_size=4)
+db = m.generate_traces_device(ctx, np.arange(8, dtype=np.uint64), 50, lambda_s=10.0)
+m.simulate_batch(ctx, db, m.SimOptions(policy="miso", cluster_size=4, predictor="noisy"))
+torch.cuda.synchronize()
+print("sanitize run ok")
