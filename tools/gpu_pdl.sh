@@ -1,4 +1,5 @@
 mkdir -p gpurun_out
-python tools/search_scaling.py > gpurun_out/scaling_dyn.json 2>&1
-MISO_B200_STATIC_TILES=1 python tools/search_scaling.py > gpurun_out/scaling_static.json 2>&1
-timeout 900 python -m pytest tests/test_search_gpu.py -x -q > gpurun_out/pytest_dyn.txt 2>&1
+python tools/search_scaling.py > gpurun_out/scaling_contig.json 2>&1
+MISO_B200_PIPE_CFG=4 python tools/search_scaling.py > gpurun_out/scaling_rr.json 2>&1
+python tools/search_scaling.py > gpurun_out/scaling_contig2.json 2>&1
+timeout 900 python -m pytest tests/test_search_gpu.py -x -q > gpurun_out/pytest_contig.txt 2>&1
