@@ -999,7 +999,7 @@ __device__ void on_completion(Ctx& c, int ji) {
   c.stp_dirty = true;
   if (ji < c.stp_cmin) c.stp_cmin = ji;
   sync_jst(c, ji, j);
-  while (c.stp_lo < c.n_arrived && (c.jobs[c.stp_lo].flags & kDone)) ++c.stp_lo;
+  while (c.stp_lo < c.n_arrived && (c.jst[c.stp_lo] & 64)) ++c.stp_lo;  // done bit, dense
   j.completion_us = c.now;
   ++c.done_count;
   if (c.now > c.last_completion) c.last_completion = c.now;
@@ -1261,15 +1261,39 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   m.events = static_cast<int64_t>(c.processed);
   m.log_records = c.log_n;
   m.stp_points = c.stp_points;
+  // sim.hpp:914-928: sums in job order over completed jobs. 32 jobs are loaded per step (one
+  // memory round trip instead of one per job) and summed sequentially through shuffles --
+  // the same additions in the same order.
   double totals[5] = {0, 0, 0, 0, 0};
   double jct_sum = 0;
-  for (int i = 0; i < JU; ++i) {
-    const DJob& j = c.jobs[i];
-    if (b.job_jct_us && !b.task_trace && lane == 0 && i < JT) b.job_jct_us[J0 + i] = (j.flags & kDone) ? j.completion_us - j.arrival_us : -1;
-    if (!(j.flags & kDone)) continue;
-    jct_sum += s_from_us(j.completion_us - j.arrival_us);
+  for (int base = 0; base < JU; base += 32) {
+    const int i = base + lane;
+    double v = 0, a[5] = {0, 0, 0, 0, 0};
+    bool done = false;
+    if (i < JU) {
+      const DJob& j = c.jobs[i];
+      done = (j.flags & kDone) != 0;
+      if (b.job_jct_us && !b.task_trace && i < JT)
+        b.job_jct_us[J0 + i] = done ? j.completion_us - j.arrival_us : -1;
+      if (done) {
+        v = s_from_us(j.completion_us - j.arrival_us);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) totals[k] += s_from_us(j.acc[k]);
+        for (int k = 0; k < 5; ++k) a[k] = s_from_us(j.acc[k]);
+      }
+    }
+    const unsigned dm = __ballot_sync(0xffffffffu, done);
+    const int cnt = JU - base < 32 ? JU - base : 32;
+    for (int t = 0; t < cnt; ++t) {
+      const double vt = __shfl_sync(0xffffffffu, v, t);
+      double at[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) at[k] = __shfl_sync(0xffffffffu, a[k], t);
+      if ((dm >> t) & 1u) {
+        jct_sum += vt;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) totals[k] += at[k];
+      }
+    }
   }
   m.queue_frac = m.mps_frac = m.checkpoint_frac = m.run_frac = m.idle_frac = 0;
   if (jct_sum > 0) {
