@@ -20,10 +20,14 @@ from ._native import (  # noqa: F401
     lib_path,
 )
 from .catalog import DEFAULT_CATALOG, partition_name  # noqa: F401
-from .sim import (SimOptions, Trace, best_static_partition, generate_trace, generate_traces, generate_traces_device, render_log,  # noqa: F401
+from .sim import (DeviceTraceBatch, SimOptions, Trace, TraceBatch, best_static_partition,  # noqa: F401
+                  generate_trace, generate_traces, generate_traces_device, render_log,
                   simulate_batch)
+from . import tracefile  # noqa: F401,E402
 
 __all__ = [
     "Context", "Assignment", "AssignmentVector", "MisoError", "DEFAULT_CATALOG",
     "partition_name", "CAND_INFEASIBLE", "CAND_BAD_M", "NUM_CANDIDATES", "KIND_NAMES",
+    "SimOptions", "Trace", "TraceBatch", "DeviceTraceBatch", "generate_trace", "generate_traces",
+    "generate_traces_device", "simulate_batch", "best_static_partition", "render_log", "tracefile",
 ]
