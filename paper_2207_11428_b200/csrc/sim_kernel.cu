@@ -106,6 +106,10 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   int64_t log_cap, log_n;
   int J, G;             // J: job capacity (trace jobs + every possible clone)
   int J_used;           // trace jobs + clones spawned so far (jobs_.size() in the reference)
+  // admission memo (optsta / nopart): capacity only grows when a slot / GPU is freed, so a
+  // failed admission of the queue head stays failed until cap_gen moves
+  uint32_t cap_gen, fail_gen;
+  int fail_job;
   int qhead, qtail;
   int64_t now;
   uint64_t seq;
@@ -737,6 +741,7 @@ __device__ __forceinline__ void occupy_slot(Ctx& c, int gi, int i, int ji) {
 }
 
 __device__ __forceinline__ void free_slot(Ctx& c, int gi, int i) {
+  ++c.cap_gen;
   DGpu& g = c.gpus[gi];
   const int k = g.slot_kind[i];
   g.slot_job[i] = -1;
@@ -752,6 +757,7 @@ __device__ __forceinline__ void free_slot(Ctx& c, int gi, int i) {
 // have distinct GPC counts, so this is: the largest feasible kind with a free slot anywhere,
 // on the lowest-numbered GPU having one, at that GPU's first free slot of the kind.
 __device__ bool admit_optsta(Ctx& c, int ji) {
+  if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // nothing freed since
   const DJob& j = c.jobs[ji];
   int bg = -1, bk = -1;
   for (int k = 4; k >= 0 && bg < 0; --k) {
@@ -768,7 +774,11 @@ __device__ bool admit_optsta(Ctx& c, int ji) {
       }
     }
   }
-  if (bg < 0) return false;
+  if (bg < 0) {
+    c.fail_job = ji;
+    c.fail_gen = c.cap_gen;
+    return false;
+  }
   DGpu& g = c.gpus[bg];
   int bi = 0;
   while (!(g.slot_kind[bi] == bk && g.slot_job[bi] == -1)) ++bi;
@@ -786,6 +796,7 @@ __device__ bool admit_optsta(Ctx& c, int ji) {
 
 // sim.hpp:465-478
 __device__ bool admit_nopart(Ctx& c, int ji) {
+  if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // no GPU went idle since
   int best = -1;
   for (int gi = lane_id(); gi < c.G; gi += 32)
     if (c.gpus[gi].mode == kGpuIdle) {
@@ -793,7 +804,11 @@ __device__ bool admit_nopart(Ctx& c, int ji) {
       break;
     }
   const unsigned any = __ballot_sync(0xffffffffu, best >= 0);
-  if (!any) return false;
+  if (!any) {
+    c.fail_job = ji;
+    c.fail_gen = c.cap_gen;
+    return false;
+  }
   // lowest id among lanes' first idle GPUs
   int b = best >= 0 ? best : INT32_MAX;
 #pragma unroll
@@ -1017,6 +1032,7 @@ __device__ void on_completion(Ctx& c, int ji) {
   roster_erase(c, g, ji);
   if (c.p->policy == MISO_B200_POLICY_NOPART) {
     g.mode = kGpuIdle;
+    ++c.cap_gen;
     return;
   }
   if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
@@ -1106,6 +1122,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.stp_cap = b.stp_cap;
   c.J = J;
   c.J_used = JT;
+  c.cap_gen = 0;
+  c.fail_gen = 0;
+  c.fail_job = -1;
   c.G = G;
   c.qhead = c.qtail = 0;
   c.now = 0;
@@ -1212,7 +1231,8 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   __syncwarp();
   c.seq = static_cast<uint64_t>(JT);  // one arrival event per trace job (sim.hpp:219)
   bool bad_job = false;
-  for (int i = 0; i < JT; ++i) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
+  for (int i = lane; i < JT; i += 32) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
+  bad_job = __any_sync(0xffffffffu, bad_job);
 
   // ---- event loop (sim.hpp:221-233) ----
   if (bad_job && (prm.policy == MISO_B200_POLICY_MISO || prm.policy == MISO_B200_POLICY_ORACLE))
