@@ -101,6 +101,8 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   int chunk;            // slots per lane: lane l owns [l*chunk, (l+1)*chunk)
   uint8_t* jst;         // [J] SoA job state for warp scans: phase | slice << 3 | done << 6
   uint32_t* freemask;   // optsta: [5][W] bit g set iff GPU g has a free slot of that kind
+  double* efftruth;     // [5][J]: effective_speed(truth[k], k, mem, qos) per job (static)
+  int64_t* arr_us;      // [J]: arrival_us per job (dense copy for coalesced scans)
   int W;                // words per freemask row
   LogRec* log;
   int64_t log_cap, log_n;
@@ -410,7 +412,7 @@ __device__ void finish_profiling(Ctx& c, int gi);
 // sim.hpp:480-489
 __device__ void start_running(Ctx& c, int ji, int s) {
   DJob& j = c.jobs[ji];
-  const double r = true_rate(j, s);
+  const double r = c.efftruth[size_t(s) * c.J + ji];  // == true_rate(j, s)
   if (c.p->check_invariants && !(r > 0)) fail(c, MISO_B200_SIM_INFEASIBLE_SLICE);
   j.slice = static_cast<uint8_t>(s);
   set_phase(c, ji, kRunning, r);  // also syncs jst
@@ -460,6 +462,9 @@ __device__ void spawn_instances(Ctx& c, int pi) {
     j.inst = 1;
     j.clone_k = static_cast<int16_t>(k);
     j.parent = pi;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) c.efftruth[size_t(q) * c.J + ci] = c.efftruth[size_t(q) * c.J + pi];
+    c.arr_us[ci] = par.arrival_us;
     __syncwarp();
     c.J_used = ci + 1;
     sync_jst(c, ci, j);
@@ -761,7 +766,7 @@ __device__ bool admit_optsta(Ctx& c, int ji) {
   const DJob& j = c.jobs[ji];
   int bg = -1, bk = -1;
   for (int k = 4; k >= 0 && bg < 0; --k) {
-    if (!(true_rate(j, k) > 0)) continue;
+    if (!(c.efftruth[size_t(k) * c.J + ji] > 0)) continue;  // == true_rate(j, k)
     for (int w0 = 0; w0 < c.W && bg < 0; w0 += 32) {
       const int wi = w0 + lane_id();
       const uint32_t word = wi < c.W ? c.freemask[k * c.W + wi] : 0u;
@@ -941,20 +946,22 @@ __device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
     int best = -1;
     double bgain = 0.0;
     int64_t barr = 0;
+    const double* eff_k = c.efftruth + size_t(kind) * c.J;
     for (int mi = c.stp_lo + lane_id(); mi < c.n_arrived; mi += 32) {
-      const uint8_t st = c.jst[mi];  // coalesced SoA state; job records only for candidates
+      // dense arrays only (coalesced): state byte, effective true speed on `kind`, the
+      // running rate (rate_eff == rate for a running job), arrival time
+      const uint8_t st = c.jst[mi];
       if ((st & 64) || (st & 7) != kRunning) continue;
       if (kind_gpc((st >> 3) & 7) >= kg) continue;
-      const DJob& m = c.jobs[mi];
-      const double ns = true_rate(m, kind);
+      const double ns = eff_k[mi];
       if (!(ns > 0)) continue;
-      const double gain = ns - m.rate;
+      const double gain = ns - c.rate_eff[mi];
       if (gain <= 0) continue;
-      if (best < 0 || gain > bgain || (gain == bgain && (m.arrival_us < barr ||
-                                                         (m.arrival_us == barr && mi < best)))) {
+      const int64_t arr = c.arr_us[mi];
+      if (best < 0 || gain > bgain || (gain == bgain && (arr < barr || (arr == barr && mi < best)))) {
         best = mi;
         bgain = gain;
-        barr = m.arrival_us;
+        barr = arr;
       }
     }
 #pragma unroll
@@ -1106,6 +1113,8 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.stp_prefix = reinterpret_cast<double*>(ws + sim_ws_prefix_off(b.max_jobs, G));
   c.jst = ws + sim_ws_jst_off(b.max_jobs, G);
   c.freemask = reinterpret_cast<uint32_t*>(ws + sim_ws_freemask_off(b.max_jobs, G));
+  c.efftruth = reinterpret_cast<double*>(ws + sim_ws_efftruth_off(b.max_jobs, G));
+  c.arr_us = reinterpret_cast<int64_t*>(ws + sim_ws_arrival_off(b.max_jobs, G));
   c.W = (G + 31) / 32;
   c.stp_cmin = INT32_MAX;
   c.stp_lo = 0;
@@ -1180,6 +1189,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     j.clone_k = 0;
     j.parent = -1;
     c.jst[i] = kQueued | (4 << 3);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) c.efftruth[size_t(k) * J + i] = effective_speed(j.truth[k], k, j.mem, j.qos);
+    c.arr_us[i] = a;
     Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
     s.t = a;
     s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;

@@ -83,8 +83,15 @@ __host__ __device__ inline size_t sim_ws_jst_off(int J, int G) {
 __host__ __device__ inline size_t sim_ws_freemask_off(int J, int G) {
   return sim_ws_jst_off(J, G) + sim_al(size_t(J + 32));
 }
-__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+// dense per-kind effective true speeds (5 x J doubles, kind-major) and arrival times (J int64)
+__host__ __device__ inline size_t sim_ws_efftruth_off(int J, int G) {
   return sim_ws_freemask_off(J, G) + sim_al(size_t(5) * ((G + 31) / 32) * 4);
+}
+__host__ __device__ inline size_t sim_ws_arrival_off(int J, int G) {
+  return sim_ws_efftruth_off(J, G) + sim_al(size_t(5) * J * 8);
+}
+__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+  return sim_ws_arrival_off(J, G) + sim_al(size_t(J) * 8);
 }
 
 size_t sim_workspace_stride(int max_jobs, int cluster_size);
