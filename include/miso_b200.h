@@ -124,6 +124,15 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
                      const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
                      double target_mae, int* entry, uint8_t* place, double* obj, double* est5);
 
+/* miso_b200_decide's execution mode. idle_us > 0 (the default: 2000, or the environment's
+ * MISO_B200_DECIDE_IDLE_US): a one-warp server kernel stays resident between calls, polling a
+ * request mailbox in mapped pinned memory, and exits after idle_us without a request (it is
+ * relaunched on the next call). While it runs, device-wide synchronisation
+ * (cudaDeviceSynchronize, cudaFree) waits for it, i.e. at most idle_us after the last call.
+ * idle_us = 0: one kernel launch per call. Stops a running server. A context serves one host
+ * thread at a time. */
+int miso_b200_decide_server(miso_b200_ctx* ctx, int idle_us);
+
 /* ---- cluster simulator (kernel (c)) ------------------------------------------------------ */
 
 /* Policies (sim.hpp:42). */

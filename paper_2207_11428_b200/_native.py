@@ -62,6 +62,7 @@ def _load():
                                          vp, vp, vp, vp, vp]
     L.miso_b200_decide.argtypes = [vp, vp, vp, vp, i32, u64, u64, i32, C.c_double,
                                    C.POINTER(i32), vp, C.POINTER(C.c_double), vp]
+    L.miso_b200_decide_server.argtypes = [vp, i32]
     L.miso_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.miso_b200_host_free.argtypes = [vp]
     L.miso_b200_host_free.restype = None
@@ -303,6 +304,15 @@ def _decide(self, jobs, nonce, rng_seed, mode=1, target_mae=0.017):
 Context.predict_batch = _predict_batch
 Context.decide_batch = _decide_batch
 Context.decide = _decide
+
+
+def _decide_server(self, idle_us):
+    """miso_b200_decide_server: idle_us > 0 keeps a one-warp server kernel resident between
+    decide() calls (exits after idle_us without a request); 0 = one launch per call."""
+    _check(lib.miso_b200_decide_server(self._h, int(idle_us)))
+
+
+Context.decide_server = _decide_server
 
 
 def host_alloc(nbytes: int):

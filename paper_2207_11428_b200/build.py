@@ -76,6 +76,14 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    tool = LIBDIR / "c1_latency"  # bench.py --config c1: the C++ caller's latency loop
+    src = ROOT / "tools" / "c1_latency.cpp"
+    if force or _stale(tool, [src, LIB, ROOT / "include" / "miso_b200.h"]):
+        cmd = ["g++", "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(src), "-o", str(tool),
+               f"-L{LIBDIR}", "-lmiso_b200", "-Wl,-rpath,$ORIGIN"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"c1_latency build failed:\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

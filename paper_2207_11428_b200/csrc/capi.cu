@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <thread>
 #include <cmath>
 #include <cstdio>
@@ -36,6 +37,14 @@ struct miso_b200_ctx {
   void* h_stage = nullptr;  // single-decision staging (miso_b200_decide)
   void* d_stage = nullptr;
   uint64_t decide_seq = 0;
+  // resident decision server (decide_server_kernel): mailbox, its stream and exit event
+  DecideMailbox* h_mail = nullptr;
+  DecideMailbox* d_mail = nullptr;
+  cudaStream_t srv_stream = nullptr;
+  cudaEvent_t srv_done = nullptr;
+  bool srv_live = false;         // launched and not yet observed to have exited
+  int64_t srv_idle_ns = -1;      // -1: not configured yet (MISO_B200_DECIDE_IDLE_US, default 2 ms)
+  std::chrono::steady_clock::time_point srv_last_ok{};
   // simulator
   int8_t* d_spare_lut = nullptr;  // max_spare_slice_for LUT of the active catalog
   bool lut_valid = false;
@@ -61,6 +70,42 @@ int cuda_fail(cudaError_t e, const char* what) {
     cudaError_t _e = (expr);                            \
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
+
+constexpr uint64_t kServerLifeNs = 500000000ull;  // a server warp lives at most 0.5 s per launch
+
+// Stop the resident decision server (if any) and wait for it to exit: used before calls that
+// synchronise the device implicitly (cudaFree) and on teardown. The server checks `stop`
+// every poll, so this costs about one PCIe round trip.
+int stop_server(miso_b200_ctx* ctx) {
+  if (!ctx->srv_live) return MISO_B200_OK;
+  *reinterpret_cast<volatile uint64_t*>(&ctx->h_mail->stop) = 1;
+  ctx->srv_live = false;
+  CUDA_TRY(cudaStreamSynchronize(ctx->srv_stream));
+  return MISO_B200_OK;
+}
+
+int64_t server_idle_ns(miso_b200_ctx* ctx) {
+  if (ctx->srv_idle_ns < 0) {
+    long us = 2000;
+    if (const char* e = getenv("MISO_B200_DECIDE_IDLE_US")) us = std::max(0l, atol(e));
+    ctx->srv_idle_ns = int64_t(us) * 1000;
+  }
+  return ctx->srv_idle_ns;
+}
+
+int launch_server(miso_b200_ctx* ctx, uint64_t last) {
+  if (!ctx->srv_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ctx->srv_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ctx->srv_done, cudaEventDisableTiming));
+  }
+  *reinterpret_cast<volatile uint64_t*>(&ctx->h_mail->stop) = 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  CUDA_TRY(launch_decide_server(ctx->d_mail, static_cast<DecideOneOut*>(ctx->d_stage), last,
+                                uint64_t(ctx->srv_idle_ns), kServerLifeNs, ctx->srv_stream));
+  CUDA_TRY(cudaEventRecord(ctx->srv_done, ctx->srv_stream));
+  ctx->srv_live = true;
+  return MISO_B200_OK;
+}
 
 // PartitionConfig::violation (topology.hpp:84-101)
 bool feasible(const uint8_t* c) {
@@ -97,6 +142,9 @@ int ensure_host_scratch(miso_b200_ctx* ctx, size_t rows, size_t inst) {
   if (!ctx->streams[1]) {
     CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[1], cudaStreamNonBlocking));
   }
+  if (rows > ctx->cap_rows || inst > ctx->cap_inst) {
+    if (int rc = stop_server(ctx)) return rc;
+  }
   if (rows > ctx->cap_rows) {
     cudaFree(ctx->d_speeds);
     ctx->d_speeds = nullptr;
@@ -131,6 +179,7 @@ struct DeviceGuard {
   }
 };
 
+
 }  // namespace
 
 extern "C" {
@@ -161,6 +210,10 @@ int miso_b200_create(int device, miso_b200_ctx** out) {
 void miso_b200_destroy(miso_b200_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard g(ctx->device);
+  stop_server(ctx);
+  if (ctx->srv_done) cudaEventDestroy(ctx->srv_done);
+  if (ctx->srv_stream) cudaStreamDestroy(ctx->srv_stream);
+  if (ctx->h_mail) cudaFreeHost(ctx->h_mail);
   cudaFree(ctx->d_speeds);
   cudaFree(ctx->d_offsets);
   cudaFree(ctx->d_cand);
@@ -363,16 +416,66 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
   a.m = m;
   a.noisy = mode;
   DecideOneOut* h = static_cast<DecideOneOut*>(ctx->h_stage);
-  cudaStream_t s = ctx->streams[0];
-  CUDA_TRY(launch_decide_one(a, static_cast<DecideOneOut*>(ctx->d_stage), s));
-  // Spin on the completion flag; after ~50 ms of spinning fall back to a stream sync, which
-  // also surfaces any launch/execution error.
-  const volatile uint64_t* flag = &h->seq;
-  for (long spin = 0; *flag != a.seq; ++spin) {
-    if (spin > (1l << 22)) {
-      CUDA_TRY(cudaStreamSynchronize(s));
-      if (*flag != a.seq) return fail(MISO_B200_E_UNEXPECTED, "decide kernel did not complete");
-      break;
+  // The result record is accepted once it names this request and its check word matches
+  // (decide_publish: the device stores it without a fence).
+  const volatile uint64_t* hw = reinterpret_cast<const volatile uint64_t*>(h);
+  auto answered = [&]() {
+    if (hw[kOutSeq] != a.seq) return false;
+    uint64_t sum = 0;
+    for (int i = 0; i < kOutEst + 5 * m; ++i)
+      if (i != kOutCheck) sum += mbx_mix(hw[i], uint64_t(i));
+    return sum == hw[kOutCheck];
+  };
+  if (server_idle_ns(ctx) > 0) {
+    // Resident server: post the request (args, then their check word), make sure a server
+    // warp is running, spin on the answer. A server that idled out between the liveness check
+    // and the post is caught by the periodic event query and relaunched; it serves the pending
+    // request because it starts from last = seq - 1.
+    if (!ctx->h_mail) {
+      CUDA_TRY(cudaHostAlloc(&ctx->h_mail, sizeof(DecideMailbox), cudaHostAllocMapped));
+      CUDA_TRY(cudaHostGetDevicePointer(&ctx->d_mail, ctx->h_mail, 0));
+      std::memset(ctx->h_mail, 0, sizeof(DecideMailbox));
+    }
+    const uint64_t* aw = reinterpret_cast<const uint64_t*>(&a);
+    uint64_t check = 0;
+    for (int i = 0; i < kArgWords; ++i) check += mbx_mix(aw[i], uint64_t(i));
+    volatile uint64_t* mw = reinterpret_cast<volatile uint64_t*>(ctx->h_mail);
+    for (int i = 0; i < kArgWords; ++i) mw[i] = aw[i];
+    mw[kArgWords] = check;
+    const auto now = std::chrono::steady_clock::now();
+    const bool surely_live =
+        ctx->srv_live && now - ctx->srv_last_ok < std::chrono::nanoseconds(ctx->srv_idle_ns / 2);
+    if (!surely_live) {
+      cudaError_t q = ctx->srv_live ? cudaEventQuery(ctx->srv_done) : cudaSuccess;
+      if (q != cudaSuccess && q != cudaErrorNotReady) return cuda_fail(q, "decide server");
+      if (q == cudaSuccess)
+        if (int rc = launch_server(ctx, a.seq - 1)) return rc;
+    }
+    int relaunches = 0;
+    for (long spin = 1; !answered(); ++spin) {
+      if ((spin & 0xfff) != 0) continue;
+      const cudaError_t q = cudaEventQuery(ctx->srv_done);
+      if (q == cudaErrorNotReady) continue;
+      if (q != cudaSuccess) {
+        ctx->srv_live = false;
+        return cuda_fail(q, "decide server");
+      }
+      if (answered()) break;
+      if (++relaunches > 3) return fail(MISO_B200_E_UNEXPECTED, "decide server did not answer");
+      if (int rc = launch_server(ctx, a.seq - 1)) return rc;
+    }
+    ctx->srv_last_ok = std::chrono::steady_clock::now();
+  } else {
+    cudaStream_t s = ctx->streams[0];
+    CUDA_TRY(launch_decide_one(a, static_cast<DecideOneOut*>(ctx->d_stage), s));
+    // Spin on the answer; after ~50 ms of spinning fall back to a stream sync, which also
+    // surfaces any launch/execution error.
+    for (long spin = 0; !answered(); ++spin) {
+      if (spin > (1l << 20)) {
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (!answered()) return fail(MISO_B200_E_UNEXPECTED, "decide kernel did not complete");
+        break;
+      }
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
@@ -380,11 +483,20 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
   if (h->cand == MISO_B200_CAND_INFEASIBLE) return 0;
   int e = -1, mm = 0;
   uint8_t p[7];
-  miso_b200_candidate(ctx, h->cand, &e, &mm, p);
+  miso_b200_candidate(ctx, static_cast<int>(h->cand), &e, &mm, p);
   if (entry) *entry = e;
   if (place) std::memcpy(place, p, size_t(m));
   if (obj) *obj = h->obj;
   return 1;
+}
+
+int miso_b200_decide_server(miso_b200_ctx* ctx, int idle_us) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (idle_us < 0) return fail(MISO_B200_E_INVALID, "idle_us must be >= 0");
+  DeviceGuard g(ctx->device);
+  if (int rc = stop_server(ctx)) return rc;
+  ctx->srv_idle_ns = int64_t(idle_us) * 1000;
+  return MISO_B200_OK;
 }
 
 int miso_b200_generate_trace(uint64_t seed, int job_count, double lambda_s,
@@ -558,6 +670,7 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
   const size_t stride = sim_workspace_stride(max_jobs, opt->cluster_size);
   const size_t need = stride * size_t(n_seeds);
   if (need > ctx->sim_ws_bytes) {
+    if (int rc = stop_server(ctx)) return rc;
     cudaFree(ctx->d_sim_ws);
     ctx->d_sim_ws = nullptr;
     CUDA_TRY(cudaMalloc(&ctx->d_sim_ws, need));
@@ -640,6 +753,10 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (n_tasks < 0 || n_traces < 0) return fail(MISO_B200_E_INVALID, "negative count");
   if (n_tasks == 0) return MISO_B200_OK;
+  {
+    DeviceGuard g(ctx->device);
+    if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
+  }
   if (!job_offsets || !arrival_s || !base_s || !speeds5 || !mem_gb || !qos_kind || !rng_seed ||
       !metrics)
     return fail(MISO_B200_E_INVALID, "null buffer");

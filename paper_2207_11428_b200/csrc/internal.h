@@ -20,7 +20,10 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
                           const double* w1, uint64_t en0, uint64_t en1, uint8_t* cand,
                           double* obj, double* est_out, cudaStream_t stream);
 
-// Single-roster decision (miso_b200_decide): everything by value, results in mapped memory.
+// Single-roster decision (miso_b200_decide). Requests and results cross PCIe through mapped
+// pinned memory with no fences: each side covers its words with a check word (the sum of
+// mbx_mix over the words), and the reader accepts a record only when the check matches, so a
+// record read while it is being written (torn) is simply read again.
 struct DecideOneArgs {
   double truth[7][3];  // (f7, f4, f3) per job
   double w2[4], w1[4];
@@ -31,12 +34,43 @@ struct DecideOneArgs {
   int8_t qos[7];
 };
 struct DecideOneOut {
-  double est[35];
+  uint64_t seq;    // the request this record answers
+  uint64_t cand;
   double obj;
-  uint64_t seq;  // written last (after a system fence): the call's completion flag
-  uint8_t cand;
+  uint64_t check;  // sum of mbx_mix over words 0..2 and the 5m est words
+  double est[35];
 };
+// Resident decision server (decide_server_kernel): the request mailbox, read by the server
+// in one PCIe round trip (20 lanes x 16 B).
+struct DecideMailbox {
+  DecideOneArgs args;  // args.seq = request number
+  uint64_t check;      // sum of mbx_mix over the kArgWords words of args
+  uint64_t stop;       // nonzero: the server exits
+};
+constexpr int kArgWords = static_cast<int>(sizeof(DecideOneArgs) / 8);
+constexpr int kArgSeqWord = static_cast<int>(__builtin_offsetof(DecideOneArgs, seq) / 8);
+constexpr int kOutWords = static_cast<int>(sizeof(DecideOneOut) / 8);
+constexpr int kOutSeq = 0, kOutCand = 1, kOutObj = 2, kOutCheck = 3, kOutEst = 4;
+static_assert(sizeof(DecideOneArgs) % 8 == 0, "mailbox records are 8-byte words");
+static_assert(sizeof(DecideMailbox) == 16 * 20, "the server fetches the mailbox as 20 x 16 B");
+static_assert(kOutWords == 39, "DecideOneOut layout");
+
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint64_t mbx_mix(uint64_t w, uint64_t i) {  // splitmix64 finaliser of (word, index)
+  uint64_t z = w + (i + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
 cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream);
+// stamps (timing probe only, else nullptr): globaltimer at request seen / roster fetched /
+// computed / published, written after each request.
+cudaError_t launch_decide_server(const DecideMailbox* mb, DecideOneOut* out, uint64_t last,
+                                 uint64_t idle_ns, uint64_t life_ns, cudaStream_t stream,
+                                 uint64_t* stamps = nullptr);
 
 // Device: generate_trace for n seeds, one warp per trace (trace_kernel.cu). mu = the
 // lognormal's log(max_duration_s) - kZ90 * sigma, computed on the host as the reference does.

@@ -102,21 +102,37 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {  // s
 }
 
 // profiles.hpp:193-205, given the entry's first three raw draws.
-__device__ __forceinline__ double perturb_with(double truth, double target_mae, const uint64_t r[3]) {
+// perturb_speed's draws (profiles.hpp:197-201): the N(0,1) magnitude and the sign coin. They
+// depend only on the entry's RNG stream, not on the speed or the target MAE.
+struct NoiseDraw {
+  double n01;
+  bool coin;
+};
+
+__device__ __forceinline__ NoiseDraw noise_draw(const uint64_t r[3]) {
   double u1 = uniform01_of(r[0]);
   const double u2 = uniform01_of(r[1]);
   if (u1 <= 0.0) u1 = 0x1.0p-53;
-  const double n01 = sqrt(-2.0 * glibc::log_fma(u1)) *
-                     glibc::cos_fma(6.283185307179586476925287 * u2);  // common.hpp:103-108
+  NoiseDraw d;
+  d.n01 = sqrt(-2.0 * glibc::log_fma(u1)) *
+          glibc::cos_fma(6.283185307179586476925287 * u2);  // common.hpp:103-108
+  d.coin = uniform01_of(r[2]) < 0.5;
+  return d;
+}
+
+__device__ __forceinline__ double perturb_apply(double truth, double target_mae, NoiseDraw d) {
   const double sigma = target_mae * sqrt(3.14159265358979323846 / 2.0);
-  const double mag = fabs(n01) * sigma;
+  const double mag = fabs(d.n01) * sigma;
   const bool up_ok = truth + mag <= 1.0;
   const bool dn_ok = truth - mag >= kSpeedFloor;
-  const bool coin = uniform01_of(r[2]) < 0.5;
-  if (up_ok && dn_ok) return coin ? truth + mag : truth - mag;
+  if (up_ok && dn_ok) return d.coin ? truth + mag : truth - mag;
   if (up_ok) return truth + mag;
   if (dn_ok) return truth - mag;
   return (1.0 - truth >= truth - kSpeedFloor) ? 1.0 : kSpeedFloor;
+}
+
+__device__ __forceinline__ double perturb_with(double truth, double target_mae, const uint64_t r[3]) {
+  return perturb_apply(truth, target_mae, noise_draw(r));
 }
 
 // profiles.hpp:193-205

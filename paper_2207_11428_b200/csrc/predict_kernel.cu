@@ -179,29 +179,108 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
 }
 
 // ---------------------------------------------------------------------------------------
-// Single-roster latency path (config 1, miso_b200_decide): the whole roster travels as kernel
-// parameters (no device-side reads of host or global input), one warp predicts -- lane
-// 2c + e perturbs entry e (4g, 3g) of column c, so the two mt19937_64 seeding chains of a
-// column run side by side -- lane 0 searches, and the results plus a completion sequence
-// number are stored straight into mapped pinned host memory (the host spins on `seq`).
+// Single-roster latency path (config 1, miso_b200_decide). One warp predicts -- lane 2c + e
+// perturbs entry e (4g, 3g) of column c -- lane 0 searches, and the result record (est rows,
+// objective, candidate, request number, check word) is stored straight into mapped pinned
+// host memory by consecutive lanes; the host accepts it when the check word matches.
+// decide_one_kernel takes the roster as a kernel parameter (one launch per call);
+// decide_server_kernel stays resident and polls a mailbox (capi.cu, miso_b200_decide).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(32) decide_one_kernel(DecideOneArgs a, DecideOneOut* out) {
-  __shared__ double s_rows[7 * 5];
+// The noise draws of one predictor call: entry e (4g, 3g) of column c < 7 is lane 2c + e.
+// Only the call's (rng_seed, nonce) picks them (profiles.hpp:234-244), so the server's second
+// warp computes them ahead for the next nonce (decide_server_kernel).
+__device__ __forceinline__ NoiseDraw call_draw(uint64_t rng_seed, uint64_t nonce, int lane) {
+  const int c = lane >> 1, e = lane & 1;
+  const uint64_t base = mix_seed(rng_seed, nonce);
+  uint64_t r[3];
+  mt64_first3(mix_seed(base, static_cast<uint64_t>(c) * 8 + 1 + e), r);
+  return noise_draw(r);
+}
+
+// optimize_partition for one roster, warp-parallel (rows: m x 5 in shared memory). Lane l
+// scores candidates kCandBase[m] + l (+ 32): the job-order DADD sum of search_rows with
+// invalid speeds poisoned to -inf; the winner is the largest objective, ties to the lowest
+// candidate id (= OptKey rank, optimizer.hpp:46-51), and NaN / -inf sums never win -- the
+// rank-ordered scan's rule, so the result is the same bits as search_any.
+template <int M>
+__device__ __forceinline__ void warp_score(const double* rows, const uint8_t (*place)[7], int c0,
+                                           int c1, uint64_t en0, uint64_t en1, double& best,
+                                           int& bc) {
+  for (int c = c0 + static_cast<int>(threadIdx.x & 31); c < c1; c += 32) {
+    const bool en = c < 64 ? ((en0 >> c) & 1ull) : ((en1 >> (c - 64)) & 1ull);
+    uint8_t p[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) p[i] = place[c][i];
+    double sum = poison(rows[p[0]]);
+#pragma unroll
+    for (int i = 1; i < M; ++i) sum = sum + poison(rows[i * 5 + p[i]]);
+    if (en && sum > best) {  // ids rise within a lane: strict '>' keeps the lowest
+      best = sum;
+      bc = c;
+    }
+  }
+}
+
+__device__ __forceinline__ uint8_t warp_search(const double* rows, int m, uint64_t en0,
+                                               uint64_t en1, const uint8_t (*place)[7],
+                                               double* obj) {
+  if (m < 1 || m > 7) {
+    *obj = 0.0;
+    return kCandBadM;  // optimizer.hpp:65-66 invalid_argument
+  }
+  double best = __longlong_as_double(0xFFF0000000000000ll);
+  int bc = kCandInfeasible;
+  // kCandBase[m], kCandBase[m + 1] packed one byte per m
+  constexpr uint64_t kBase = uint64_t(kCandBase[1]) | uint64_t(kCandBase[2]) << 8 |
+                             uint64_t(kCandBase[3]) << 16 | uint64_t(kCandBase[4]) << 24 |
+                             uint64_t(kCandBase[5]) << 32 | uint64_t(kCandBase[6]) << 40 |
+                             uint64_t(kCandBase[7]) << 48 | uint64_t(kCandBase[8]) << 56;
+  const int c0 = static_cast<int>((kBase >> (8 * (m - 1))) & 0xff);
+  const int c1 = static_cast<int>((kBase >> (8 * m)) & 0xff);
+  switch (m) {
+    case 1: warp_score<1>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 2: warp_score<2>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 3: warp_score<3>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 4: warp_score<4>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 5: warp_score<5>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 6: warp_score<6>(rows, place, c0, c1, en0, en1, best, bc); break;
+    default: warp_score<7>(rows, place, c0, c1, en0, en1, best, bc); break;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, d);
+    const int oc = __shfl_xor_sync(0xffffffffu, bc, d);
+    if (ob > best || (ob == best && oc < bc)) {
+      best = ob;
+      bc = oc;
+    }
+  }
+  *obj = bc == kCandInfeasible ? 0.0 : best;
+  return static_cast<uint8_t>(bc);
+}
+
+// pre: this lane's draw when the caller has it (the server's draw-ahead), else nullptr.
+// place: the candidate placement table (shared-memory copy in the server).
+__device__ __forceinline__ void decide_one_body(const DecideOneArgs& a, DecideOneOut& o,
+                                                const uint8_t (*place)[7],
+                                                uint64_t* cyc = nullptr,
+                                                const NoiseDraw* pre = nullptr) {
   __shared__ double s_pert[7][2];
   const int lane = threadIdx.x;
   const int m = a.m;
+  const long long c0 = clock64();
   // perturbed 4g / 3g entries (profiles.hpp:234-244), one per lane
   if (lane < 2 * m) {
     const int c = lane >> 1, e = lane & 1;
     const double truth = a.truth[c][1 + e];
     double v = truth;
-    if (a.noisy) {
-      const uint64_t base = mix_seed(a.rng_seed, a.nonce);
-      v = perturb_speed(truth, a.target_mae, mix_seed(base, static_cast<uint64_t>(c) * 8 + 1 + e));
+    if (a.noisy && a.target_mae > 0.0) {  // (target_mae <= 0: perturb_speed returns the truth)
+      v = perturb_apply(truth, a.target_mae, pre ? *pre : call_draw(a.rng_seed, a.nonce, lane));
     }
     s_pert[c][e] = v;
   }
   __syncwarp();
+  const long long c1 = clock64();
   if (lane < m) {
     // re-anchor, clamp and extrapolate exactly as predict_column (oracle-mode inputs)
     ModelW w;
@@ -214,28 +293,241 @@ __global__ void __launch_bounds__(32) decide_one_kernel(DecideOneArgs a, DecideO
     predict_column(a.truth[lane][0], s_pert[lane][0], s_pert[lane][1], lane, 0, 0, false, 0.0,
                    w, e5);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      const double v = effective_speed(e5[k], k, a.mem[lane], a.qos[lane]);
-      s_rows[lane * 5 + k] = v;
-      out->est[lane * 5 + k] = v;
+    for (int k = 0; k < 5; ++k) o.est[lane * 5 + k] = effective_speed(e5[k], k, a.mem[lane], a.qos[lane]);
+  } else if (lane < 7) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o.est[lane * 5 + k] = 0.0;
+  }
+  __syncwarp();
+  const long long c2 = clock64();
+  double ob;
+  const uint8_t c = warp_search(o.est, m, a.en0, a.en1, place, &ob);
+  if (lane == 0) {
+    o.cand = c;
+    o.obj = ob;
+    o.seq = a.seq;
+  }
+  __syncwarp();
+  if (cyc && lane == 0) {  // timing probe: perturb, predict, search cycles
+    cyc[0] = uint64_t(c1 - c0);
+    cyc[1] = uint64_t(c2 - c1);
+    cyc[2] = uint64_t(clock64() - c2);
+  }
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  return v;
+}
+
+// Store the shared record o to out (mapped host memory) with its check word; no fence: the
+// host re-reads until the check matches.
+__device__ __forceinline__ void decide_publish(const DecideOneOut& o, DecideOneOut* out, int m) {
+  const int lane = threadIdx.x;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(&o);
+  const int n = kOutEst + 5 * m;  // the record's live words: header + m est rows
+  const uint64_t mine = lane < n ? w[lane] : 0;
+  uint64_t part = lane < n && lane != kOutCheck ? mbx_mix(mine, uint64_t(lane)) : 0;
+  const uint64_t extra = lane + 32 < n ? w[lane + 32] : 0;
+  if (lane + 32 < n) part += mbx_mix(extra, uint64_t(lane + 32));
+  const uint64_t check = warp_sum_u64(part);
+  volatile uint64_t* dst = reinterpret_cast<volatile uint64_t*>(out);
+  if (lane < n) dst[lane] = lane == kOutCheck ? check : mine;
+  if (lane + 32 < n) dst[lane + 32] = extra;
+}
+
+__global__ void __launch_bounds__(32) decide_one_kernel(DecideOneArgs a, DecideOneOut* out) {
+  __shared__ DecideOneOut s_o;
+  decide_one_body(a, s_o, kCandPlaceD);
+  decide_publish(s_o, out, a.m);
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Resident form: warp 0 polls the mailbox (mapped pinned host memory). Every poll is one
+// PCIe round trip that fetches the whole mailbox (lanes 0..19, 16 B each); a request is
+// taken when args.seq differs from the last one served and the check word matches the
+// fetched words (a fetch that raced the host's writes fails the check and is repeated). The
+// server exits when the host sets `stop`, after idle_ns without a request, or after life_ns
+// in total; the host relaunches it on demand.
+//
+// Warp 1 computes ahead: after each request warp 0 posts (rng_seed, nonce + 1) -- callers
+// number their predictor calls consecutively (SimEngine's call nonce) -- and warp 1 makes
+// sure the draws of nonces +1 and +2 are in a 4-slot ring (lanes 0..13 and 14..27 run the
+// two calls' 158-step seeding chains plus log/cos side by side, ~75% of a request's
+// compute). A request finds its draws by nonce; each slot is a seqlock (odd version = being
+// written), so a slot rewritten while warp 0 read it is detected and warp 0 computes the
+// draws itself -- as it does for any call nobody computed ahead. Either way the draws are the
+// same bits.
+constexpr int kAheadSlots = 4, kAhead = 2;
+
+struct DrawSlot {
+  double n01[14];
+  uint64_t rng_seed, nonce;
+  uint32_t coins;         // bit l = lane l's coin
+  volatile uint32_t ver;  // seqlock version; odd = being written (or never written)
+};
+
+struct DrawAhead {
+  DrawSlot slot[kAheadSlots];
+  uint64_t want_seed, want_nonce;
+  volatile uint32_t posted, quit;
+};
+
+__device__ __forceinline__ void draw_ahead_worker(DrawAhead& da) {
+  const int lane = threadIdx.x & 31;
+  uint32_t served = 0;
+  for (;;) {
+    for (;;) {
+      if (da.quit) return;
+      if (da.posted != served) break;
+      __nanosleep(128);
+    }
+    served = da.posted;
+    __threadfence_block();
+    // (a post racing these reads only mixes keys; the slot records the key it computed for)
+    const uint64_t rs = da.want_seed, first = da.want_nonce;
+    const int k = lane / 14, l = lane % 14;
+    bool need[kAhead];
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      const DrawSlot& sl = da.slot[(first + q) % kAheadSlots];
+      need[q] = (sl.ver & 1u) || sl.nonce != first + q || sl.rng_seed != rs;
+    }
+    if (!need[0] && !need[1]) continue;
+    NoiseDraw d{0.0, false};
+    if (k < kAhead && need[k]) d = call_draw(rs, first + k, l);
+    const uint32_t coins = __ballot_sync(0xffffffffu, d.coin);
+#pragma unroll
+    for (int q = 0; q < kAhead; ++q) {
+      if (!need[q]) continue;
+      DrawSlot& sl = da.slot[(first + q) % kAheadSlots];
+      if (lane == 0) sl.ver = sl.ver | 1u;
+      __syncwarp();
+      __threadfence_block();
+      if (k == q) sl.n01[l] = d.n01;
+      if (lane == 0) {
+        sl.coins = (coins >> (14 * q)) & 0x3fffu;
+        sl.rng_seed = rs;
+        sl.nonce = first + q;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) sl.ver = sl.ver + 1u;
     }
   }
-  __syncwarp();
-  if (lane == 0) {
-    double ob = 0.0;
-    const bool all = a.en0 == ~0ull && a.en1 == (1ull << (kNumCands - 64)) - 1;
-    const uint8_t c = all ? search_any<true>(s_rows, m, a.en0, a.en1, &ob)
-                          : search_any<false>(s_rows, m, a.en0, a.en1, &ob);
-    out->cand = c;
-    out->obj = ob;
+}
+
+// Warp 0: this lane's draw of call (rng_seed, nonce) from the ring, if a consistent copy is
+// there (seqlock read, warp-uniform result).
+__device__ __forceinline__ bool take_ahead(const DrawAhead& da, uint64_t rng_seed, uint64_t nonce,
+                                           NoiseDraw& d) {
+  const int lane = threadIdx.x & 31;
+  const DrawSlot& sl = da.slot[nonce % kAheadSlots];
+  const uint32_t v1 = sl.ver;
+  __threadfence_block();
+  bool ok = !(v1 & 1u) && sl.nonce == nonce && sl.rng_seed == rng_seed;
+  if (ok && lane < 14) {
+    d.n01 = sl.n01[lane];
+    d.coin = (sl.coins >> lane) & 1u;
   }
-  __threadfence_system();
-  __syncwarp();
-  if (lane == 0) *reinterpret_cast<volatile uint64_t*>(&out->seq) = a.seq;
+  __threadfence_block();
+  ok = ok && sl.ver == v1;
+  return __all_sync(0xffffffffu, ok);
+}
+
+__global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* mb,
+                                                           DecideOneOut* out, uint64_t last,
+                                                           uint64_t idle_ns, uint64_t life_ns,
+                                                           uint64_t* stamps) {
+  __shared__ DecideOneArgs s_a;
+  __shared__ DecideOneOut s_o;
+  __shared__ DrawAhead da;
+  __shared__ uint8_t s_place[kNumCands][7];
+  for (int i = threadIdx.x; i < kNumCands * 7; i += blockDim.x)
+    (&s_place[0][0])[i] = (&kCandPlaceD[0][0])[i];
+  if (threadIdx.x < kAheadSlots) da.slot[threadIdx.x].ver = 1u;
+  if (threadIdx.x == 0) {
+    da.posted = 0;
+    da.quit = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    draw_ahead_worker(da);
+    return;
+  }
+  const int lane = threadIdx.x;
+  const uint64_t t0 = global_ns();
+  uint64_t t_last = t0;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(mb);
+  for (;;) {
+    unsigned long long w0 = 0, w1 = 0;
+    if (lane < 20)
+      asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(w0), "=l"(w1) : "l"(src + 2 * lane) : "memory");
+    const uint64_t seq = __shfl_sync(0xffffffffu, (kArgSeqWord & 1) ? w1 : w0, kArgSeqWord >> 1);
+    const uint64_t stop = __shfl_sync(0xffffffffu, w1, 19);
+    if (stop) break;
+    if (seq != last) {
+      const uint64_t ts0 = stamps ? global_ns() : 0;
+      uint64_t part = 0;
+      if (2 * lane < kArgWords) part += mbx_mix(w0, uint64_t(2 * lane));
+      if (2 * lane + 1 < kArgWords) part += mbx_mix(w1, uint64_t(2 * lane + 1));
+      const uint64_t check = __shfl_sync(0xffffffffu, w0, kArgWords >> 1);  // word kArgWords
+      if (warp_sum_u64(part) != check) continue;  // torn fetch: poll again
+      uint64_t* dst = reinterpret_cast<uint64_t*>(&s_a);
+      if (2 * lane < kArgWords) dst[2 * lane] = w0;
+      if (2 * lane + 1 < kArgWords) dst[2 * lane + 1] = w1;
+      __syncwarp();
+      const uint64_t ts1 = stamps ? global_ns() : 0;
+      const long long c1 = clock64();
+      NoiseDraw mine{0.0, false};
+      const bool hit = s_a.noisy && take_ahead(da, s_a.rng_seed, s_a.nonce, mine);
+      decide_one_body(s_a, s_o, s_place, stamps ? stamps + 8 : nullptr, hit ? &mine : nullptr);
+      const uint64_t ts2 = stamps ? global_ns() : 0;
+      const long long c2 = clock64();
+      decide_publish(s_o, out, s_a.m);
+      // post the next calls' draws (warp 1 picks the new generation up when it is idle)
+      if (lane == 0) {
+        da.want_seed = s_a.rng_seed;
+        da.want_nonce = s_a.nonce + 1;
+        __threadfence_block();
+        da.posted = da.posted + 1u;
+      }
+      if (stamps && lane == 0) {  // timing probe (tools/decide_probe.cu)
+        stamps[0] = ts0;
+        stamps[1] = ts1;
+        stamps[2] = ts2;
+        stamps[3] = global_ns();
+        stamps[4] = hit;
+        stamps[5] = uint64_t(c2 - c1);
+        stamps[6] = uint64_t(clock64() - c2);
+      }
+      last = seq;
+      __syncwarp();
+      t_last = global_ns();
+      continue;
+    }
+    const uint64_t now = global_ns();
+    if (now - t_last > idle_ns || now - t0 > life_ns) break;
+  }
+  if (lane == 0) da.quit = 1;
 }
 
 cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream) {
   decide_one_kernel<<<1, 32, 0, stream>>>(a, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decide_server(const DecideMailbox* mb, DecideOneOut* out, uint64_t last,
+                                 uint64_t idle_ns, uint64_t life_ns, cudaStream_t stream,
+                                 uint64_t* stamps) {
+  decide_server_kernel<<<1, 64, 0, stream>>>(mb, out, last, idle_ns, life_ns, stamps);
   return cudaGetLastError();
 }
 

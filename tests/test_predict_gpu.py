@@ -147,3 +147,67 @@ def test_decide_batch_vs_oracle_chain(ctx, oracle):
     feas = np.repeat(e >= 0, m)
     assert np.array_equal(gp[feas], p[feas])
     assert np.array_equal(bits(obj.cpu().numpy()), bits(ob))
+
+
+def test_decide_server_matches_launch_mode(ctx, oracle):
+    """miso_b200_decide through the resident server == one launch per call == the oracle chain,
+    with and without the server's draw-ahead (consecutive / random nonces), across server idle-outs (relaunch with a pending request), catalog changes between calls
+    and host-pipeline calls that stop the server."""
+    import time
+    rng = np.random.default_rng(11)
+    w2, w1 = oracle.default_model()
+    cases = []
+    for i in range(60):
+        m = int(rng.integers(1, 8))
+        t, _ = oracle.gen_profiles(100 + i, m)
+        mem = rng.choice([5, 10, 20, 40], m).astype(np.uint8)
+        qos = np.where(rng.random(m) < 0.2, rng.integers(0, 5, m), -1).astype(np.int8)
+        jobs = [(f"j{c}", tuple(t[3 * c:3 * c + 3]), int(mem[c]), None if qos[c] < 0 else int(qos[c]))
+                for c in range(m)]
+        # runs of consecutive call nonces (the server's draw-ahead hits) broken by random ones
+        cases.append((jobs, 5000 + i if i % 3 else int(rng.integers(1, 1 << 40))))
+
+    from paper_2207_11428_b200.catalog import DEFAULT_CATALOG
+    full = [list(c) for c in DEFAULT_CATALOG]
+
+    def run(idle_us, pause_every=0, poke=False, catalog=None):
+        ctx.decide_server(idle_us)
+        out = []
+        for k, (jobs, nonce) in enumerate(cases):
+            if pause_every and k % pause_every == pause_every - 1:
+                time.sleep(0.01)  # longer than the idle window: the server exits meanwhile
+            if catalog is not None:
+                ctx.set_catalog(catalog if k % 2 else full)
+            if poke and k % 7 == 3:  # growing host batches: scratch is reallocated (cudaFree)
+                n = 5000 * (k + 1)
+                ctx.optimize_batch(np.ones((n, 5)), np.arange(n + 1, dtype=np.uint32))
+            r, est = ctx.decide(jobs, nonce=nonce, rng_seed=5, mode=1, target_mae=0.017)
+            out.append((None if r is None else (r.entry, tuple(a.slice for a in r.assignments),
+                                                 np.float64(r.objective).view(np.uint64)),
+                        bits(est)))
+        return out
+
+    sub = [c for c in full if c[4] == 0][::2]  # a catalog without 7g, changed between calls
+    try:
+        launched = run(0)
+        served = run(2000)
+        idled = run(200, pause_every=5)
+        poked = run(2000, poke=True)
+        sub_launched = run(0, catalog=sub)
+        sub_served = run(2000, catalog=sub)
+    finally:
+        ctx.decide_server(2000)
+        ctx.set_catalog(full)
+    for a, b, c, d in zip(launched, served, idled, poked):
+        assert a[0] == b[0] == c[0] == d[0]
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[1], c[1]) and np.array_equal(a[1], d[1])
+    for a, b in zip(sub_launched, sub_served):
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    assert any(a[0] != b[0] for a, b in zip(launched, sub_launched))
+    # the chain itself against the oracle for the served results
+    for (jobs, nonce), (res, est_bits) in zip(cases, served):
+        m = len(jobs)
+        t3 = np.array([j[1] for j in jobs], np.float64).reshape(-1)
+        est = oracle.predict_batch(t3, m, nonce, 5, 1, 0.017, w2, w1).reshape(m, 5)
+        est = zero_eff(est, np.array([j[2] for j in jobs]), np.array([-1 if j[3] is None else j[3] for j in jobs]))
+        assert np.array_equal(bits(est), est_bits)
