@@ -246,17 +246,20 @@ __device__ __forceinline__ uint8_t warp_search(const double* rows, int m, uint64
     case 6: warp_score<6>(rows, place, c0, c1, en0, en1, best, bc); break;
     default: warp_score<7>(rows, place, c0, c1, en0, en1, best, bc); break;
   }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, d);
-    const int oc = __shfl_xor_sync(0xffffffffu, bc, d);
-    if (ob > best || (ob == best && oc < bc)) {
-      best = ob;
-      bc = oc;
-    }
+  // Warp argmax on the objective's bits: a valid objective is positive (+inf included), where
+  // the IEEE order is the unsigned order of the bit patterns and equality is bit equality;
+  // no valid candidate = key 0. Then the lowest id among the lanes holding the maximum.
+  const uint64_t key = bc == kCandInfeasible ? 0ull : static_cast<uint64_t>(__double_as_longlong(best));
+  const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned id = __reduce_min_sync(0xffffffffu, hi == mhi && lo == mlo ? unsigned(bc) : 0xffu);
+  if ((mhi | mlo) == 0u) {
+    *obj = 0.0;
+    return kCandInfeasible;
   }
-  *obj = bc == kCandInfeasible ? 0.0 : best;
-  return static_cast<uint8_t>(bc);
+  *obj = __longlong_as_double(static_cast<long long>((uint64_t(mhi) << 32) | mlo));
+  return static_cast<uint8_t>(id);
 }
 
 // pre: this lane's draw when the caller has it (the server's draw-ahead), else nullptr.
@@ -364,40 +367,65 @@ __device__ __forceinline__ uint64_t global_ns() {
 // written), so a slot rewritten while warp 0 read it is detected and warp 0 computes the
 // draws itself -- as it does for any call nobody computed ahead. Either way the draws are the
 // same bits.
+// Every shared word the two warps hand to each other is accessed with shared-memory atomics
+// (relaxed, ordered by __threadfence_block): the protocol is flag/seqlock based rather than
+// barrier based, and atomics make each cross-warp access well defined (and visible as such to
+// compute-sanitizer's racecheck).
 constexpr int kAheadSlots = 4, kAhead = 2;
 
 struct DrawSlot {
-  double n01[14];
-  uint64_t rng_seed, nonce;
-  uint32_t coins;         // bit l = lane l's coin
-  volatile uint32_t ver;  // seqlock version; odd = being written (or never written)
+  unsigned long long n01[14];            // double bits
+  unsigned long long rng_seed, nonce;
+  unsigned coins;                        // bit l = lane l's coin
+  unsigned ver;                          // seqlock version; odd = being written (or never written)
 };
 
 struct DrawAhead {
   DrawSlot slot[kAheadSlots];
-  uint64_t want_seed, want_nonce;
-  volatile uint32_t posted, quit;
+  unsigned long long want_seed, want_nonce;
+  unsigned posted, quit;
 };
+
+__device__ __forceinline__ unsigned long long sh_ld(unsigned long long* p) { return atomicAdd(p, 0ull); }
+__device__ __forceinline__ unsigned sh_ld(unsigned* p) { return atomicAdd(p, 0u); }
+__device__ __forceinline__ void sh_st(unsigned long long* p, unsigned long long v) { atomicExch(p, v); }
+__device__ __forceinline__ void sh_st(unsigned* p, unsigned v) { atomicExch(p, v); }
+
+// Control words are read by lane 0 and broadcast: per-lane atomics are separate reads, and a
+// warp must branch on one snapshot.
+__device__ __forceinline__ unsigned long long bcast_ld(unsigned long long* p) {
+  unsigned long long v = 0;
+  if ((threadIdx.x & 31) == 0) v = sh_ld(p);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
+__device__ __forceinline__ unsigned bcast_ld(unsigned* p) {
+  unsigned v = 0;
+  if ((threadIdx.x & 31) == 0) v = sh_ld(p);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
 
 __device__ __forceinline__ void draw_ahead_worker(DrawAhead& da) {
   const int lane = threadIdx.x & 31;
-  uint32_t served = 0;
+  unsigned served = 0;
   for (;;) {
+    unsigned posted;
     for (;;) {
-      if (da.quit) return;
-      if (da.posted != served) break;
+      if (bcast_ld(&da.quit)) return;
+      posted = bcast_ld(&da.posted);
+      if (posted != served) break;
       __nanosleep(128);
     }
-    served = da.posted;
+    served = posted;
     __threadfence_block();
     // (a post racing these reads only mixes keys; the slot records the key it computed for)
-    const uint64_t rs = da.want_seed, first = da.want_nonce;
+    const uint64_t rs = bcast_ld(&da.want_seed), first = bcast_ld(&da.want_nonce);
     const int k = lane / 14, l = lane % 14;
     bool need[kAhead];
 #pragma unroll
     for (int q = 0; q < kAhead; ++q) {
-      const DrawSlot& sl = da.slot[(first + q) % kAheadSlots];
-      need[q] = (sl.ver & 1u) || sl.nonce != first + q || sl.rng_seed != rs;
+      DrawSlot& sl = da.slot[(first + q) % kAheadSlots];
+      need[q] = (bcast_ld(&sl.ver) & 1u) || bcast_ld(&sl.nonce) != first + q ||
+                bcast_ld(&sl.rng_seed) != rs;
     }
     if (!need[0] && !need[1]) continue;
     NoiseDraw d{0.0, false};
@@ -407,38 +435,43 @@ __device__ __forceinline__ void draw_ahead_worker(DrawAhead& da) {
     for (int q = 0; q < kAhead; ++q) {
       if (!need[q]) continue;
       DrawSlot& sl = da.slot[(first + q) % kAheadSlots];
-      if (lane == 0) sl.ver = sl.ver | 1u;
-      __syncwarp();
-      __threadfence_block();
-      if (k == q) sl.n01[l] = d.n01;
       if (lane == 0) {
-        sl.coins = (coins >> (14 * q)) & 0x3fffu;
-        sl.rng_seed = rs;
-        sl.nonce = first + q;
+        atomicOr(&sl.ver, 1u);
+        __threadfence_block();
       }
       __syncwarp();
-      __threadfence_block();
-      if (lane == 0) sl.ver = sl.ver + 1u;
+      if (k == q) sh_st(&sl.n01[l], static_cast<unsigned long long>(__double_as_longlong(d.n01)));
+      if (lane == 0) {
+        sh_st(&sl.coins, (coins >> (14 * q)) & 0x3fffu);
+        sh_st(&sl.rng_seed, rs);
+        sh_st(&sl.nonce, first + q);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_block();
+        atomicAdd(&sl.ver, 1u);
+      }
+      __syncwarp();
     }
   }
 }
 
 // Warp 0: this lane's draw of call (rng_seed, nonce) from the ring, if a consistent copy is
-// there (seqlock read, warp-uniform result).
-__device__ __forceinline__ bool take_ahead(const DrawAhead& da, uint64_t rng_seed, uint64_t nonce,
+// there (seqlock read by lane 0 around the lanes' data reads; warp-uniform result).
+__device__ __forceinline__ bool take_ahead(DrawAhead& da, uint64_t rng_seed, uint64_t nonce,
                                            NoiseDraw& d) {
   const int lane = threadIdx.x & 31;
-  const DrawSlot& sl = da.slot[nonce % kAheadSlots];
-  const uint32_t v1 = sl.ver;
+  DrawSlot& sl = da.slot[nonce % kAheadSlots];
+  const unsigned v1 = bcast_ld(&sl.ver);
   __threadfence_block();
-  bool ok = !(v1 & 1u) && sl.nonce == nonce && sl.rng_seed == rng_seed;
-  if (ok && lane < 14) {
-    d.n01 = sl.n01[lane];
-    d.coin = (sl.coins >> lane) & 1u;
+  if ((v1 & 1u) || bcast_ld(&sl.nonce) != nonce || bcast_ld(&sl.rng_seed) != rng_seed) return false;
+  if (lane < 14) {
+    d.n01 = __longlong_as_double(static_cast<long long>(sh_ld(&sl.n01[lane])));
+    d.coin = (sh_ld(&sl.coins) >> lane) & 1u;
   }
+  __syncwarp();
   __threadfence_block();
-  ok = ok && sl.ver == v1;
-  return __all_sync(0xffffffffu, ok);
+  return bcast_ld(&sl.ver) == v1;
 }
 
 __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* mb,
@@ -465,11 +498,17 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
   const uint64_t t0 = global_ns();
   uint64_t t_last = t0;
   const unsigned long long* src = reinterpret_cast<const unsigned long long*>(mb);
+  // The expected next call (rng_seed, nonce + 1) and, once the ring has it, its draws in
+  // registers: fetched while a poll is in flight, so a matching request skips the ring read.
+  bool want_pre = false, have_pre = false;
+  uint64_t pre_seed = 0, pre_nonce = 0;
+  NoiseDraw pre{0.0, false};
   for (;;) {
     unsigned long long w0 = 0, w1 = 0;
     if (lane < 20)
       asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
                    : "=l"(w0), "=l"(w1) : "l"(src + 2 * lane) : "memory");
+    if (want_pre && !have_pre) have_pre = take_ahead(da, pre_seed, pre_nonce, pre);
     const uint64_t seq = __shfl_sync(0xffffffffu, (kArgSeqWord & 1) ? w1 : w0, kArgSeqWord >> 1);
     const uint64_t stop = __shfl_sync(0xffffffffu, w1, 19);
     if (stop) break;
@@ -486,18 +525,26 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
       __syncwarp();
       const uint64_t ts1 = stamps ? global_ns() : 0;
       const long long c1 = clock64();
-      NoiseDraw mine{0.0, false};
-      const bool hit = s_a.noisy && take_ahead(da, s_a.rng_seed, s_a.nonce, mine);
+      NoiseDraw mine = pre;
+      bool hit = false;
+      if (s_a.noisy) {
+        hit = have_pre && s_a.rng_seed == pre_seed && s_a.nonce == pre_nonce;
+        if (!hit) hit = take_ahead(da, s_a.rng_seed, s_a.nonce, mine);
+      }
       decide_one_body(s_a, s_o, s_place, stamps ? stamps + 8 : nullptr, hit ? &mine : nullptr);
+      want_pre = true;
+      have_pre = false;
+      pre_seed = s_a.rng_seed;
+      pre_nonce = s_a.nonce + 1;
       const uint64_t ts2 = stamps ? global_ns() : 0;
       const long long c2 = clock64();
       decide_publish(s_o, out, s_a.m);
       // post the next calls' draws (warp 1 picks the new generation up when it is idle)
       if (lane == 0) {
-        da.want_seed = s_a.rng_seed;
-        da.want_nonce = s_a.nonce + 1;
+        sh_st(&da.want_seed, s_a.rng_seed);
+        sh_st(&da.want_nonce, s_a.nonce + 1);
         __threadfence_block();
-        da.posted = da.posted + 1u;
+        atomicAdd(&da.posted, 1u);
       }
       if (stamps && lane == 0) {  // timing probe (tools/decide_probe.cu)
         stamps[0] = ts0;
@@ -507,6 +554,11 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
         stamps[4] = hit;
         stamps[5] = uint64_t(c2 - c1);
         stamps[6] = uint64_t(clock64() - c2);
+        DrawSlot& sl = da.slot[(s_a.nonce + 1) % kAheadSlots];  // the next call's slot
+        stamps[12] = sh_ld(&sl.ver);
+        stamps[13] = sh_ld(&sl.nonce);
+        stamps[14] = sh_ld(&da.posted);
+        stamps[15] = s_a.nonce;
       }
       last = seq;
       __syncwarp();
@@ -516,7 +568,7 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
     const uint64_t now = global_ns();
     if (now - t_last > idle_ns || now - t0 > life_ns) break;
   }
-  if (lane == 0) da.quit = 1;
+  if (lane == 0) sh_st(&da.quit, 1u);
 }
 
 cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream) {

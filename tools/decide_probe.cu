@@ -82,6 +82,8 @@ int main(int argc, char** argv) {
     for (int q = 0; q < 3; ++q) cyc[q].push_back(double(st[4 + q]));
     for (int q = 0; q < 3; ++q) ph[q].push_back(double(st[8 + q]));
   }
+  printf("slot(next) ver=%llu nonce=%llu posted=%llu req_nonce=%llu\n", (unsigned long long)st[12],
+         (unsigned long long)st[13], (unsigned long long)st[14], (unsigned long long)st[15]);
   *reinterpret_cast<volatile uint64_t*>(&mb->stop) = 1;
   cudaStreamSynchronize(s);
   auto med = [](std::vector<double> v) {

@@ -8,3 +8,5 @@ for i in 1 2; do timeout 60 ./tools/decide_probe.bin 3000; done > gpurun_out/pro
 cat gpurun_out/probe.txt
 timeout 300 python bench.py --config c1 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
 cat gpurun_out/bench_c1.json; tail -5 gpurun_out/bench_c1.err
+timeout 1200 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_run.py > gpurun_out/sanitize_racecheck.txt 2>&1
+echo "racecheck rc=$?"; tail -2 gpurun_out/sanitize_racecheck.txt

@@ -5,6 +5,8 @@ predictor, the fused decide kernel, the single-roster latency kernel, the simula
 policy, clones, optsta), and the device trace generator."""
 import sys
 
+import time
+
 import numpy as np
 import torch
 
@@ -27,7 +29,14 @@ mem = np.full(700, 5, np.uint8); qos = np.full(700, -1, np.int8)
 offs = np.arange(0, 701, 7).astype(np.uint32)
 ctx.decide_batch(t, mem, qos, offs, np.arange(1, 101, dtype=np.uint64), 7, 1, 0.017)
 tr = m.generate_trace(7, 3)
-ctx.decide([(f"j{i}", (tr.speeds5[i, 4], tr.speeds5[i, 3], tr.speeds5[i, 2]), int(tr.mem_gb[i]), None) for i in range(3)], 1, 7)
+jobs3 = [(f"j{i}", (tr.speeds5[i, 4], tr.speeds5[i, 3], tr.speeds5[i, 2]), int(tr.mem_gb[i]), None) for i in range(3)]
+for nonce in range(1, 9):  # resident server: consecutive nonces exercise the draw-ahead ring
+    ctx.decide(jobs3, nonce, 7)
+    time.sleep(0.002 if nonce % 3 == 0 else 0.0)
+ctx.decide(jobs3, 1000, 7)
+ctx.decide_server(0)       # one launch per call
+ctx.decide(jobs3, 1, 7)
+ctx.decide_server(2000)
 traces = m.generate_traces(range(6), 60, lambda_s=20.0)
 traces[2].instances = np.array([1] * 10 + [3] + [1] * 49, np.uint8)
 for pol in ("nopart", "oracle", "miso"):
