@@ -42,8 +42,23 @@ __device__ __forceinline__ uint64_t mt64_temper(uint64_t y) {
   return y;
 }
 
-__device__ __forceinline__ uint64_t mt64_seed_step(uint64_t x, uint64_t i) {
-  return 6364136223846793005ull * (x ^ (x >> 62)) + i;  // [rand.eng.mers] seeding
+// [rand.eng.mers] seeding step x' = f * (x ^ (x >> 62)) + i mod 2^64, f = 0x5851F42D4C957F2D,
+// i < 2^32, in 32-bit halves: the xor only flips the low word's two low bits, so
+//   lo' = lo ^ (hi >> 30);  t = lo' * f_hi + hi * f_lo  (hi * f_lo is off the critical path);
+//   lo(x') = lo(lo' * f_lo) + i, carry;  hi(x') = hi(lo' * f_lo) + t + carry
+// as a mad.lo.cc / madc.hi carry chain: 6 instructions per step. (The plain 64-bit expression
+// compiles to a wide multiply plus a separate 64-bit add of i, 8.)
+__device__ __forceinline__ uint64_t mt64_seed_step(uint64_t x, uint32_t i) {
+  constexpr uint32_t kFLo = 0x4C957F2Du, kFHi = 0x5851F42Du;
+  const uint32_t hi = static_cast<uint32_t>(x >> 32);
+  const uint32_t lo = static_cast<uint32_t>(x) ^ (hi >> 30);
+  const uint32_t t = lo * kFHi + hi * kFLo;
+  uint32_t rlo, rhi;
+  asm("mad.lo.cc.u32 %0, %2, %3, %4;\n\t"
+      "madc.hi.u32 %1, %2, %3, %5;"
+      : "=r"(rlo), "=r"(rhi)
+      : "r"(lo), "r"(kFLo), "r"(i), "r"(t));
+  return (static_cast<uint64_t>(rhi) << 32) | rlo;
 }
 
 __device__ __forceinline__ uint64_t mt64_twist_draw(uint64_t xk, uint64_t xk1, uint64_t xk156) {

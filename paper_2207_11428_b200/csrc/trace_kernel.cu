@@ -34,7 +34,7 @@ __device__ __forceinline__ void mt_seed(uint64_t* mt, uint64_t seed) {  // [rand
     uint64_t x = seed;
     mt[0] = x;
     for (int i = 1; i < kMtN; ++i) {
-      x = mt64_seed_step(x, static_cast<uint64_t>(i));
+      x = mt64_seed_step(x, static_cast<uint32_t>(i));
       mt[i] = x;
     }
   }
