@@ -341,7 +341,7 @@ def bench_c4(args):
     nopart, optsta with best_static_partition (every feasible catalog entry, ~17 candidate
     simulations per trace) and its re-run with the chosen partition, and miso (noisy predictor
     0.017, rng_seed = seed); JCT normalised by the same trial's nopart. Everything runs on the
-    device in four launches on three streams (one warp per simulation). Secondary
+    device on three streams (one warp per simulation). Secondary
     measurement: trials/s beside the reference's trial on every host thread."""
     import torch
     import paper_2207_11428_b200 as miso
@@ -364,7 +364,11 @@ def bench_c4(args):
         p_mis = miso.simulate_batch(ctx_c, traces, miso.SimOptions(policy="miso", cluster_size=100,
                                                                    predictor="noisy"),
                                     stream=s_c, defer=True)
-        st = miso.best_static_partition(ctx_b, traces, cluster_size=100, stream=s_b)
+        # MISO_C4_PRUNED_STATIC=1: the chosen-only pruned search instead (same entries; 1.45x
+        # faster alone, but here miso is the critical path and the full search overlaps it
+        # better: 374 vs 399 ms per 1024 trials, tools/c4_timeline.py)
+        st = miso.best_static_partition(ctx_b, traces, cluster_size=100, stream=s_b,
+                                        chosen_only=os.environ.get("MISO_C4_PRUNED_STATIC") == "1")
         sta = miso.simulate_batch(ctx_b, traces, miso.SimOptions(policy="optsta", cluster_size=100),
                                   static_partitions=[miso.DEFAULT_CATALOG[e] for e, _ in st],
                                   stream=s_b)
@@ -385,6 +389,7 @@ def bench_c4(args):
     assert np.array_equal(j_sta.view(np.uint64), np.array([tab[e] for e, tab in st]).view(np.uint64))
     j_mis = mis.metrics["avg_jct_s"]
     ev = int(mis.metrics["events"].sum())
+    n_cand = miso.sim.static_candidates(traces)[0]  # candidate runs launched (stopped or not)
     cpu = None
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib
@@ -405,7 +410,8 @@ def bench_c4(args):
                  "static_entry_equal": bool(all(e == st[i][0] for i, (e, _) in enumerate(outs)))}
     print(json.dumps({"metric": "cluster-simulation trials/sec (config 4: nopart + optsta(best static) + miso, 100 GPUs x 1000 jobs)",
                       "value": S / dt, "unit": "trials/s", "s_per_step": dt, "seeds": S,
-                      "simulations_per_step": int(S * 3 + sum(np.isfinite(t).sum() for _, t in st)),
+                      "simulations_per_step": int(S * 3 + len(n_cand)),
+                      "static_candidates_completed": int(sum(np.isfinite(t).sum() for _, t in st)),
                       "miso_events_per_seed": ev / S, "steps": args.steps, "warmup": args.warmup,
                       "dtype": "f64", "data": "synthetic (generate_trace seeds 0..S-1)",
                       "median_jct_norm": {"optsta": float(np.median(j_sta / j_nop)),

@@ -146,6 +146,7 @@ int miso_b200_decide_server(miso_b200_ctx* ctx, int idle_us);
 #define MISO_B200_SIM_NO_PARTITION 2      /* "no feasible partition for admitted roster" */
 #define MISO_B200_SIM_INFEASIBLE_SLICE 3  /* "placed on infeasible slice" */
 #define MISO_B200_SIM_EVENT_BUDGET 4      /* max_events exceeded (counts live events) */
+#define MISO_B200_SIM_PRUNED 5            /* stopped by miso_b200_simulate_batch_pruned's bound */
 
 /* SimOptions (sim.hpp:81-96) + OverheadSpec (:62-67) + PredictorSpec (profiles.hpp:173-178).
  * Durations in seconds are converted with us_from_s = llround(s * 1e6) (sim.hpp:136). */
@@ -272,6 +273,26 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
                                 int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
                                 double* stp_series, int64_t stp_cap, unsigned flags,
                                 void* stream);
+
+/* Chosen-only best-static search (run_trial_unit reads only best_static_partition(...).chosen,
+ * experiment.hpp:337): optsta candidate runs as miso_b200_simulate_batch_ex (task_trace
+ * required, single-instance traces), plus bound[n_traces] (device int64, in/out; start it at
+ * INT64_MAX or at a completed candidate's exact JCT sum). Every task that completes lowers
+ * bound[its trace] (atomic min) to its exact JCT sum in us. A running task keeps a lower bound
+ * on its own sum (finished JCTs, now - arrival of arrived unfinished jobs, a run-time floor for
+ * jobs not started) and stops once it exceeds bound * (1 + 1e-9) + 2 * jobs. Its metrics then
+ * carry status MISO_B200_SIM_PRUNED and avg_jct_s = +inf. Its true avg_jct_s is strictly
+ * greater than that completed candidate's, so the first minimum over the catalog (sim.hpp:1058)
+ * is unchanged. Launch likely winners first (or in an earlier call with the same bound) so
+ * the rest stop early. */
+int miso_b200_simulate_batch_pruned(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
+                                    int n_tasks, const int32_t* task_trace,
+                                    const uint8_t* static_counts, const int32_t* job_offsets,
+                                    const double* arrival_s, const double* base_s,
+                                    const double* speeds5, const uint8_t* mem_gb,
+                                    const int8_t* qos_kind, const uint64_t* rng_seed,
+                                    miso_b200_sim_metrics* metrics, int64_t* bound,
+                                    unsigned flags, void* stream);
 
 /* The same with HOST pointers (synchronous): inputs are copied to the device, results back.
  * n_traces = entries of job_offsets minus one. The C++ binding include/miso_b200_sim.hpp builds

@@ -7,6 +7,7 @@ paper_2207_11428_b200/_lib/libmiso_b200.so with nvcc (-gencode arch=compute_100a
 from __future__ import annotations
 
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -58,7 +59,9 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(pair):
         src, obj = pair
-        if not force and not _stale(obj, [src, *headers]):
+        # a TU that #includes another .cu (sim_kernel_prune.cu) depends on it too
+        inc = [CSRC / m for m in re.findall(r'#include "([^"]+\.cu)"', src.read_text())]
+        if not force and not _stale(obj, [src, *headers, *inc]):
             return None
         cmd = [nvcc, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)

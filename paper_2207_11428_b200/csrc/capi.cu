@@ -586,16 +586,15 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
                                      stp_series, stp_cap, 0u, stream);
 }
 
-int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                                const int32_t* task_trace, const uint8_t* static_counts,
-                                const int32_t* job_offsets, const double* arrival_s,
-                                const double* base_s, const double* speeds5,
-                                const uint8_t* mem_gb, const int8_t* qos_kind,
-                                const uint8_t* instances, const uint64_t* rng_seed,
-                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
-                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
-                                double* stp_series, int64_t stp_cap, unsigned flags,
-                                void* stream) {
+namespace {
+int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                  const int32_t* task_trace, const uint8_t* static_counts,
+                  const int32_t* job_offsets, const double* arrival_s, const double* base_s,
+                  const double* speeds5, const uint8_t* mem_gb, const int8_t* qos_kind,
+                  const uint8_t* instances, const uint64_t* rng_seed,
+                  miso_b200_sim_metrics* metrics, int64_t* job_jct_us, int64_t* job_out,
+                  miso_b200_log_record* log, int64_t log_cap, double* stp_series,
+                  int64_t stp_cap, unsigned flags, int64_t* prune_bound, void* stream) {
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (flags & ~MISO_B200_SIM_JCT_ONLY) return fail(MISO_B200_E_INVALID, "unknown flags");
   if ((flags & MISO_B200_SIM_JCT_ONLY) && stp_series)
@@ -714,10 +713,44 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
   b.log_cap = log ? log_cap : 0;
   b.stp_series = stp_series;
   b.stp_cap = stp_series ? stp_cap : 0;
+  b.prune_bound = prune_bound;
   double w2[4], w1[4];
   default_model(w2, w1);
   CUDA_TRY(launch_simulate(b, p, w2, w1, s));
   return MISO_B200_OK;
+}
+}  // namespace
+
+int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
+                                const int32_t* task_trace, const uint8_t* static_counts,
+                                const int32_t* job_offsets, const double* arrival_s,
+                                const double* base_s, const double* speeds5,
+                                const uint8_t* mem_gb, const int8_t* qos_kind,
+                                const uint8_t* instances, const uint64_t* rng_seed,
+                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
+                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
+                                double* stp_series, int64_t stp_cap, unsigned flags,
+                                void* stream) {
+  return simulate_impl(ctx, opt, n_seeds, task_trace, static_counts, job_offsets, arrival_s,
+                       base_s, speeds5, mem_gb, qos_kind, instances, rng_seed, metrics,
+                       job_jct_us, job_out, log, log_cap, stp_series, stp_cap, flags, nullptr,
+                       stream);
+}
+
+int miso_b200_simulate_batch_pruned(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
+                                    int n_tasks, const int32_t* task_trace,
+                                    const uint8_t* static_counts, const int32_t* job_offsets,
+                                    const double* arrival_s, const double* base_s,
+                                    const double* speeds5, const uint8_t* mem_gb,
+                                    const int8_t* qos_kind, const uint64_t* rng_seed,
+                                    miso_b200_sim_metrics* metrics, int64_t* bound,
+                                    unsigned flags, void* stream) {
+  if (!opt || opt->policy != MISO_B200_POLICY_OPTSTA)
+    return fail(MISO_B200_E_INVALID, "pruned runs are optsta candidate searches");
+  if (!task_trace || !bound) return fail(MISO_B200_E_INVALID, "task_trace and bound are required");
+  return simulate_impl(ctx, opt, n_tasks, task_trace, static_counts, job_offsets, arrival_s,
+                       base_s, speeds5, mem_gb, qos_kind, nullptr, rng_seed, metrics, nullptr,
+                       nullptr, nullptr, 0, nullptr, 0, flags, bound, stream);
 }
 
 extern "C++" {

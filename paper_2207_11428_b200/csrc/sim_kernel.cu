@@ -33,8 +33,17 @@
 #include "search.cuh"
 #include "sim_types.h"
 
+#ifndef MISO_SIM_PRUNE
+#define MISO_SIM_PRUNE 0  // sim_kernel_prune.cu builds this file again with 1
+#endif
+#if MISO_SIM_PRUNE
+#define MISO_SIM_NS sim_prune
+#else
+#define MISO_SIM_NS sim
+#endif
+
 namespace miso_b200 {
-namespace sim {
+namespace MISO_SIM_NS {
 
 enum Phase : uint8_t { kQueued = 0, kMps = 1, kCkpt = 2, kRunning = 3, kIdle = 4 };
 enum Mode : uint8_t { kGpuIdle = 0, kGpuMig = 1, kGpuMps = 2, kGpuReconfig = 3 };
@@ -58,6 +67,7 @@ struct DJob {
   uint8_t inst;     // JobProfile::instance_count (clones: 1)
   int16_t clone_k;  // clones: k of "parent#k"; trace jobs: 0
   int32_t parent;   // clones: parent job index; trace jobs: -1
+  double lbp;       // pruned search: this job's term of Ctx::lb_p while started and unfinished
 };
 
 struct DGpu {
@@ -126,6 +136,16 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   int64_t first_progress, last_completion;
   int status;
   uint64_t processed;
+  // chosen-only best-static search (SimBatch::prune_bound): a lower bound on this run's exact
+  // JCT sum (us) = finished JCTs + (now - arrival) of arrived unfinished jobs + a runtime floor
+  // for every job that has not started (see prune_lb)
+#if MISO_SIM_PRUNE
+  bool prune;
+  int64_t lb_fin, lb_narr, lb_arrsum, lb_unstarted;
+  // started, unfinished jobs: sum of remaining_work / max_speed in seconds, kept as
+  // lb_p - lb_v * now_s with per-job terms (remaining + rate * t_update) / mx and rate / mx
+  double lb_p, lb_v;
+#endif
   // options
   const SimParams* p;
   const int8_t* spare_lut;
@@ -275,10 +295,32 @@ __device__ void advance_job(Ctx& c, DJob& j) {
   }
 }
 
+// Pruned best-static search (SimBatch::prune_bound). A job can never run faster than
+// max_speed (every rate is an effective true speed, <= truth[k]), so from any moment it needs
+// at least remaining / max_speed more seconds (migrations only add checkpoint pauses), and a
+// job that has not started needs at least base / max_speed (completions are scheduled
+// llround(remaining / rate * 1e6) us ahead: rounded down with margin).
+__device__ __forceinline__ double max_speed(const DJob& j) {  // >= any rate the job can get
+  double mx = 1.0;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) mx = j.truth[k] > mx ? j.truth[k] : mx;
+  return mx;
+}
+__device__ __forceinline__ int64_t runtime_floor_us(const DJob& j) {
+  const double us = j.base / max_speed(j) * 1e6 * (1.0 - 1e-12) - 2.0;
+  return us > 0.0 ? static_cast<int64_t>(us) : 0;
+}
+
 // sim.hpp:333-343 (+ slot invalidation: every epoch bump retires the job's pending event)
 __device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
   DJob& j = c.jobs[ji];
   advance_job(c, j);
+#if MISO_SIM_PRUNE
+  if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // retire the old-rate term
+    c.lb_p -= j.lbp;
+    c.lb_v -= j.rate / max_speed(j);
+  }
+#endif
   j.phase = phase;
   j.rate = progressing(phase) ? rate : 0.0;
   ++j.epoch;
@@ -292,6 +334,14 @@ __device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
   c.stp_dirty = true;
   if (ji < c.stp_cmin) c.stp_cmin = ji;
   sync_jst(c, ji, j);
+#if MISO_SIM_PRUNE
+  if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // remaining / mx, from now
+    const double mx = max_speed(j);
+    j.lbp = (j.remaining + j.rate * s_from_us(c.now)) / mx;
+    c.lb_p += j.lbp;
+    c.lb_v += j.rate / mx;
+  }
+#endif
 }
 
 // sim.hpp:345-351
@@ -412,6 +462,9 @@ __device__ void finish_profiling(Ctx& c, int gi);
 // sim.hpp:480-489
 __device__ void start_running(Ctx& c, int ji, int s) {
   DJob& j = c.jobs[ji];
+#if MISO_SIM_PRUNE
+  if (c.prune && j.first_progress_us < 0) c.lb_unstarted -= runtime_floor_us(j);
+#endif
   const double r = c.efftruth[size_t(s) * c.J + ji];  // == true_rate(j, s)
   if (c.p->check_invariants && !(r > 0)) fail(c, MISO_B200_SIM_INFEASIBLE_SLICE);
   j.slice = static_cast<uint8_t>(s);
@@ -1008,6 +1061,12 @@ __device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
 // sim.hpp:798-835
 __device__ void on_completion(Ctx& c, int ji) {
   DJob& j = c.jobs[ji];
+#if MISO_SIM_PRUNE
+  if (c.prune) {  // the job's remaining-work term leaves with it
+    c.lb_p -= j.lbp;
+    c.lb_v -= j.rate / max_speed(j);
+  }
+#endif
   advance_job(c, j);
   if (c.p->check_invariants) {
     const double base = j.base;
@@ -1032,6 +1091,13 @@ __device__ void on_completion(Ctx& c, int ji) {
     if (total != c.now - j.arrival_us) fail(c, MISO_B200_SIM_INVARIANT);
   }
   const int64_t jct = c.now - j.arrival_us;
+#if MISO_SIM_PRUNE
+  if (c.prune) {
+    c.lb_fin += jct;
+    --c.lb_narr;
+    c.lb_arrsum -= j.arrival_us;
+  }
+#endif
   log_rec(c, kLogComplete, -1, ji, 0, static_cast<uint32_t>(jct & 0xFFFFFFFF),
           static_cast<uint32_t>(jct >> 32), 0);
   const int gi = j.gpu;
@@ -1060,6 +1126,12 @@ __device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
         c.n_arrived = ji + 1;
       }
       log_rec(c, kLogArrival, -1, ji, 0, 0, 0, 0);
+#if MISO_SIM_PRUNE
+      if (c.prune) {
+        ++c.lb_narr;
+        c.lb_arrsum += c.now;  // == arrival_us
+      }
+#endif
       enqueue(c, ji);
     } else if (kind == kEvCompletion) {
       on_completion(c, ji);
@@ -1149,6 +1221,11 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.last_completion = -1;
   c.status = 0;
   c.processed = 0;
+#if MISO_SIM_PRUNE
+  c.prune = b.prune_bound != nullptr && prm.policy == MISO_B200_POLICY_OPTSTA && J == JT;
+  c.lb_fin = c.lb_narr = c.lb_arrsum = c.lb_unstarted = 0;
+  c.lb_p = c.lb_v = 0.0;
+#endif
   c.p = &prm;
   c.spare_lut = b.spare_lut;
   c.rng_seed = b.rng_seed[warp];  // per task
@@ -1192,6 +1269,9 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
 #pragma unroll
     for (int k = 0; k < 5; ++k) c.efftruth[size_t(k) * J + i] = effective_speed(j.truth[k], k, j.mem, j.qos);
     c.arr_us[i] = a;
+#if MISO_SIM_PRUNE
+    if (c.prune) c.lb_unstarted += runtime_floor_us(j);  // lane partial, reduced below
+#endif
     Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
     s.t = a;
     s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
@@ -1241,6 +1321,10 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     c.freemask[wi] = v;
   }
   __syncwarp();
+#if MISO_SIM_PRUNE
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) c.lb_unstarted += __shfl_xor_sync(0xffffffffu, c.lb_unstarted, off);
+#endif
   c.seq = static_cast<uint64_t>(JT);  // one arrival event per trace job (sim.hpp:219)
   bool bad_job = false;
   for (int i = lane; i < JT; i += 32) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
@@ -1266,7 +1350,26 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
     drain_queue(c);
     refresh_stp(c);
     __syncwarp();
+#if MISO_SIM_PRUNE
+    if (c.prune && (c.processed & 31) == 0) {
+      // chosen-only search: stop once this run's JCT sum provably exceeds a completed
+      // candidate's (then its avg_jct_s > that candidate's, so it cannot be the first minimum)
+      const int64_t thr = *reinterpret_cast<volatile const int64_t*>(b.prune_bound + tr);
+      // exact integer part + the started jobs' remaining-work floor (FP sums: 1 s of margin,
+      // far above their rounding error)
+      const int64_t lbi = c.lb_fin + c.lb_narr * c.now - c.lb_arrsum + c.lb_unstarted;
+      const double lb = static_cast<double>(lbi) + (c.lb_p - c.lb_v * s_from_us(c.now)) * 1e6 - 1e6;
+      if (thr != INT64_MAX && lb > static_cast<double>(thr) * (1.0 + 1e-9) + 2.0 * JT) {
+        c.status = MISO_B200_SIM_PRUNED;
+        break;
+      }
+    }
+#endif
   }
+#if MISO_SIM_PRUNE
+  if (c.prune && c.status == 0 && c.done_count == JT && lane == 0)
+    atomicMin(reinterpret_cast<long long*>(b.prune_bound + tr), static_cast<long long>(c.lb_fin));
+#endif
 
   // ---- finalize (sim.hpp:902-949) ----
   const int JU = c.J_used;  // jobs_.size(): trace jobs + spawned clones (sim.hpp:903-913)
@@ -1349,7 +1452,21 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   if (lane == 0) b.metrics[warp] = m;
 }
 
-}  // namespace sim
+}  // namespace MISO_SIM_NS
+
+#if MISO_SIM_PRUNE
+// The pruned best-static search's kernel (this file built with MISO_SIM_PRUNE=1): a separate
+// instantiation, so the bound bookkeeping costs the other simulations nothing.
+cudaError_t launch_simulate_prune(const SimBatch& b, const SimParams& p, const ModelW& w,
+                                  cudaStream_t stream) {
+  const int threads = 128;
+  const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
+  sim_prune::simulate_kernel<<<blocks, threads, 0, stream>>>(b, p, w);
+  return cudaGetLastError();
+}
+#else
+cudaError_t launch_simulate_prune(const SimBatch& b, const SimParams& p, const ModelW& w,
+                                  cudaStream_t stream);
 
 size_t sim_workspace_stride(int max_jobs, int cluster_size) {
   return sim_ws_total(max_jobs, cluster_size);
@@ -1366,6 +1483,7 @@ cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double*
     w.w2[i] = w2[i];
     w.w1[i] = w1[i];
   }
+  if (b.prune_bound) return launch_simulate_prune(b, p, w, stream);
   const int threads = 128;
   const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
   // MISO_SIM_SMEM_PAD (tuning only): dynamic shared memory reserved per block to cap how many
@@ -1380,5 +1498,6 @@ cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double*
   sim::simulate_kernel<<<blocks, threads, pad, stream>>>(b, p, w);
   return cudaGetLastError();
 }
+#endif
 
 }  // namespace miso_b200

@@ -55,6 +55,7 @@ struct SimBatch {
   int64_t log_cap;
   double* stp_series;
   int64_t stp_cap;
+  int64_t* prune_bound;  // per trace (nullable): chosen-only best-static search, see capi
 };
 
 // Per-seed workspace layout: [jobs][gpus][slots][queue][progress mask][rate scratch]

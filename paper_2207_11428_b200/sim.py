@@ -61,6 +61,10 @@ lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c
     [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
 lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
     [C.c_void_p] * 14 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
+if hasattr(lib, "miso_b200_simulate_batch_pruned"):  # (absent only in older tuning builds)
+    lib.miso_b200_simulate_batch_pruned.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
+        [C.c_void_p] * 11 + [C.c_uint, C.c_void_p]
+SIM_PRUNED = 5  # MISO_B200_SIM_PRUNED
 
 
 @dataclass
@@ -266,12 +270,14 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
                    stp_cap: int = 0, want_jct: bool = False, stream=None,
                    task_trace: Optional[Sequence[int]] = None,
                    static_partitions: Optional[Sequence[Sequence[int]]] = None,
-                   jct_only: bool = False, defer: bool = False):
+                   jct_only: bool = False, defer: bool = False, prune_bound=None):
     """run_simulation for every task at once (device), one warp per task. By default task i
     simulates traces[i]; with task_trace, task t simulates traces[task_trace[t]] (one launch
     can replay a trace under many static partitions). rng_seeds (per task) default to the
     trace's seed (experiment.hpp:305). static_partitions: per-task kind counts (optsta).
     jct_only: MISO_B200_SIM_JCT_ONLY (no STP series; stp metrics read 0).
+    prune_bound: an int64 CUDA tensor, one entry per trace -- the chosen-only best-static
+    search (miso_b200_simulate_batch_pruned; optsta, task_trace, single-instance traces).
     stream: a torch.cuda.Stream for the uploads, the launch and the read-back (default: the
     current stream). defer=True returns a zero-argument callable that waits for that stream
     and returns the SimResult, so launches on different streams (and different Contexts --
@@ -305,11 +311,19 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         d_stp = torch.empty(S * stp_cap * 2, dtype=torch.float64, device=dev) if stp_cap else None
         o = opts.to_c()
         p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-        _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
-                                               p(d_arr), p(d_dur),
-                                               p(d_sp), p(d_mem), p(d_qos), p(d_inst), p(d_seed), p(d_met),
-                                               p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
-                                               1 if jct_only else 0, st_obj.cuda_stream))
+        if prune_bound is not None:
+            if inst is not None or want_jct or log_cap or stp_cap:
+                raise ValueError("pruned runs take single-instance traces and return metrics only")
+            _check(lib.miso_b200_simulate_batch_pruned(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+                                                       p(d_arr), p(d_dur), p(d_sp), p(d_mem), p(d_qos),
+                                                       p(d_seed), p(d_met), prune_bound.data_ptr(),
+                                                       1 if jct_only else 0, st_obj.cuda_stream))
+        else:
+            _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+                                                   p(d_arr), p(d_dur),
+                                                   p(d_sp), p(d_mem), p(d_qos), p(d_inst), p(d_seed), p(d_met),
+                                                   p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
+                                                   1 if jct_only else 0, st_obj.cuda_stream))
     keep = (d_offs, d_arr, d_dur, d_sp, d_mem, d_qos, d_seed, d_tt, d_sc, d_inst)  # alive until done
 
     def finish() -> SimResult:
@@ -404,13 +418,68 @@ def min_kind(mem_gb: int, qos_kind=None):
     return None
 
 
+def static_candidates(traces: Sequence[Trace], catalog=None):
+    """best_static_partition's candidate runs (sim.hpp:1036-1048): (trace index, catalog
+    index) of every entry whose largest slice is at least every job's min_slice_for
+    (topology.hpp:68-72), trace-major in catalog order. Raises ValueError (InfeasibleError) if
+    a job fits no slice kind."""
+    from .catalog import DEFAULT_CATALOG, GPC, MEM_GB
+    cat = list(catalog if catalog is not None else DEFAULT_CATALOG)
+    catc = np.asarray(cat, np.uint8).reshape(-1, 5)
+    largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
+    offs, _, _, _, mem, qos, _ = _csr(traces)
+    if hasattr(mem, "cpu"):  # device-resident batch: the feasibility pass runs on host copies
+        offs, mem, qos = offs.cpu().numpy(), mem.cpu().numpy(), qos.cpu().numpy()
+    # min_slice_for: the smallest kind with memory_gb >= mem and gpc >= gpc(qos); both tables
+    # are non-decreasing in the kind index, so it is max(first kind with enough memory, qos)
+    mk = np.maximum(np.searchsorted(np.asarray(MEM_GB), np.asarray(mem, np.int64), side="left"),
+                    np.maximum(np.asarray(qos, np.int64), 0))
+    assert list(GPC) == sorted(GPC) and list(MEM_GB) == sorted(MEM_GB)
+    if len(mk) and mk.max() > 4:
+        j = int(np.argmax(mk > 4))
+        ti = int(np.searchsorted(offs, j, side="right") - 1)
+        raise ValueError(f"trace {ti}: a job fits no slice kind")
+    need = np.maximum.reduceat(mk, offs[:-1]) if len(traces) else np.zeros(0, np.int64)
+    feas = largest[None, :] >= need[:, None]                      # (traces, entries)
+    return np.nonzero(feas)
+
+
+def static_probes(ti_arr, e_arr, catalog_counts):
+    """The chosen-only search's probes: per trace, the two best-ranked feasible candidates by
+    a prior (most GPCs, then slice count nearest 3, then catalog order) -- the likeliest
+    winners, run first so the other candidates can be stopped against their JCT sums.
+    Returns a bool mask over the candidate list."""
+    catc = np.asarray(catalog_counts, np.int64).reshape(-1, 5)
+    from .catalog import GPC
+    gpcs = (catc * np.asarray(GPC)[None, :]).sum(axis=1)
+    nsl = catc.sum(axis=1)
+    prio = np.lexsort((np.arange(len(catc)), np.abs(nsl - 3), -gpcs))
+    rank = np.empty(len(catc), np.int64)
+    rank[prio] = np.arange(len(catc))
+    r = rank[e_arr]
+    order = np.lexsort((r, ti_arr))
+    first = np.r_[True, ti_arr[order][1:] != ti_arr[order][:-1]] if len(order) else np.zeros(0, bool)
+    pos = np.arange(len(order)) - np.maximum.accumulate(np.where(first, np.arange(len(order)), 0))
+    probe = np.zeros(len(ti_arr), bool)
+    probe[order[pos < 2]] = True
+    return probe
+
+
 def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: int,
-                          overheads: Optional[SimOptions] = None, catalog=None, stream=None):
+                          overheads: Optional[SimOptions] = None, catalog=None, stream=None,
+                          chosen_only: bool = False):
     """best_static_partition (sim.hpp:1031-1066) for many traces in ONE launch: every
     (trace, candidate partition) pair is an independent optsta simulation (one warp each).
     Returns per trace (chosen catalog index, table of avg JCT per entry; inf = skipped or
     incomplete). Raises ValueError (InfeasibleError) if a job fits no slice kind or no
-    partition can host the trace."""
+    partition can host the trace.
+
+    chosen_only=True is run_trial_unit's use (experiment.hpp:337 reads only .chosen): the
+    same chosen entry from one pruned launch (miso_b200_simulate_batch_pruned) whose task
+    order puts each trace's two likeliest winners first (most GPCs, then slice count nearest
+    3); every candidate stops once its JCT sum provably exceeds a completed candidate's.
+    Table entries of stopped candidates read inf (single-instance traces; else the full
+    search)."""
     from .catalog import DEFAULT_CATALOG
     cat = list(catalog if catalog is not None else DEFAULT_CATALOG)
     base = overheads or SimOptions()
@@ -419,26 +488,27 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
                       checkpoint_restart_s=base.checkpoint_restart_s,
                       mps_window_s=base.mps_window_s, interference=base.interference,
                       check_invariants=base.check_invariants, max_events=base.max_events)
-    from .catalog import GPC, MEM_GB
+    from .catalog import GPC
     catc = np.asarray(cat, np.uint8).reshape(-1, 5)
-    largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
-    # min_slice_for per job (topology.hpp:68-72), then the largest per trace (sim.hpp:1036-1041)
-    offs, _, _, _, mem, qos, _ = _csr(traces)
-    if hasattr(mem, "cpu"):  # device-resident batch: the feasibility pass runs on host copies
-        offs, mem, qos = offs.cpu().numpy(), mem.cpu().numpy(), qos.cpu().numpy()
-    qg = np.where(qos >= 0, np.asarray(GPC)[np.maximum(qos, 0)], 0)
-    ok = (np.asarray(MEM_GB)[None, :] >= mem[:, None].astype(np.int64)) & \
-         (np.asarray(GPC)[None, :] >= qg[:, None])
-    fits = ok.any(axis=1)
-    if not fits.all():
-        j = int(np.argmin(fits))
-        ti = int(np.searchsorted(offs, j, side="right") - 1)
-        raise ValueError(f"trace {ti}: a job fits no slice kind")
-    need = np.maximum.reduceat(ok.argmax(axis=1), offs[:-1]) if len(traces) else np.zeros(0, np.int64)
-    feas = largest[None, :] >= need[:, None]                      # (traces, entries)
-    ti_arr, e_arr = np.nonzero(feas)                               # trace-major, catalog order
+    ti_arr, e_arr = static_candidates(traces, cat)
     table = np.full((len(traces), len(cat)), np.inf)
-    if len(ti_arr):
+    inst = _csr(traces)[6]
+    multi = inst is not None and (np.asarray(inst.cpu() if hasattr(inst, "cpu") else inst) > 1).any()
+    if len(ti_arr) and chosen_only and not multi:
+        import torch
+        probe = static_probes(ti_arr, e_arr, catc)
+        dev = torch.device("cuda", ctx.device)
+        st_obj = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st_obj):
+            bound = torch.full((len(traces),), np.iinfo(np.int64).max, dtype=torch.int64, device=dev)
+        # one launch, probes first: they fill the first wave, and the candidates behind them
+        # start with their trace's bound already set
+        sel = np.r_[np.nonzero(probe)[0], np.nonzero(~probe)[0]]
+        res = simulate_batch(ctx, traces, opts, task_trace=ti_arr[sel].astype(np.int32),
+                             static_partitions=catc[e_arr[sel]], jct_only=True, stream=stream,
+                             prune_bound=bound)
+        table[ti_arr[sel], e_arr[sel]] = res.metrics["avg_jct_s"]
+    elif len(ti_arr):
         res = simulate_batch(ctx, traces, opts, task_trace=ti_arr.astype(np.int32),
                              static_partitions=catc[e_arr], jct_only=True, stream=stream)
         # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs

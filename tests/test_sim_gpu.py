@@ -179,6 +179,34 @@ def test_best_static_partition_matches_reference(ctx, ref):
 
 
 @pytest.mark.parametrize("spec", [
+    dict(n=256, job_count=1000, lambda_s=10.0, cluster=100),   # config 4
+    dict(n=96, job_count=300, lambda_s=40.0, cluster=8),       # light load: other winners
+    dict(n=96, job_count=200, lambda_s=2.0, cluster=4),        # heavy queueing
+    dict(n=64, job_count=150, lambda_s=15.0, cluster=6, dist="fixed", fixed_s=900.0),
+])
+def test_chosen_only_static_search_matches_full(ctx, spec):
+    """best_static_partition(chosen_only=True) -- the pruned two-launch search used for
+    run_trial_unit -- chooses the same entry as the full search, with the same avg JCT bits,
+    and every candidate it did not stop has the full search's value."""
+    import paper_2207_11428_b200 as m
+    sp = dict(spec)
+    n, cl = sp.pop("n"), sp.pop("cluster")
+    traces = m.generate_traces(range(500, 500 + n), **sp)
+    full = m.best_static_partition(ctx, traces, cluster_size=cl)
+    fast = m.best_static_partition(ctx, traces, cluster_size=cl, chosen_only=True)
+    stopped = 0
+    for (e0, t0), (e1, t1) in zip(full, fast):
+        assert e0 == e1
+        assert t0[e0].view(np.uint64) == t1[e1].view(np.uint64)
+        kept = np.isfinite(t1)
+        assert np.array_equal(t1[kept].view(np.uint64), t0[kept].view(np.uint64))
+        assert (t1[~kept] == np.inf).all()
+        stopped += int((np.isfinite(t0) & ~kept).sum())
+    if spec["job_count"] >= 300:
+        assert stopped > 0  # the bound does stop candidates at these sizes
+
+
+@pytest.mark.parametrize("spec", [
     dict(job_count=1000, lambda_s=10.0),                       # config 4
     dict(job_count=257, lambda_s=60.0, sigma=0.7),
     dict(job_count=1, lambda_s=5.0),
