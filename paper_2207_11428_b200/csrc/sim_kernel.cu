@@ -330,9 +330,13 @@ __device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
     if (j.first_progress_us < 0) j.first_progress_us = c.now;
     if (c.first_progress < 0) c.first_progress = c.now;
   }
-  c.rate_eff[ji] = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
-  c.stp_dirty = true;
-  if (ji < c.stp_cmin) c.stp_cmin = ji;
+  // the STP window's sums only need redoing from ji if the job's term actually changed
+  const double re = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
+  if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
+    c.rate_eff[ji] = re;
+    c.stp_dirty = true;
+    if (ji < c.stp_cmin) c.stp_cmin = ji;
+  }
   sync_jst(c, ji, j);
 #if MISO_SIM_PRUNE
   if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // remaining / mx, from now
@@ -363,35 +367,32 @@ __device__ void refresh_stp(Ctx& c) {
   if (!c.stp_dirty || !c.p->track_stp) return;
   c.stp_dirty = false;
   const double* r = c.rate_eff;
-  double* P = c.stp_prefix;
+  double* P = c.stp_prefix;  // P[q]: the sum through index 8q + 7, cached at block ends
   const int lo = c.stp_lo, hi = c.n_arrived;
-  int i = c.stp_cmin > lo ? c.stp_cmin : lo;
+  int i0 = c.stp_cmin > lo ? c.stp_cmin : lo;
+  if (i0 > hi) i0 = hi;  // changes at not-yet-arrived indices: the window's sum is unchanged
   c.stp_cmin = INT32_MAX;
-  double s = i > lo ? P[i - 1] : 0.0;
-  for (; i + 8 <= hi; i += 8) {
-    const double a0 = r[i], a1 = r[i + 1], a2 = r[i + 2], a3 = r[i + 3], a4 = r[i + 4],
-                 a5 = r[i + 5], a6 = r[i + 6], a7 = r[i + 7];
-    double p0, p1, p2, p3, p4, p5, p6, p7;
-    p0 = s = s + a0;
-    p1 = s = s + a1;
-    p2 = s = s + a2;
-    p3 = s = s + a3;
-    p4 = s = s + a4;
-    p5 = s = s + a5;
-    p6 = s = s + a6;
-    p7 = s = s + a7;
-    if (lane_id() == 0) {
-      P[i] = p0; P[i + 1] = p1; P[i + 2] = p2; P[i + 3] = p3;
-      P[i + 4] = p4; P[i + 5] = p5; P[i + 6] = p6; P[i + 7] = p7;
-    }
+  // restart at i0's 8-aligned block from the cached sum before it: the block's terms below i0
+  // are unchanged, so re-adding them reproduces the same partial sums (and jobs below lo are
+  // done, contributing +0.0, so a start below lo is exact too)
+  int i = i0 & ~7;
+  double s = (i > 0 && i - 1 >= lo) ? P[(i >> 3) - 1] : 0.0;
+  for (; i + 8 <= hi; i += 8) {  // 64-byte aligned: four 16-byte loads per block
+    const double2* r2 = reinterpret_cast<const double2*>(r + i);
+    const double2 a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
+    s = s + a01.x;
+    s = s + a01.y;
+    s = s + a23.x;
+    s = s + a23.y;
+    s = s + a45.x;
+    s = s + a45.y;
+    s = s + a67.x;
+    s = s + a67.y;
+    if (lane_id() == 0) P[i >> 3] = s;
   }
-  for (; i < hi; ++i) {
-    s = s + r[i];
-    if (lane_id() == 0) P[i] = s;
-  }
+  for (; i < hi; ++i) s = s + r[i];
   __syncwarp();
   if (hi <= lo) s = 0.0;
-  else s = P[hi - 1];
   if (s != c.stp_cur) {
     c.stp_cur = s;
     if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
