@@ -109,6 +109,7 @@ struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
   int lmin_idx;
   bool lmin_valid;
   int chunk;            // slots per lane: lane l owns [l*chunk, (l+1)*chunk)
+  int own_lo;           // this lane's chunk start, lane * chunk (per lane)
   uint8_t* jst;         // [J] SoA job state for warp scans: phase | slice << 3 | done << 6
   uint32_t* freemask;   // optsta: [5][W] bit g set iff GPU g has a free slot of that kind
   double* efftruth;     // [5][J]: effective_speed(truth[k], k, mem, qos) per job (static)
@@ -202,7 +203,8 @@ __device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t
   s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
   ++c.seq;
   c.slots[slot] = s;
-  if (slot / c.chunk == lane_id()) {  // owner lane keeps its minimum current
+  if (static_cast<unsigned>(slot - c.own_lo) < static_cast<unsigned>(c.chunk)) {  // owner lane
+    // keeps its minimum current
     if (c.lmin_idx == slot) c.lmin_valid = false;
     else if (c.lmin_valid && (t < c.lmin_t || (t == c.lmin_t && s.pk < c.lmin_pk))) {
       c.lmin_t = t;
@@ -214,7 +216,7 @@ __device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t
 
 __device__ __forceinline__ void clear_slot(Ctx& c, int slot) {
   c.slots[slot].t = kNoEvent;
-  if (slot / c.chunk == lane_id() && c.lmin_idx == slot) c.lmin_valid = false;
+  if (c.lmin_idx == slot) c.lmin_valid = false;  // a lane's lmin_idx lies in its own chunk
 }
 
 // Next event = minimum live (t, prio, seq) key. Lane l owns the contiguous slot chunk
@@ -1197,6 +1199,7 @@ __global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimB
   c.lmin_idx = -1;
   c.lmin_valid = false;
   c.chunk = (J + G + 31) / 32;
+  c.own_lo = lane * c.chunk;
   c.log = b.log ? b.log + size_t(warp) * b.log_cap : nullptr;
   c.log_cap = b.log_cap;
   c.log_n = 0;
