@@ -296,7 +296,11 @@ int miso_b200_simulate_batch_pruned(miso_b200_ctx* ctx, const miso_b200_sim_opti
 
 /* The same with HOST pointers (synchronous): inputs are copied to the device, results back.
  * n_traces = entries of job_offsets minus one. The C++ binding include/miso_b200_sim.hpp builds
- * run_simulation / best_static_partition / run_experiment_in_memory on this call. */
+ * run_simulation / best_static_partition / run_experiment_in_memory on this call.
+ * MISO_B200_SIM_PRUNE: the tasks are a chosen-only best-static search, run as
+ * miso_b200_simulate_batch_pruned with one bound per trace starting at INT64_MAX (optsta,
+ * task_trace, single-instance traces, metrics only). */
+#define MISO_B200_SIM_PRUNE 2u
 int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
                                   int n_tasks, int n_traces, const int32_t* task_trace,
                                   const uint8_t* static_counts, const int32_t* job_offsets,

@@ -99,8 +99,9 @@ inline ExperimentResult run_experiment_in_memory(const ExperimentConfig& config)
     }
     std::vector<std::optional<PartitionConfig>> static_part(static_cast<size_t>(T));
     if (want_optsta) {
-      auto st = b200::best_static_partition_batch(traces, config.cluster_size, overheads);
-      for (int t = 0; t < T; ++t) static_part[static_cast<size_t>(t)] = st[static_cast<size_t>(t)].chosen;
+      // run_trial_unit reads only .chosen (experiment.hpp:337): the pruned chosen-only search
+      auto st = b200::best_static_chosen_batch(traces, config.cluster_size, overheads);
+      for (int t = 0; t < T; ++t) static_part[static_cast<size_t>(t)] = st[static_cast<size_t>(t)];
     }
     std::map<std::string, std::vector<MetricsReport>> reports;
     for (Policy p : run_policies) {

@@ -24,6 +24,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <limits>
+#include <mutex>
 #include <optional>
 #include <ostream>
 #include <set>
@@ -388,6 +391,109 @@ inline std::vector<StaticSearchResult> best_static_partition_batch(
       }
     }
     if (!found) throw InfeasibleError("no static partition can host this trace");
+  }
+  return out;
+}
+
+// run_trial_unit's use of best_static_partition (experiment.hpp:337 reads only .chosen): the
+// same chosen entries from one pruned launch (MISO_B200_SIM_PRUNE). Every trace is uploaded
+// once, its two likeliest winners (most GPCs, then slice count nearest 3) run first, and every
+// other candidate stops once its JCT sum provably exceeds a completed candidate's
+// (miso_b200_simulate_batch_pruned). Traces with multi-instance jobs take the full search.
+inline std::vector<PartitionConfig> best_static_chosen_batch(
+    const std::vector<const JobTrace*>& traces, int cluster_size, const OverheadSpec& overheads,
+    const PartitionCatalog& catalog = default_catalog()) {
+  std::vector<PartitionConfig> out;
+  bool multi = false;
+  for (const JobTrace* t : traces)
+    for (const TraceJob& j : t->jobs) multi = multi || j.profile.instance_count > 1;
+  if (multi) {
+    for (auto& r : best_static_partition_batch(traces, cluster_size, overheads, catalog))
+      out.push_back(r.chosen);
+    return out;
+  }
+  const size_t E = catalog.entries.size();
+  std::vector<int> prio(E);
+  for (size_t e = 0; e < E; ++e) prio[e] = static_cast<int>(e);
+  auto gpcs = [&](size_t e) {
+    int g = 0;
+    for (int k = 0; k < 5; ++k) g += catalog.entries[e].counts()[static_cast<size_t>(k)] * gpc_count(static_cast<Slice>(k));
+    return g;
+  };
+  auto nsl = [&](size_t e) {
+    int n = 0;
+    for (int k = 0; k < 5; ++k) n += catalog.entries[e].counts()[static_cast<size_t>(k)];
+    return n;
+  };
+  std::stable_sort(prio.begin(), prio.end(), [&](int a, int b) {
+    const int ga = gpcs(size_t(a)), gb = gpcs(size_t(b));
+    if (ga != gb) return ga > gb;
+    return std::abs(nsl(size_t(a)) - 3) < std::abs(nsl(size_t(b)) - 3);
+  });
+  SimOptions opt;
+  opt.policy = Policy::optsta;
+  opt.cluster_size = cluster_size;
+  opt.overheads = overheads;
+  opt.catalog = catalog;
+  opt.static_partition = catalog.entries.front();
+  detail::TraceArrays ta;
+  std::vector<int32_t> probe_tt, rest_tt;
+  std::vector<uint8_t> probe_sc, rest_sc;
+  std::vector<int> probe_e, rest_e;
+  for (size_t ti = 0; ti < traces.size(); ++ti) {
+    detail::validate(*traces[ti], opt);
+    int need = 0;  // largest minimal slice kind over all jobs (sim.hpp:1036-1041)
+    for (const auto& t : traces[ti]->jobs) {
+      auto k = min_slice_for(t.profile.mem_demand_gb,
+                             t.profile.qos_min_slice ? gpc_count(*t.profile.qos_min_slice) : 0);
+      if (!k) throw InfeasibleError("job '" + t.profile.job_id + "' fits no slice kind");
+      need = std::max(need, slice_index(*k));
+    }
+    ta.add(*traces[ti]);
+    int taken = 0;
+    for (int e : prio) {
+      const auto& cand = catalog.entries[size_t(e)];
+      if (slice_index(cand.slices_desc().front()) < need) continue;
+      const bool probe = taken++ < 2;
+      (probe ? probe_tt : rest_tt).push_back(static_cast<int32_t>(ti));
+      (probe ? probe_e : rest_e).push_back(e);
+      for (int k = 0; k < 5; ++k)
+        (probe ? probe_sc : rest_sc).push_back(cand.counts()[static_cast<size_t>(k)]);
+    }
+  }
+  probe_tt.insert(probe_tt.end(), rest_tt.begin(), rest_tt.end());
+  probe_sc.insert(probe_sc.end(), rest_sc.begin(), rest_sc.end());
+  probe_e.insert(probe_e.end(), rest_e.begin(), rest_e.end());
+  const size_t n = probe_tt.size();
+  std::vector<miso_b200_sim_metrics> met(n);
+  if (n) {
+    std::vector<uint64_t> seeds(n, opt.predictor.rng_seed);
+    const miso_b200_sim_options c = detail::to_c(opt);
+    Device& d = Device::get();
+    std::lock_guard<std::mutex> lock(d.mu());
+    d.use_catalog(catalog);
+    Device::check(miso_b200_simulate_batch_host(
+        d.ctx(), &c, static_cast<int>(n), static_cast<int>(traces.size()), probe_tt.data(),
+        probe_sc.data(), ta.offsets.data(), ta.arrival.data(), ta.base.data(), ta.speeds.data(),
+        ta.mem.data(), ta.qos.data(), nullptr, seeds.data(), met.data(), nullptr, nullptr, 0,
+        nullptr, 0, MISO_B200_SIM_JCT_ONLY | MISO_B200_SIM_PRUNE));
+  }
+  std::vector<std::vector<double>> table(traces.size(),
+                                         std::vector<double>(E, std::numeric_limits<double>::infinity()));
+  for (size_t i = 0; i < n; ++i) {
+    if (met[i].status && met[i].status != MISO_B200_SIM_PRUNED) detail::throw_status(met[i].status);
+    table[size_t(probe_tt[i])][size_t(probe_e[i])] = met[i].avg_jct_s;
+  }
+  for (size_t ti = 0; ti < traces.size(); ++ti) {
+    double best = std::numeric_limits<double>::infinity();
+    std::optional<PartitionConfig> chosen;
+    for (size_t e = 0; e < E; ++e)  // first minimum in catalog order (sim.hpp:1058)
+      if (table[ti][e] < best) {
+        best = table[ti][e];
+        chosen = catalog.entries[e];
+      }
+    if (!chosen) throw InfeasibleError("no static partition can host this trace");
+    out.push_back(*chosen);
   }
   return out;
 }

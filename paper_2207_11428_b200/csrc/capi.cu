@@ -794,6 +794,16 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
       !metrics)
     return fail(MISO_B200_E_INVALID, "null buffer");
   if (!task_trace && n_traces < n_tasks) return fail(MISO_B200_E_INVALID, "fewer traces than tasks");
+  const bool prune = (flags & MISO_B200_SIM_PRUNE) != 0;
+  flags &= ~MISO_B200_SIM_PRUNE;
+  if (prune) {  // miso_b200_simulate_batch_pruned's contract
+    if (opt->policy != MISO_B200_POLICY_OPTSTA || !task_trace)
+      return fail(MISO_B200_E_INVALID, "pruned runs are optsta candidate searches with task_trace");
+    if (job_out || log || stp_series)
+      return fail(MISO_B200_E_INVALID, "pruned runs return metrics only");
+    for (int q = 0; instances && q < job_offsets[n_traces]; ++q)
+      if (instances[q] != 1) return fail(MISO_B200_E_INVALID, "pruned runs take single-instance traces");
+  }
   for (int i = 0; i < n_traces; ++i)
     if (job_offsets[i + 1] < job_offsets[i]) return fail(MISO_B200_E_INVALID, "job_offsets must be non-decreasing");
   if (task_trace)
@@ -832,15 +842,19 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if ((rc = alloc_out(d_log, log_n * sizeof(miso_b200_log_record)))) return rc;
   const size_t stp_n = stp_series ? size_t(n_tasks) * 2 * size_t(std::max<int64_t>(stp_cap, 0)) : 0;
   if ((rc = alloc_out(d_stp, stp_n * sizeof(double)))) return rc;
-  rc = miso_b200_simulate_batch_ex(
+  DevBuf d_bound;
+  std::vector<int64_t> b0(prune ? size_t(n_traces) : 0, INT64_MAX);  // no completed candidate yet
+  if ((rc = upload(d_bound, b0.data(), b0.size(), s))) return rc;
+  rc = simulate_impl(
       ctx, opt, n_tasks, static_cast<const int32_t*>(d_tt.p), static_cast<const uint8_t*>(d_sc.p),
       static_cast<const int32_t*>(d_off.p), static_cast<const double*>(d_arr.p),
       static_cast<const double*>(d_base.p), static_cast<const double*>(d_sp.p),
       static_cast<const uint8_t*>(d_mem.p), static_cast<const int8_t*>(d_qos.p),
-      static_cast<const uint8_t*>(d_inst.p), static_cast<const uint64_t*>(d_seed.p),
+      prune ? nullptr : static_cast<const uint8_t*>(d_inst.p), static_cast<const uint64_t*>(d_seed.p),
       static_cast<miso_b200_sim_metrics*>(d_met.p),
       nullptr, static_cast<int64_t*>(d_jo.p), static_cast<miso_b200_log_record*>(d_log.p),
-      log ? log_cap : 0, static_cast<double*>(d_stp.p), stp_series ? stp_cap : 0, flags, s);
+      log ? log_cap : 0, static_cast<double*>(d_stp.p), stp_series ? stp_cap : 0, flags,
+      prune ? static_cast<int64_t*>(d_bound.p) : nullptr, s);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(metrics, d_met.p, sizeof(miso_b200_sim_metrics) * size_t(n_tasks),
                            cudaMemcpyDeviceToHost, s));
