@@ -554,11 +554,6 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
         stamps[4] = hit;
         stamps[5] = uint64_t(c2 - c1);
         stamps[6] = uint64_t(clock64() - c2);
-        DrawSlot& sl = da.slot[(s_a.nonce + 1) % kAheadSlots];  // the next call's slot
-        stamps[12] = sh_ld(&sl.ver);
-        stamps[13] = sh_ld(&sl.nonce);
-        stamps[14] = sh_ld(&da.posted);
-        stamps[15] = s_a.nonce;
       }
       last = seq;
       __syncwarp();

@@ -82,8 +82,6 @@ int main(int argc, char** argv) {
     for (int q = 0; q < 3; ++q) cyc[q].push_back(double(st[4 + q]));
     for (int q = 0; q < 3; ++q) ph[q].push_back(double(st[8 + q]));
   }
-  printf("slot(next) ver=%llu nonce=%llu posted=%llu req_nonce=%llu\n", (unsigned long long)st[12],
-         (unsigned long long)st[13], (unsigned long long)st[14], (unsigned long long)st[15]);
   *reinterpret_cast<volatile uint64_t*>(&mb->stop) = 1;
   cudaStreamSynchronize(s);
   auto med = [](std::vector<double> v) {
@@ -93,7 +91,7 @@ int main(int argc, char** argv) {
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   printf("{\"host_roundtrip_us\": %.3f, \"fetch_ns\": %.0f, \"compute_ns\": %.0f, \"publish_ns\": %.0f, "
-         "\"fetch_cyc\": %.0f, \"compute_cyc\": %.0f, \"publish_cyc\": %.0f, \"clock_khz\": %d, \"obj\": %.17g, "
+         "\"hit\": %.0f, \"compute_cyc\": %.0f, \"publish_cyc\": %.0f, \"clock_khz\": %d, \"obj\": %.17g, "
          "\"perturb_cyc\": %.0f, \"predict_cyc\": %.0f, \"search_cyc\": %.0f, \"err\": \"%s\"}\n",
          med(host_us), med(fetch_ns), med(comp_ns), med(pub_ns), med(cyc[0]), med(cyc[1]), med(cyc[2]),
          clk, out->obj, med(ph[0]), med(ph[1]), med(ph[2]), cudaGetErrorString(cudaGetLastError()));
