@@ -29,7 +29,7 @@ def ev(stream):
     return e
 
 
-def batch(chosen_only):
+def batch(chosen_only, chunks=1):
     t0 = ev(torch.cuda.current_stream())
     for s in (s_a, s_b, s_c):
         s.wait_stream(torch.cuda.current_stream())
@@ -40,7 +40,11 @@ def batch(chosen_only):
     p_mis = miso.simulate_batch(ctx_c, traces, miso.SimOptions(policy="miso", cluster_size=100, predictor="noisy"), stream=s_c, defer=True)
     c1 = ev(s_c)
     b0 = ev(s_b)
-    st = miso.best_static_partition(ctx_b, traces, cluster_size=100, stream=s_b, chosen_only=chosen_only)
+    st = []
+    step = S // chunks
+    for c in range(chunks):  # fewer concurrent static warps: smaller L2 footprint beside miso
+        st += miso.best_static_partition(ctx_b, traces[c * step:(c + 1) * step], cluster_size=100,
+                                         stream=s_b, chosen_only=chosen_only)
     b1 = ev(s_b)
     miso.simulate_batch(ctx_b, traces, miso.SimOptions(policy="optsta", cluster_size=100),
                         static_partitions=[miso.DEFAULT_CATALOG[e] for e, _ in st], stream=s_b)
@@ -90,9 +94,8 @@ def batch_probes_full():
 
 
 out = {}
-for mode in (False, True, False, True):
-    batch(mode)
-    out["chosen_only" if mode else "full"] = batch(mode)
-batch_probes_full()
-out["probes_full"] = batch_probes_full()
+for rep in range(2):
+    for mode in (False, True):
+        batch(mode)
+        out[f"{'pruned' if mode else 'full'}_{rep}"] = batch(mode)
 print(json.dumps(out))
