@@ -100,8 +100,13 @@ int launch_server(miso_b200_ctx* ctx, uint64_t last) {
   }
   *reinterpret_cast<volatile uint64_t*>(&ctx->h_mail->stop) = 0;
   std::atomic_thread_fence(std::memory_order_seq_cst);
+  static const uint32_t poll_ns = [] {  // spacing of the server's two in-flight polls (about
+    const char* e = getenv("MISO_B200_DECIDE_POLL_NS");  // half a PCIe read round trip)
+    return e ? static_cast<uint32_t>(std::max(0, atoi(e))) : 400u;
+  }();
   CUDA_TRY(launch_decide_server(ctx->d_mail, static_cast<DecideOneOut*>(ctx->d_stage), last,
-                                uint64_t(ctx->srv_idle_ns), kServerLifeNs, ctx->srv_stream));
+                                uint64_t(ctx->srv_idle_ns), kServerLifeNs, ctx->srv_stream,
+                                nullptr, poll_ns));
   CUDA_TRY(cudaEventRecord(ctx->srv_done, ctx->srv_stream));
   ctx->srv_live = true;
   return MISO_B200_OK;

@@ -68,9 +68,10 @@ inline uint64_t mbx_mix(uint64_t w, uint64_t i) {  // splitmix64 finaliser of (w
 cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStream_t stream);
 // stamps (timing probe only, else nullptr): globaltimer at request seen / roster fetched /
 // computed / published, written after each request.
+// poll_ns: spacing of the server's two in-flight mailbox polls.
 cudaError_t launch_decide_server(const DecideMailbox* mb, DecideOneOut* out, uint64_t last,
                                  uint64_t idle_ns, uint64_t life_ns, cudaStream_t stream,
-                                 uint64_t* stamps = nullptr);
+                                 uint64_t* stamps = nullptr, uint32_t poll_ns = 0);
 
 // Device: generate_trace for n seeds, one warp per trace (trace_kernel.cu). mu = the
 // lognormal's log(max_duration_s) - kZ90 * sigma, computed on the host as the reference does.

@@ -477,7 +477,7 @@ __device__ __forceinline__ bool take_ahead(DrawAhead& da, uint64_t rng_seed, uin
 __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* mb,
                                                            DecideOneOut* out, uint64_t last,
                                                            uint64_t idle_ns, uint64_t life_ns,
-                                                           uint64_t* stamps) {
+                                                           uint64_t* stamps, uint32_t poll_ns) {
   __shared__ DecideOneArgs s_a;
   __shared__ DecideOneOut s_o;
   __shared__ DrawAhead da;
@@ -503,22 +503,24 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
   bool want_pre = false, have_pre = false;
   uint64_t pre_seed = 0, pre_nonce = 0;
   NoiseDraw pre{0.0, false};
-  for (;;) {
-    unsigned long long w0 = 0, w1 = 0;
+  auto poll = [&](unsigned long long& w0, unsigned long long& w1) {
     if (lane < 20)
       asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
                    : "=l"(w0), "=l"(w1) : "l"(src + 2 * lane) : "memory");
+  };
+  // One fetched mailbox image: serve it if it holds a new request; true = exit.
+  auto serve = [&](unsigned long long w0, unsigned long long w1) -> bool {
     if (want_pre && !have_pre) have_pre = take_ahead(da, pre_seed, pre_nonce, pre);
     const uint64_t seq = __shfl_sync(0xffffffffu, (kArgSeqWord & 1) ? w1 : w0, kArgSeqWord >> 1);
     const uint64_t stop = __shfl_sync(0xffffffffu, w1, 19);
-    if (stop) break;
+    if (stop) return true;
     if (seq != last) {
       const uint64_t ts0 = stamps ? global_ns() : 0;
       uint64_t part = 0;
       if (2 * lane < kArgWords) part += mbx_mix(w0, uint64_t(2 * lane));
       if (2 * lane + 1 < kArgWords) part += mbx_mix(w1, uint64_t(2 * lane + 1));
       const uint64_t check = __shfl_sync(0xffffffffu, w0, kArgWords >> 1);  // word kArgWords
-      if (warp_sum_u64(part) != check) continue;  // torn fetch: poll again
+      if (warp_sum_u64(part) != check) return false;  // torn fetch: poll again
       uint64_t* dst = reinterpret_cast<uint64_t*>(&s_a);
       if (2 * lane < kArgWords) dst[2 * lane] = w0;
       if (2 * lane + 1 < kArgWords) dst[2 * lane + 1] = w1;
@@ -558,10 +560,22 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
       last = seq;
       __syncwarp();
       t_last = global_ns();
-      continue;
+      return false;
     }
     const uint64_t now = global_ns();
-    if (now - t_last > idle_ns || now - t0 > life_ns) break;
+    return now - t_last > idle_ns || now - t0 > life_ns;
+  };
+  // Two polls in flight, issued poll_ns apart: the mailbox is sampled twice per PCIe round
+  // trip, so a request waits about a quarter round trip less to be noticed.
+  unsigned long long a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+  poll(a0, a1);
+  for (;;) {
+    if (poll_ns) __nanosleep(poll_ns);
+    poll(b0, b1);
+    if (serve(a0, a1)) break;
+    if (poll_ns) __nanosleep(poll_ns);
+    poll(a0, a1);
+    if (serve(b0, b1)) break;
   }
   if (lane == 0) sh_st(&da.quit, 1u);
 }
@@ -573,8 +587,8 @@ cudaError_t launch_decide_one(const DecideOneArgs& a, DecideOneOut* out, cudaStr
 
 cudaError_t launch_decide_server(const DecideMailbox* mb, DecideOneOut* out, uint64_t last,
                                  uint64_t idle_ns, uint64_t life_ns, cudaStream_t stream,
-                                 uint64_t* stamps) {
-  decide_server_kernel<<<1, 64, 0, stream>>>(mb, out, last, idle_ns, life_ns, stamps);
+                                 uint64_t* stamps, uint32_t poll_ns) {
+  decide_server_kernel<<<1, 64, 0, stream>>>(mb, out, last, idle_ns, life_ns, stamps, poll_ns);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,7 @@ using namespace miso_b200;
 
 int main(int argc, char** argv) {
   const int K = argc > 1 ? atoi(argv[1]) : 2000;
+  const uint32_t poll_ns = argc > 2 ? uint32_t(atoi(argv[2])) : 0u;
   double arr[3], dur[3], sp[15];
   int mem[3];
   miso_b200_generate_trace(7, 3, 10.0, 7200.0, 0, 1.5, 0, 0, 0, arr, dur, sp, mem);
@@ -49,7 +50,7 @@ int main(int argc, char** argv) {
   a.en1 = (1ull << (kNumCands - 64)) - 1;
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  launch_decide_server(mb, out, 0, 2000000000ull, 4000000000ull, s, st);
+  launch_decide_server(mb, out, 0, 2000000000ull, 4000000000ull, s, st, poll_ns);
   std::vector<double> host_us, fetch_ns, comp_ns, pub_ns, cyc[3], ph[3];
   std::vector<double> dev_total;
   for (int k = 1; k <= K + 100; ++k) {
@@ -90,10 +91,10 @@ int main(int argc, char** argv) {
   };
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-  printf("{\"host_roundtrip_us\": %.3f, \"fetch_ns\": %.0f, \"compute_ns\": %.0f, \"publish_ns\": %.0f, "
+  printf("{\"poll_ns\": %u, \"host_roundtrip_us\": %.3f, \"fetch_ns\": %.0f, \"compute_ns\": %.0f, \"publish_ns\": %.0f, "
          "\"hit\": %.0f, \"compute_cyc\": %.0f, \"publish_cyc\": %.0f, \"clock_khz\": %d, \"obj\": %.17g, "
          "\"perturb_cyc\": %.0f, \"predict_cyc\": %.0f, \"search_cyc\": %.0f, \"err\": \"%s\"}\n",
-         med(host_us), med(fetch_ns), med(comp_ns), med(pub_ns), med(cyc[0]), med(cyc[1]), med(cyc[2]),
+         poll_ns, med(host_us), med(fetch_ns), med(comp_ns), med(pub_ns), med(cyc[0]), med(cyc[1]), med(cyc[2]),
          clk, out->obj, med(ph[0]), med(ph[1]), med(ph[2]), cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
