@@ -4,7 +4,7 @@ set -x
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_predict_gpu.py -x -q > gpurun_out/pytest_c1.txt 2>&1
 tail -3 gpurun_out/pytest_c1.txt
-for i in 1 2; do timeout 60 ./tools/decide_probe.bin 3000; done > gpurun_out/probe.txt 2>&1
+for i in 1 2; do timeout 60 ./tools/decide_probe.bin 3000 400; done > gpurun_out/probe.txt 2>&1
 cat gpurun_out/probe.txt
 timeout 300 python bench.py --config c1 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
 cat gpurun_out/bench_c1.json; tail -5 gpurun_out/bench_c1.err
