@@ -211,3 +211,10 @@ def test_decide_server_matches_launch_mode(ctx, oracle):
         est = oracle.predict_batch(t3, m, nonce, 5, 1, 0.017, w2, w1).reshape(m, 5)
         est = zero_eff(est, np.array([j[2] for j in jobs]), np.array([-1 if j[3] is None else j[3] for j in jobs]))
         assert np.array_equal(bits(est), est_bits)
+
+
+def test_decide_server_option_checked(ctx):
+    import paper_2207_11428_b200 as m
+    with pytest.raises(m.MisoError) as ei:
+        ctx.decide_server(-1)
+    assert ei.value.code == -2

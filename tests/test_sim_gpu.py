@@ -144,6 +144,35 @@ def test_invalid_sim_options(ctx):
         assert ei.value.code == -2
 
 
+def test_pruned_search_contract(ctx):
+    """miso_b200_simulate_batch_pruned rejects what its bound cannot cover: another policy,
+    no task_trace, multi-instance traces (the Python wrapper), per-job outputs."""
+    import torch
+    import paper_2207_11428_b200 as m
+    tr = m.generate_traces(range(3), 40, lambda_s=20.0)
+    bound = torch.full((3,), np.iinfo(np.int64).max, dtype=torch.int64, device="cuda")
+    part = [m.DEFAULT_CATALOG[8]] * 3
+    with pytest.raises(m.MisoError) as ei:
+        m.simulate_batch(ctx, tr, m.SimOptions(policy="nopart", cluster_size=4), task_trace=[0, 1, 2],
+                         static_partitions=part, prune_bound=bound)
+    assert ei.value.code == -2
+    with pytest.raises(m.MisoError):
+        m.simulate_batch(ctx, tr, m.SimOptions(policy="optsta", cluster_size=4),
+                         static_partitions=part, prune_bound=bound)
+    with pytest.raises(ValueError):
+        m.simulate_batch(ctx, tr, m.SimOptions(policy="optsta", cluster_size=4), task_trace=[0, 1, 2],
+                         static_partitions=part, prune_bound=bound, want_jct=True)
+    # a completed candidate lowers its trace's bound to its exact JCT sum (us)
+    res = m.simulate_batch(ctx, tr, m.SimOptions(policy="optsta", cluster_size=4), task_trace=[0, 1, 2],
+                           static_partitions=part, prune_bound=bound, jct_only=True)
+    full = m.simulate_batch(ctx, tr, m.SimOptions(policy="optsta", cluster_size=4),
+                            static_partitions=part, want_jct=True)
+    assert (res.metrics["status"] == 0).all()
+    want = [int(np.asarray(j).sum()) for j in full.job_jct_us]
+    assert bound.cpu().tolist() == want
+    assert np.array_equal(res.metrics["avg_jct_s"].view(np.uint64), full.metrics["avg_jct_s"].view(np.uint64))
+
+
 def test_optsta_event_log_parity(ctx, ref):
     """optsta policy (sim.hpp:493-572): fixed slots, largest-free-slot admission and
     small-to-large migrations with checkpoint restarts, byte-identical logs."""
