@@ -74,7 +74,8 @@ int miso_b200_optimize_batch(miso_b200_ctx* ctx, const double* speeds, const uin
                              uint64_t n, uint8_t* cand, double* obj, void* stream);
 
 /* Same contract with HOST pointers: chunked H2D -> search -> D2H pipeline over two streams.
- * Synchronous. */
+ * Synchronous. Offsets are validated chunk by chunk as the pipeline advances: on
+ * MISO_B200_E_MALFORMED, results of instances before the offending chunk may have been written. */
 int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
                                   const uint32_t* offsets, uint64_t n, uint8_t* cand,
                                   double* obj);

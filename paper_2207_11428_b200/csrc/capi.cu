@@ -284,8 +284,7 @@ int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
   if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
   if (n == 0) return MISO_B200_OK;
   if (!speeds || !offsets || !cand || !obj) return fail(MISO_B200_E_INVALID, "null buffer");
-  for (uint64_t i = 0; i < n; ++i)
-    if (offsets[i + 1] < offsets[i]) return fail(MISO_B200_E_MALFORMED, "offsets must be non-decreasing");
+  if (offsets[n] < offsets[0]) return fail(MISO_B200_E_MALFORMED, "offsets must be non-decreasing");
   DeviceGuard g(ctx->device);
   const size_t rows = offsets[n];
   int rc = ensure_host_scratch(ctx, rows, n);
@@ -300,6 +299,15 @@ int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
   for (uint64_t i0 = 0; i0 < n; i0 += kChunk, ++k) {
     const uint64_t i1 = std::min(n, i0 + kChunk);
     cudaStream_t s = ctx->streams[k & 1];
+    // each chunk's offsets are checked just before its copies are queued, so the host check
+    // of chunk k+1 overlaps the transfers of chunk k (a malformed chunk stops the pipeline:
+    // earlier chunks' results may have been written)
+    for (uint64_t i = i0; i < i1; ++i)
+      if (offsets[i + 1] < offsets[i] || offsets[i + 1] > rows) {  // (rows = offsets[n])
+        cudaStreamSynchronize(ctx->streams[0]);
+        cudaStreamSynchronize(ctx->streams[1]);
+        return fail(MISO_B200_E_MALFORMED, "offsets must be non-decreasing");
+      }
     const uint32_t r0 = offsets[i0], r1 = offsets[i1];
     CUDA_TRY(cudaMemcpyAsync(ctx->d_offsets + i0, offsets + i0, (i1 - i0 + 1) * sizeof(uint32_t),
                              cudaMemcpyHostToDevice, s));

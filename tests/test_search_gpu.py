@@ -71,6 +71,30 @@ def test_job_count_out_of_range(ctx):
     assert list(cand) == [0xFE, 0xFE, 0xFE] and list(obj) == [0, 0, 0]
 
 
+def test_host_path_rejects_malformed_offsets(ctx, oracle):
+    """miso_b200_optimize_batch_host validates offsets chunk by chunk (131072 instances per
+    chunk): a decrease or an offset beyond offsets[n] anywhere -- first chunk, a later chunk,
+    the last entry -- fails with MISO_B200_E_MALFORMED and copies nothing out of bounds; a
+    valid batch afterwards is still exact."""
+    import paper_2207_11428_b200 as m
+    n = 300_000
+    rng = np.random.default_rng(3)
+    mm = rng.integers(1, 8, n)
+    offs = np.concatenate([[0], np.cumsum(mm)]).astype(np.uint32)
+    sp = rng.random((int(offs[-1]), 5))
+    for pos, val in ((5, None), (200_000, None), (n, None), (10, int(offs[-1]) + 100)):
+        bad = offs.copy()
+        bad[pos] = bad[pos - 1] - 1 if val is None else val
+        with pytest.raises(m.MisoError) as ei:
+            ctx.optimize_batch(sp[: int(max(bad[-1], 1))] if bad[-1] < offs[-1] else sp, bad)
+        assert ei.value.code == -3
+    cand, obj = ctx.optimize_batch(sp, offs)
+    e, p, ob = oracle.optimize_batch(sp.reshape(-1), offs)
+    ge, _ = ctx.decode(cand, offs)
+    assert np.array_equal(ge, e.astype(np.int32))
+    assert np.array_equal(obj.view(np.uint64), ob.view(np.uint64))
+
+
 def test_empty_batch(ctx):
     cand, obj = ctx.optimize_batch(np.zeros(0), np.array([0], np.uint32))
     assert len(cand) == 0 and len(obj) == 0
