@@ -99,11 +99,18 @@ int miso_b200_default_model(double w2[4], double w1[4]);
  * 0..cols_per_group-1, pad_to_seven profiles.hpp:106-113). truth3: (f7, f4, f3) per column;
  * out5: the estimated speed table per column, kind order 1g..7g. mode 0 = oracle, 1 = noisy
  * (PredictorSpec::Mode, profiles.hpp:173-178); target_mae in [0, 0.5] else -2. w2/w1 NULL =
- * the default model. */
+ * the default model. mode 2 = extrapolate_small_slices alone (profiles.hpp:370-384): truth3
+ * holds a mig matrix's (7g, 4g, 3g) rows, taken as given (no re-anchoring), and out5 gets
+ * them back with the extrapolated 2g/1g. */
 int miso_b200_predict_batch(miso_b200_ctx* ctx, const double* truth3, uint64_t ncols,
                             int cols_per_group, uint64_t first_nonce, uint64_t rng_seed, int mode,
                             double target_mae, const double* w2, const double* w1, double* out5,
                             void* stream);
+
+/* The same with HOST pointers (synchronous). */
+int miso_b200_predict_host(miso_b200_ctx* ctx, const double* truth3, uint64_t ncols,
+                           int cols_per_group, uint64_t first_nonce, uint64_t rng_seed, int mode,
+                           double target_mae, const double* w2, const double* w1, double* out5);
 
 /* Fused per-GPU decision for n rosters, DEVICE pointers: for each instance i (jobs
  * offsets[i]..offsets[i+1]-1 in columns 0..m-1, call nonce nonce[i]) predict every job's

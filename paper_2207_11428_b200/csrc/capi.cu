@@ -364,7 +364,8 @@ int miso_b200_predict_batch(miso_b200_ctx* ctx, const double* truth3, uint64_t n
                             double target_mae, const double* w2, const double* w1, double* out5,
                             void* stream) {
   if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
-  if (int rc = check_predictor(mode, target_mae)) return rc;
+  if (mode != 2)
+    if (int rc = check_predictor(mode, target_mae)) return rc;
   if (cols_per_group < 1 || cols_per_group > 7)
     return fail(MISO_B200_E_INVALID, "cols_per_group must be 1..7 (pad_to_seven)");
   if (ncols == 0) return MISO_B200_OK;
@@ -874,6 +875,29 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if (jo_n) CUDA_TRY(cudaMemcpyAsync(job_out, d_jo.p, jo_n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   if (log_n) CUDA_TRY(cudaMemcpyAsync(log, d_log.p, log_n * sizeof(miso_b200_log_record), cudaMemcpyDeviceToHost, s));
   if (stp_n) CUDA_TRY(cudaMemcpyAsync(stp_series, d_stp.p, stp_n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return MISO_B200_OK;
+}
+
+int miso_b200_predict_host(miso_b200_ctx* ctx, const double* truth3, uint64_t ncols,
+                           int cols_per_group, uint64_t first_nonce, uint64_t rng_seed, int mode,
+                           double target_mae, const double* w2, const double* w1, double* out5) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (ncols == 0) return MISO_B200_OK;
+  if (!truth3 || !out5) return fail(MISO_B200_E_INVALID, "null buffer");
+  DeviceGuard g(ctx->device);
+  if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
+  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  cudaStream_t s = ctx->streams[0];
+  DevBuf d_in, d_out;
+  int rc;
+  if ((rc = upload(d_in, truth3, size_t(ncols) * 3, s))) return rc;
+  if ((rc = alloc_out(d_out, size_t(ncols) * 5 * sizeof(double)))) return rc;
+  rc = miso_b200_predict_batch(ctx, static_cast<const double*>(d_in.p), ncols, cols_per_group,
+                               first_nonce, rng_seed, mode, target_mae, w2, w1,
+                               static_cast<double*>(d_out.p), s);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out5, d_out.p, size_t(ncols) * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return MISO_B200_OK;
 }

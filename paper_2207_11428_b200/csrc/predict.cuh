@@ -168,7 +168,7 @@ struct ModelW {
 __device__ __forceinline__ void predict_column(double f7, double f4, double f3, int col,
                                                uint64_t rng_seed, uint64_t nonce, bool noisy,
                                                double target_mae, const ModelW& w,
-                                               double out5[5]) {
+                                               double out5[5], bool anchor = true) {
   double v0 = f7, v1 = f4, v2 = f3;
   if (noisy && target_mae > 0.0) {  // (target_mae <= 0: perturb_speed returns the truth)
     const uint64_t base = mix_seed(rng_seed, nonce);
@@ -178,12 +178,14 @@ __device__ __forceinline__ void predict_column(double f7, double f4, double f3, 
     v1 = perturb_with(f4, target_mae, ra);
     v2 = perturb_with(f3, target_mae, rb);
   }
-  double mx = v0;  // std::max({a, b, c})
-  if (mx < v1) mx = v1;
-  if (mx < v2) mx = v2;
-  v0 = clampd(v0 / mx, kSpeedFloor, 1.0);
-  v1 = clampd(v1 / mx, kSpeedFloor, 1.0);
-  v2 = clampd(v2 / mx, kSpeedFloor, 1.0);
+  if (anchor) {  // (anchor = false: extrapolate_small_slices alone, on given mig rows)
+    double mx = v0;  // std::max({a, b, c})
+    if (mx < v1) mx = v1;
+    if (mx < v2) mx = v2;
+    v0 = clampd(v0 / mx, kSpeedFloor, 1.0);
+    v1 = clampd(v1 / mx, kSpeedFloor, 1.0);
+    v2 = clampd(v2 / mx, kSpeedFloor, 1.0);
+  }
   const double p2 = w.w2[0] * v0 + w.w2[1] * v1 + w.w2[2] * v2 + w.w2[3];
   const double p1 = w.w1[0] * v0 + w.w1[1] * v1 + w.w1[2] * v2 + w.w1[3];
   const double f2 = clampd(p2, kSpeedFloor, v2);

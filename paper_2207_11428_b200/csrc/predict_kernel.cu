@@ -34,8 +34,8 @@ __global__ void __launch_bounds__(kPredBlock) predict_batch_kernel(
     const uint64_t g = j / static_cast<uint64_t>(cpg);
     const int c = static_cast<int>(j - g * static_cast<uint64_t>(cpg));
     const double* t = s_in + threadIdx.x * 3;
-    predict_column(t[0], t[1], t[2], c, rng_seed, first_nonce + g, noisy != 0, target_mae, w,
-                   s_out + threadIdx.x * 5);
+    predict_column(t[0], t[1], t[2], c, rng_seed, first_nonce + g, noisy == 1, target_mae, w,
+                   s_out + threadIdx.x * 5, noisy != 2);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < cnt * 5; i += kPredBlock) out5[j0 * 5 + i] = s_out[i];

@@ -25,11 +25,13 @@ def test_reference_optimizer_tests_against_b200():
 # The reference's simulator, experiment and acceptance test files, compiled unmodified with
 # run_simulation / best_static_partition / run_experiment_in_memory routed to the B200 binding
 # (tools/dropin/prelude_sim.hpp): every test passes, multi-instance clone spawning included.
-EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set()}
-TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9}
+# profiles_test.cpp runs the same way with predict_mig_speeds / extrapolate_small_slices routed
+# to the B200 predictor (tools/dropin/prelude_profiles.hpp).
+EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set(), "profiles": set()}
+TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9, "profiles": 19}
 
 
-@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance"])
+@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance", "profiles"])
 def test_reference_sim_experiment_tests_against_b200(name):
     b = BIN.parent / f"{name}_test_b200"
     if not b.exists():
