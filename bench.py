@@ -249,6 +249,17 @@ def bench_c3(args):
                "sample": f"{k} profiles, {threads} threads"}
     peak, src = measured_peak()
     gbs = n * 64 / (ms / 1e3) / 1e9
+    # the binding roof is the FMA-heavy pipe (every IMAD of the seeding chains): its busy
+    # fraction from the committed ncu capture of this kernel
+    compute = None
+    cap = ROOT / "profiles" / "predict_kernel_ncu.json"
+    if cap.exists():
+        l0 = json.loads(cap.read_text())["launches"][0]
+        pct = lambda k: float(str(l0.get(k, "nan")).split()[0]) / 100  # noqa: E731
+        compute = {"bound": "FMA-heavy pipe (IMAD: 3 integer multiplies per mt19937_64 seeding step, 158 steps x 2 entries per profile)",
+                   "ncu_pipe_busy": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                   "ncu_issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                   "source": "profiles/predict_kernel_ncu.json (ncu --set full of this kernel, 16M profiles)"}
     print(json.dumps({"metric": "MPS profiles predicted/sec (config 3, noisy, mae 0.017)",
                       "value": n / (ms / 1e3), "unit": "profiles/s", "ms_per_step": ms,
                       "steps": args.steps, "warmup": args.warmup, "n_profiles": n,
@@ -256,6 +267,7 @@ def bench_c3(args):
                       "roofline": {"bound": "int-issue (mt19937_64 seeding); hbm shown for scale",
                                    "achieved_gbs": gbs, "peak_gbs": peak, "frac_hbm": gbs / peak,
                                    "algorithmic_bytes_per_profile": 64},
+                      "compute_roofline": compute,
                       "cpu_baseline": cpu}), flush=True)
 
 
