@@ -232,6 +232,15 @@ int miso_b200_generate_traces_device(miso_b200_ctx* ctx, const uint64_t* seeds, 
                                      double hi_s, double* arrival_s, double* duration_s,
                                      double* speeds5, int* mem_gb, void* stream);
 
+/* The same generation on the device with HOST pointers (synchronous): seeds in, the arrays out
+ * (n_traces x job_count, trace-major). */
+int miso_b200_generate_traces_device_host(miso_b200_ctx* ctx, const uint64_t* seeds,
+                                          int n_traces, int job_count, double lambda_s,
+                                          double max_duration_s, int dist, double sigma,
+                                          double fixed_s, double lo_s, double hi_s,
+                                          double* arrival_s, double* duration_s, double* speeds5,
+                                          int* mem_gb);
+
 /* run_simulation (sim.hpp:976-979) for n_seeds independent tasks at once, one warp per task,
  * DEVICE pointers. Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r owns
  * jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in

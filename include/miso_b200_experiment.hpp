@@ -18,8 +18,9 @@
 namespace miso {
 namespace b200 {
 
-// Trace generation for many seeds on every host thread (miso_b200_generate_traces), identical
-// to generate_trace(spec) per seed (job ids "j<i>", workload.hpp:97-114).
+// Trace generation for many seeds on the device (miso_b200_generate_traces_device_host: one
+// warp per trace, glibc-exact libm restatements), identical to generate_trace(spec) per seed
+// (job ids "j<i>", workload.hpp:97-114).
 inline std::vector<JobTrace> generate_traces(const TraceSpec& spec, const std::vector<uint64_t>& seeds) {
   validate_trace_spec(spec);
   const size_t n = seeds.size(), J = static_cast<size_t>(spec.job_count);
@@ -28,11 +29,15 @@ inline std::vector<JobTrace> generate_traces(const TraceSpec& spec, const std::v
   const int kind = spec.duration_dist.kind == DurationDist::Kind::lognormal ? 0
                    : spec.duration_dist.kind == DurationDist::Kind::fixed   ? 1
                                                                             : 2;
-  if (n)
-    Device::check(miso_b200_generate_traces(
-        seeds.data(), static_cast<int>(n), spec.job_count, spec.lambda_s, spec.max_duration_s, kind,
-        spec.duration_dist.sigma, spec.duration_dist.fixed_s, spec.duration_dist.lo_s,
-        spec.duration_dist.hi_s, 0, a.data(), d.data(), sp.data(), mem.data()));
+  if (n) {
+    Device& dev = Device::get();
+    std::lock_guard<std::mutex> lock(dev.mu());
+    Device::check(miso_b200_generate_traces_device_host(
+        dev.ctx(), seeds.data(), static_cast<int>(n), spec.job_count, spec.lambda_s,
+        spec.max_duration_s, kind, spec.duration_dist.sigma, spec.duration_dist.fixed_s,
+        spec.duration_dist.lo_s, spec.duration_dist.hi_s, a.data(), d.data(), sp.data(),
+        mem.data()));
+  }
   std::vector<JobTrace> out(n);
   for (size_t r = 0; r < n; ++r) {
     JobTrace& t = out[r];
@@ -55,6 +60,11 @@ inline std::vector<JobTrace> generate_traces(const TraceSpec& spec, const std::v
     }
   }
   return out;
+}
+
+// Drop-in for generate_trace (workload.hpp:97-114), on the device.
+inline JobTrace generate_trace(const TraceSpec& spec) {
+  return std::move(generate_traces(spec, {spec.seed}).front());
 }
 
 // Drop-in for run_experiment_in_memory (experiment.hpp:364-415). config.workers is ignored

@@ -902,6 +902,44 @@ int miso_b200_predict_host(miso_b200_ctx* ctx, const double* truth3, uint64_t nc
   return MISO_B200_OK;
 }
 
+int miso_b200_generate_traces_device_host(miso_b200_ctx* ctx, const uint64_t* seeds,
+                                          int n_traces, int job_count, double lambda_s,
+                                          double max_duration_s, int dist, double sigma,
+                                          double fixed_s, double lo_s, double hi_s,
+                                          double* arrival_s, double* duration_s, double* speeds5,
+                                          int* mem_gb) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (n_traces < 0) return fail(MISO_B200_E_INVALID, "n_traces < 0");
+  if (n_traces == 0 || job_count < 1)  // (the spec checks and their messages: the device call)
+    return miso_b200_generate_traces_device(ctx, seeds, n_traces, job_count, lambda_s,
+                                            max_duration_s, dist, sigma, fixed_s, lo_s, hi_s,
+                                            arrival_s, duration_s, speeds5, mem_gb, nullptr);
+  if (!seeds || !arrival_s || !duration_s || !speeds5 || !mem_gb) return fail(MISO_B200_E_INVALID, "null buffer");
+  DeviceGuard g(ctx->device);
+  if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
+  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  cudaStream_t s = ctx->streams[0];
+  const size_t J = size_t(n_traces) * size_t(job_count);
+  DevBuf d_seed, d_a, d_d, d_sp, d_m;
+  int rc;
+  if ((rc = upload(d_seed, seeds, size_t(n_traces), s))) return rc;
+  if ((rc = alloc_out(d_a, J * sizeof(double)))) return rc;
+  if ((rc = alloc_out(d_d, J * sizeof(double)))) return rc;
+  if ((rc = alloc_out(d_sp, J * 5 * sizeof(double)))) return rc;
+  if ((rc = alloc_out(d_m, J * sizeof(int)))) return rc;
+  rc = miso_b200_generate_traces_device(
+      ctx, static_cast<const uint64_t*>(d_seed.p), n_traces, job_count, lambda_s, max_duration_s,
+      dist, sigma, fixed_s, lo_s, hi_s, static_cast<double*>(d_a.p), static_cast<double*>(d_d.p),
+      static_cast<double*>(d_sp.p), static_cast<int*>(d_m.p), s);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(arrival_s, d_a.p, J * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(duration_s, d_d.p, J * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(speeds5, d_sp.p, J * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(mem_gb, d_m.p, J * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return MISO_B200_OK;
+}
+
 int miso_b200_host_alloc(size_t bytes, void** out) {
   if (!out) return fail(MISO_B200_E_INVALID, "null out pointer");
   CUDA_TRY(cudaMallocHost(out, std::max<size_t>(bytes, 1)));

@@ -27,11 +27,14 @@ def test_reference_optimizer_tests_against_b200():
 # (tools/dropin/prelude_sim.hpp): every test passes, multi-instance clone spawning included.
 # profiles_test.cpp runs the same way with predict_mig_speeds / extrapolate_small_slices routed
 # to the B200 predictor (tools/dropin/prelude_profiles.hpp).
-EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set(), "profiles": set()}
-TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9, "profiles": 19}
+# workload_test.cpp likewise with generate_trace on the device trace generator
+# (tools/dropin/prelude_workload.hpp).
+EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set(), "profiles": set(),
+                 "workload": set()}
+TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9, "profiles": 19, "workload": 8}
 
 
-@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance", "profiles"])
+@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance", "profiles", "workload"])
 def test_reference_sim_experiment_tests_against_b200(name):
     b = BIN.parent / f"{name}_test_b200"
     if not b.exists():
