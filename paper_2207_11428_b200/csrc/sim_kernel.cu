@@ -819,7 +819,6 @@ __device__ __forceinline__ void free_slot(Ctx& c, int gi, int i) {
 // on the lowest-numbered GPU having one, at that GPU's first free slot of the kind.
 __device__ bool admit_optsta(Ctx& c, int ji) {
   if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // nothing freed since
-  const DJob& j = c.jobs[ji];
   int bg = -1, bk = -1;
   for (int k = 4; k >= 0 && bg < 0; --k) {
     if (!(c.efftruth[size_t(k) * c.J + ji] > 0)) continue;  // == true_rate(j, k)
