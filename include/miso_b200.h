@@ -141,6 +141,12 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
  * thread at a time. */
 int miso_b200_decide_server(miso_b200_ctx* ctx, int idle_us);
 
+/* max_spare_slice_for (topology.hpp:227-252) over the context's catalog: the largest slice
+ * kind a partition could spare beside jobs pinned to at least min_kinds[0..n) (kind 0..4 =
+ * 1g..7g), -1 if none (std::nullopt). This reads the table the simulator uses on the device
+ * (the spare-slice LUT of placement, sim.hpp:581-607). */
+int miso_b200_max_spare_slice(miso_b200_ctx* ctx, const uint8_t* min_kinds, int n, int* kind);
+
 /* ---- cluster simulator (kernel (c)) ------------------------------------------------------ */
 
 /* Policies (sim.hpp:42). */

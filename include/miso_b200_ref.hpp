@@ -141,5 +141,21 @@ inline std::vector<std::optional<AssignmentVector>> optimize_partition_batch(
   return out;
 }
 
+// Drop-in for max_spare_slice_for (topology.hpp:227-252), answered from the spare-slice table
+// the simulator's placement reads on the device (miso_b200_max_spare_slice).
+inline std::optional<Slice> max_spare_slice_for(const PartitionCatalog& catalog,
+                                                std::vector<Slice> pinned_min_kinds) {
+  std::vector<uint8_t> kinds;
+  kinds.reserve(pinned_min_kinds.size());
+  for (Slice s : pinned_min_kinds) kinds.push_back(static_cast<uint8_t>(slice_index(s)));
+  Device& d = Device::get();
+  std::lock_guard<std::mutex> lock(d.mu());
+  d.use_catalog(catalog);
+  int kind = -1;
+  Device::check(miso_b200_max_spare_slice(d.ctx(), kinds.data(), static_cast<int>(kinds.size()), &kind));
+  if (kind < 0) return std::nullopt;
+  return kAllSlices[static_cast<size_t>(kind)];
+}
+
 }  // namespace b200
 }  // namespace miso

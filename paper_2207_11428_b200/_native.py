@@ -63,6 +63,7 @@ def _load():
     L.miso_b200_decide.argtypes = [vp, vp, vp, vp, i32, u64, u64, i32, C.c_double,
                                    C.POINTER(i32), vp, C.POINTER(C.c_double), vp]
     L.miso_b200_decide_server.argtypes = [vp, i32]
+    L.miso_b200_max_spare_slice.argtypes = [vp, vp, i32, C.POINTER(i32)]
     L.miso_b200_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
     L.miso_b200_host_free.argtypes = [vp]
     L.miso_b200_host_free.restype = None
@@ -313,6 +314,18 @@ def _decide_server(self, idle_us):
 
 
 Context.decide_server = _decide_server
+
+
+def _max_spare_slice(self, min_kinds):
+    """max_spare_slice_for (topology.hpp:227-252) over the context's catalog, from the table
+    the device simulator reads: kind 0..4 or None."""
+    k = np.ascontiguousarray(min_kinds, np.uint8)
+    out = C.c_int()
+    _check(lib.miso_b200_max_spare_slice(self._h, k.ctypes.data, len(k), C.byref(out)))
+    return None if out.value < 0 else out.value
+
+
+Context.max_spare_slice = _max_spare_slice
 
 
 def host_alloc(nbytes: int):

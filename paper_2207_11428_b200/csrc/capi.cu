@@ -47,7 +47,9 @@ struct miso_b200_ctx {
   std::chrono::steady_clock::time_point srv_last_ok{};
   // simulator
   int8_t* d_spare_lut = nullptr;  // max_spare_slice_for LUT of the active catalog
-  bool lut_valid = false;
+  bool lut_valid = false;          // device copy of the LUT matches the catalog
+  std::vector<int8_t> h_lut;       // host copy (built from the same catalog)
+  bool h_lut_valid = false;
   unsigned char* d_sim_ws = nullptr;
   size_t sim_ws_bytes = 0;
 };
@@ -138,6 +140,17 @@ void apply_catalog(miso_b200_ctx* ctx) {
     if (c < 64) ctx->en0 |= 1ull << c;
     else ctx->en1 |= 1ull << (c - 64);
   }
+}
+
+// max_spare_slice_for over the active catalog for every roster of <= 6 min kinds (the table
+// the simulator reads on the device; index = base-7 digits of the per-kind counts).
+const std::vector<int8_t>& host_lut(miso_b200_ctx* ctx) {
+  if (!ctx->h_lut_valid) {
+    ctx->h_lut.assign(16807, -1);
+    host_spare_lut(&ctx->counts[0][0], ctx->n_entries, ctx->h_lut.data());
+    ctx->h_lut_valid = true;
+  }
+  return ctx->h_lut;
 }
 
 int ensure_host_scratch(miso_b200_ctx* ctx, size_t rows, size_t inst) {
@@ -248,6 +261,7 @@ int miso_b200_set_catalog(miso_b200_ctx* ctx, const uint8_t* counts, int n) {
   std::memcpy(ctx->default_to_active, map, sizeof(map));
   apply_catalog(ctx);
   ctx->lut_valid = false;
+  ctx->h_lut_valid = false;
   return MISO_B200_OK;
 }
 
@@ -674,8 +688,7 @@ int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_se
     max_jobs = std::max(max_jobs, J);
   }
   if (!ctx->lut_valid) {
-    std::vector<int8_t> lut(16807);
-    host_spare_lut(&ctx->counts[0][0], ctx->n_entries, lut.data());
+    const std::vector<int8_t>& lut = host_lut(ctx);
     if (!ctx->d_spare_lut) CUDA_TRY(cudaMalloc(&ctx->d_spare_lut, lut.size()));
     CUDA_TRY(cudaMemcpy(ctx->d_spare_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
     ctx->lut_valid = true;
@@ -937,6 +950,20 @@ int miso_b200_generate_traces_device_host(miso_b200_ctx* ctx, const uint64_t* se
   CUDA_TRY(cudaMemcpyAsync(speeds5, d_sp.p, J * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaMemcpyAsync(mem_gb, d_m.p, J * sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
+  return MISO_B200_OK;
+}
+
+int miso_b200_max_spare_slice(miso_b200_ctx* ctx, const uint8_t* min_kinds, int n, int* kind) {
+  if (!ctx || !kind || (n > 0 && !min_kinds)) return fail(MISO_B200_E_INVALID, "null argument");
+  if (n < 0) return fail(MISO_B200_E_INVALID, "negative count");
+  *kind = -1;
+  if (n >= 7) return MISO_B200_OK;  // no entry has n + 1 > 7 slices (topology.hpp:229)
+  int cnt[5] = {0, 0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    if (min_kinds[i] > 4) return fail(MISO_B200_E_INVALID, "slice kind must be 0..4");
+    ++cnt[min_kinds[i]];
+  }
+  *kind = host_lut(ctx)[size_t((((cnt[0] * 7 + cnt[1]) * 7 + cnt[2]) * 7 + cnt[3]) * 7 + cnt[4])];
   return MISO_B200_OK;
 }
 

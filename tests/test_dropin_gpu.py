@@ -29,12 +29,16 @@ def test_reference_optimizer_tests_against_b200():
 # to the B200 predictor (tools/dropin/prelude_profiles.hpp).
 # workload_test.cpp likewise with generate_trace on the device trace generator
 # (tools/dropin/prelude_workload.hpp).
+# and topology_test.cpp with max_spare_slice_for answered from the device simulator's
+# spare-slice table (tools/dropin/prelude_topology.hpp).
 EXPECTED_FAIL = {"sim": set(), "experiment": set(), "acceptance": set(), "profiles": set(),
-                 "workload": set()}
-TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9, "profiles": 19, "workload": 8}
+                 "workload": set(), "topology": set()}
+TOTALS = {"sim": 19, "experiment": 12, "acceptance": 9, "profiles": 19, "workload": 8,
+          "topology": 14}
 
 
-@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance", "profiles", "workload"])
+@pytest.mark.parametrize("name", ["sim", "experiment", "acceptance", "profiles", "workload",
+                                  "topology"])
 def test_reference_sim_experiment_tests_against_b200(name):
     b = BIN.parent / f"{name}_test_b200"
     if not b.exists():

@@ -229,3 +229,14 @@ print("ok")
     env = dict(os.environ, MISO_B200_SIMPLE_SEARCH="1")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr
+
+
+def test_spare_slice_table_matches_oracle(ctx, oracle):
+    """miso_b200_max_spare_slice -- the spare-slice table the simulator's placement reads --
+    equals the oracle's max_spare_slice_for for every roster of up to 7 pinned kinds."""
+    import itertools
+    for n in range(8):
+        for kinds in itertools.combinations_with_replacement(range(5), n):
+            want = oracle.max_spare(list(kinds))
+            got = ctx.max_spare_slice(list(kinds))
+            assert (got if got is not None else -1) == want, (kinds, got, want)
