@@ -6,14 +6,21 @@ each, acceptance_test.cpp:72-85 distribution), full search over the 36-entry MIG
 every distinct job-to-slice assignment (111 candidates). One step = one pass of the partition-
 search kernel over the 1M-instance batch resident in HBM.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c1|c2|c3|c4|c5]
 
-N>1 runs under torchrun, one rank per GPU; every rank owns an independent 1M-instance shard
-(weak scaling, no data-path collective); timings are device-side (CUDA events) and the max over
-ranks is reported. `e2e` measures the same metric through the C-ABI host-pointer call
-(pinned host buffers; H2D, search, D2H inside the timed region). `cpu_baseline` times the
-reference's own optimize_partition (oracle/_ref, the unmodified reference headers) on a bounded
-sample with every host thread. `--impl reference` times only that reference CPU path.
+--gpus N > 1 without a torch.distributed environment re-executes this script under
+torch.distributed.run with N ranks (one per GPU over NCCL; gloo with ranks sharing GPUs when
+the box has fewer than N). Every rank owns an independent 1M-instance shard (weak scaling, no
+data-path collective); timings are device-side (CUDA events) and the max over ranks is reported;
+the decisions are gathered to rank 0 at the end (byte-exact, `result_gather`). `e2e` measures
+the same metric through the C-ABI host-pointer call (pinned host buffers; H2D, search, D2H
+inside the timed region). `cpu_baseline` times the reference's own optimize_partition
+(oracle/_ref, the unmodified reference headers) on a bounded sample of the same batch with every
+host thread (and with one), and its decisions on that sample are the `parity` check.
+
+The default line also carries `secondary`: configs 1, 3, 4 and 5 (BASELINE.json configs[0],
+[2], [3], [4]), each with its value, reference CPU baseline, parity check and bound.
+`--config cX` prints one of them alone.
 """
 from __future__ import annotations
 
@@ -37,6 +44,83 @@ WORKLOAD = ("config2: 1M random job mixes per GPU (m~U{1..7}, acceptance_test.cp
             "distribution), exhaustive search over 36 MIG partitions x distinct assignments "
             "(111 candidates), FP64 objective, reference tie-break")
 
+
+# ---------------------------------------------------------------------------------------------
+# ranks
+
+class Dist:
+    """One process per GPU (RANK / WORLD_SIZE / LOCAL_RANK from torch.distributed.run)."""
+
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.backend = os.environ.get("MISO_B200_DIST_BACKEND", "nccl")
+        self.pg = None
+
+    def init(self):
+        import torch
+        ndev = max(1, torch.cuda.device_count())
+        self.local %= ndev  # gloo fallback: ranks share the box's GPUs
+        self.shared_gpus = self.world > ndev
+        torch.cuda.set_device(self.local)
+        self.device = torch.device("cuda", self.local)
+        self.coll_dev = torch.device("cpu") if self.backend == "gloo" else self.device
+        if self.world > 1:
+            import torch.distributed as dist
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.device)
+            else:
+                dist.init_process_group(self.backend)
+            self.pg = dist
+        return self
+
+    def barrier(self):
+        if self.pg is not None:
+            self.pg.barrier()
+
+    def reduce(self, vals, op="max"):
+        """Element-wise max (or sum) over ranks of a list of floats."""
+        if self.pg is None:
+            return list(vals)
+        import torch
+        t = torch.tensor(list(vals), dtype=torch.float64, device=self.coll_dev)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX if op == "max" else self.pg.ReduceOp.SUM)
+        return t.tolist()
+
+    def gather(self, local, n_total):
+        from paper_2207_11428_b200.dist import gather_to_rank0
+        return gather_to_rank0(local, n_total, self.rank, self.world,
+                               device=self.coll_dev if self.world > 1 else None)
+
+    def close(self):
+        if self.pg is not None:
+            self.pg.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torch.distributed: re-execute under torch.distributed.run, N ranks on
+    127.0.0.1 (NCCL, one GPU each; gloo with ranks sharing GPUs if the box has fewer)."""
+    import socket
+    import subprocess
+    import torch
+    env = dict(os.environ)
+    ndev = torch.cuda.device_count()
+    if ndev < args.gpus:
+        env["MISO_B200_DIST_BACKEND"] = "gloo"
+    env.setdefault("NCCL_DEBUG", "INFO")           # rank/ring setup lines, on stderr
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+# ---------------------------------------------------------------------------------------------
+# helpers
 
 def gen_mixes(seed: int, n: int):
     """Synthetic config-2 input (same distribution as the reference generator; numpy stream)."""
@@ -66,23 +150,46 @@ def algorithmic_bytes(m: np.ndarray) -> int:
     return int(40 * int(m.sum()) + 13 * len(m) + 4)
 
 
-def measured_peak():
+def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
+        return json.loads(p.read_text())
+    return {}
+
+
+def measured_peak():
+    d = measured_peaks()
+    if "hbm_gbs" in d:
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of the search kernel from the committed ncu --set full capture."""
-    p = ROOT / "profiles" / "search_kernel_ncu.json"
+def ncu_capture(name):
+    p = ROOT / "profiles" / name
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get("dram_bytes_per_launch")
+        return json.loads(p.read_text())
     except Exception:
         return None
+
+
+def ncu_val(launch, key):
+    try:
+        return float(str(launch.get(key, "nan")).split()[0])
+    except (ValueError, AttributeError):
+        return float("nan")
+
+
+def oracle_lib():
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as ol
+    return ol
+
+
+def bits_equal(a, b) -> bool:
+    a, b = np.ascontiguousarray(a, np.float64), np.ascontiguousarray(b, np.float64)
+    return a.shape == b.shape and bool(np.array_equal(a.view(np.uint64), b.view(np.uint64)))
 
 
 class ClockSampler:
@@ -100,6 +207,7 @@ class ClockSampler:
         self.period = period_s
         self._stop = threading.Event()
         self._th = None
+        self._on = threading.Event()
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -111,20 +219,25 @@ class ClockSampler:
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and bit != 0x1:
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            if self._on.is_set():
+                try:
+                    self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit and bit != 0x1:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
             time.sleep(self.period)
 
     def start(self):
         if self.nv:
             self._th = threading.Thread(target=self._run, daemon=True)
             self._th.start()
+        return self
+
+    def timed(self, on: bool):  # sample only inside timed regions
+        (self._on.set if on else self._on.clear)()
 
     def stop(self):
         if self._th:
@@ -139,52 +252,220 @@ class ClockSampler:
         }
 
 
-def cpu_reference_rate(speeds, offs, m, target_s: float = 12.0):
-    """Reference optimize_partition (oracle/_ref) on every host thread over a bounded sample of
-    the same workload. Falls back to the C restatement (kind "port") if _ref is absent."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib
-    threads = oracle_lib.host_threads()
-    if oracle_lib.have_ref():
-        impl, kind = oracle_lib.Ref(), "reference"
-        run = lambda s, f: impl.optimize_batch(s, f, threads=threads)  # noqa: E731
+def cuda_time(stream, fn, reps=1):
+    """ms of `reps` calls of fn() between one CUDA-event pair on `stream`."""
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b)
+
+
+# ---------------------------------------------------------------------------------------------
+# config 2 (headline)
+
+def c2_cpu_baseline(speeds, offs, m, ctx, h_cand, h_obj, target_s: float = 8.0):
+    """The reference's optimize_partition (oracle/_ref) on a bounded sample of the same batch:
+    all host threads (the baseline) and one thread; its decisions on the sample are compared with
+    the GPU's (parity). Falls back to the C restatement (kind "port") without _ref."""
+    ol = oracle_lib()
+    threads = ol.host_threads()
+    if ol.have_ref():
+        impl, kind = ol.Ref(), "reference"
+        run = lambda s, f, t: impl.optimize_batch(s, f, threads=t)  # noqa: E731
     else:
-        impl, kind, threads = oracle_lib.Oracle(), "port", 1
-        run = lambda s, f: impl.optimize_batch(s, f)  # noqa: E731
+        impl, kind, threads = ol.Oracle(), "port", 1
+        run = lambda s, f, t: impl.optimize_batch(s, f)  # noqa: E731
 
     def sample(n):
         f = offs[: n + 1]
         return speeds[: int(f[-1]) * 5], f
 
     n = min(100_000, len(m))
-    t0 = time.perf_counter(); run(*sample(n)); dt = time.perf_counter() - t0
+    t0 = time.perf_counter(); run(*sample(n), threads); dt = time.perf_counter() - t0
     n = int(min(len(m), max(n, n * target_s / max(dt, 1e-6))))
     passes = 1
     if n == len(m):  # whole batch is quick: repeat passes to reach ~target_s of CPU work
-        t0 = time.perf_counter(); run(*sample(n)); dt1 = time.perf_counter() - t0
+        t0 = time.perf_counter(); run(*sample(n), threads); dt1 = time.perf_counter() - t0
         passes = max(1, min(100, int(target_s / max(dt1, 1e-6))))
     t0 = time.perf_counter()
     for _ in range(passes):
-        run(*sample(n))
+        e, p, o = run(*sample(n), threads)
     dt = time.perf_counter() - t0
-    return {"value": n * passes / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"first {n} instances of the rank-0 config-2 batch x {passes} passes, "
-                      f"{threads} host threads, {dt:.2f} s",
-            "candidates_per_s": candidates_of(m[:n]) * passes / dt}
+    # one thread: a sample of ~target_s / 2
+    n1 = max(1000, min(n, int(n * passes / dt * (target_s / 2) / max(threads, 1))))
+    t0 = time.perf_counter(); run(*sample(n1), 1); dt1 = time.perf_counter() - t0
+    # parity on the all-thread sample: entry, placement and objective bits
+    s_off = offs[: n + 1].astype(np.int64)
+    g_e, g_p = ctx.decode(h_cand[:n], s_off)
+    feas = np.repeat(e >= 0, np.diff(s_off))
+    ent_eq = bool(np.array_equal(g_e, e.astype(np.int32)))
+    pl_eq = bool(np.array_equal(g_p[feas], p[: int(s_off[-1])][feas]))
+    ob_eq = bits_equal(h_obj[:n], o)
+    cpu = {"value": n * passes / dt, "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"first {n} instances of the rank-0 config-2 batch x {passes} passes, "
+                     f"{threads} host threads, {dt:.2f} s",
+           "candidates_per_s": candidates_of(m[:n]) * passes / dt,
+           "one_thread": {"value": n1 / dt1, "unit": UNIT, "cores": 1,
+                          "sample": f"first {n1} instances, 1 thread, {dt1:.2f} s"}}
+    parity = {"checked_against": "oracle/_ref (the unmodified reference optimize_partition)"
+              if kind == "reference" else "oracle C restatement",
+              "instances": n, "entry_equal": ent_eq, "placement_equal": pl_eq,
+              "objective_bits_equal": ob_eq,
+              "mismatches": int((g_e != e.astype(np.int32)).sum() +
+                                (h_obj[:n].view(np.uint64) != o.view(np.uint64)).sum()),
+              "ok": ent_eq and pl_eq and ob_eq}
+    return cpu, parity
 
 
-def run_reference_arm(args, rank, world):
-    if rank != 0:
+def run_c2(args, D, ctx, clocks):
+    import ctypes as C
+    import torch
+    from paper_2207_11428_b200._native import host_alloc, host_free
+    import paper_2207_11428_b200 as miso
+
+    speeds, offs, m = gen_mixes(1000 + D.rank, N_PER_GPU)
+    n = len(m)
+    d_speeds = torch.from_numpy(speeds).cuda()
+    d_offs = torch.from_numpy(offs.view(np.int32)).cuda()
+    d_cand = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d_obj = torch.empty(n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    # Steps are independent batches: they alternate over S streams, each with its own copy of
+    # the input and its own outputs, so one step's ramp-up overlaps the previous step's tail.
+    # The single-stream rate (one launch per step on one stream) is reported beside it.
+    S = 2
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    bufs = [(d_speeds, d_offs, d_cand, d_obj)] + [
+        (d_speeds.clone(), d_offs.clone(), torch.empty_like(d_cand), torch.empty_like(d_obj))
+        for _ in range(S - 1)]
+    for _ in range(max(3, args.warmup)):
+        for k in range(S):
+            ctx.optimize_batch(*bufs[k], stream=streams[k].cuda_stream)
+    torch.cuda.synchronize()
+    K = args.steps
+
+    def timed(n_streams):
+        # K launches between ONE event pair on the launching stream(s): an event between
+        # launches would serialise them, so the per-step time is the timed region / K.
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        D.barrier(); torch.cuda.synchronize()
+        clocks.timed(True)
+        t0.record(stream)
+        for st in streams[:n_streams]:
+            st.wait_stream(stream)
+        for i in range(K):
+            k = i % n_streams
+            ctx.optimize_batch(*bufs[k], stream=streams[k].cuda_stream)
+        for st in streams[:n_streams]:
+            stream.wait_stream(st)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        clocks.timed(False)
+        D.barrier()
+        return t0.elapsed_time(t1)
+
+    single_ms = timed(1)
+    total_ms = timed(S)
+    kern_ms = total_ms / K
+    for k in range(1, S):  # every stream computed the same decisions
+        assert torch.equal(bufs[k][2], d_cand) and torch.equal(bufs[k][3].view(torch.int64), d_obj.view(torch.int64))
+
+    # --- e2e: the C-ABI host-pointer call, pinned buffers, H2D + search + D2H timed ---
+    nb_s, nb_o = speeds.nbytes, offs.nbytes
+    p_s, p_o, p_c, p_b = host_alloc(nb_s), host_alloc(nb_o), host_alloc(n), host_alloc(8 * n)
+    C.memmove(p_s, speeds.ctypes.data, nb_s)
+    C.memmove(p_o, offs.ctypes.data, nb_o)
+    lib = miso.lib
+    for _ in range(2):
+        lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
+    E = max(3, min(K, 20))
+    D.barrier(); torch.cuda.synchronize()
+    clocks.timed(True)
+    w0 = time.perf_counter()
+    for _ in range(E):
+        rc = lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
+        assert rc == 0, lib.miso_b200_last_error()
+    e2e_s = time.perf_counter() - w0
+    clocks.timed(False)
+    D.barrier()
+    h_c = np.ctypeslib.as_array((C.c_uint8 * n).from_address(p_c)).copy()
+    h_b = np.ctypeslib.as_array((C.c_double * n).from_address(p_b)).copy()
+    d_c = d_cand.cpu().numpy()
+    d_o = d_obj.cpu().numpy()
+    assert np.array_equal(h_c, d_c) and bits_equal(h_b, d_o)
+    for p in (p_s, p_o, p_c, p_b):
+        host_free(p)
+
+    total_ms, kern_ms, e2e_s, single_ms = D.reduce([total_ms, kern_ms, e2e_s, single_ms], "max")
+    gather = None
+    if D.world > 1:
+        # final result gather (untimed): every rank's decisions and objectives to rank 0 in
+        # global instance order (dist.gather_to_rank0: all_gather of equal shards, byte-exact)
+        g0 = time.perf_counter()
+        all_c = D.gather(d_c, D.world * n)
+        all_o = D.gather(d_o, D.world * n)
+        g_s = D.reduce([time.perf_counter() - g0], "max")[0]
+        if D.rank == 0:
+            byte_exact = bool(np.array_equal(all_c[:n], d_c) and bits_equal(all_o[:n], d_o))
+            gather = {"instances": int(len(all_c)), "bytes": int(all_c.nbytes + all_o.nbytes),
+                      "feasible": int((all_c < 111).sum()), "s": g_s, "backend": D.backend,
+                      "rank0_shard_byte_exact": byte_exact}
+    alg = algorithmic_bytes(m)
+    cands = candidates_of(m)
+    achieved = alg / (kern_ms / 1e3) / 1e9
+    single_achieved = alg / (single_ms / K / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    cap = ncu_capture("search_kernel_ncu.json") or {}
+    line = {
+        "metric": METRIC, "value": D.world * n * K / (total_ms / 1e3), "unit": UNIT,
+        "n_gpus": D.world, "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "instances_per_gpu": n, "jobs_per_gpu": int(m.sum()),
+                   "candidates_per_gpu_step": cands,
+                   "l2": "inputs %.0f MB per GPU > 126 MB L2; no flush" % ((speeds.nbytes + offs.nbytes) / 1e6),
+                   "parallelism": f"{D.world} independent shards ({D.backend}"
+                                  + (", ranks sharing GPUs" if D.shared_gpus else "") + ")",
+                   "streams": f"{S} streams per GPU, steps alternate (independent batches, per-stream input copies and outputs)"},
+        "configs_scored_per_s": D.world * cands * K / (total_ms / 1e3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": cap.get("dram_bytes_per_launch"),
+                     "kernel": "optimize_pipe_kernel", "kernel_ms": kern_ms,
+                     "kernel_ms_note": f"pipelined throughput: timed region / K, K launches alternating over {S} streams between one event pair (consecutive independent launches overlap); the single-launch figure is single_stream",
+                     "single_stream": {"kernel_ms": single_ms / K, "achieved": single_achieved,
+                                       "frac": single_achieved / peak,
+                                       "note": "one stream, launches back to back: per-launch duration"},
+                     "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+        "e2e": {"value": D.world * n * E / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": D.world * (nb_s + nb_o), "d2h_bytes_per_step": D.world * n * 9,
+                "api": "miso_b200_optimize_batch_host (pinned host buffers)", "steps": E},
+        "gpu_launches": K,
+    }
+    if gather is not None:
+        line["result_gather"] = gather
+    return line, (speeds, offs, m, d_c, d_o)
+
+
+# ---------------------------------------------------------------------------------------------
+# reference arm
+
+def run_reference_arm(args, D):
+    if D.rank != 0:
         return
     speeds, offs, m = gen_mixes(12345, N_PER_GPU)
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib
-    threads = oracle_lib.host_threads()
-    if oracle_lib.have_ref():
-        impl, kind = oracle_lib.Ref(), "reference"
+    ol = oracle_lib()
+    threads = ol.host_threads()
+    if ol.have_ref():
+        impl, kind = ol.Ref(), "reference"
         run = lambda s, f: impl.optimize_batch(s, f, threads=threads)  # noqa: E731
     else:
-        impl, kind, threads = oracle_lib.Oracle(), "port", 1
+        impl, kind, threads = ol.Oracle(), "port", 1
         run = lambda s, f: impl.optimize_batch(s, f)  # noqa: E731
     per_step = 250_000
     f = offs[: per_step + 1]
@@ -197,7 +478,7 @@ def run_reference_arm(args, rank, world):
     dt = time.perf_counter() - t0
     value = per_step * args.steps / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
@@ -211,84 +492,88 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def bench_c3(args):
-    """Config 3: batched noisy predictor on 16M synthetic MPS profiles (7-column groups,
-    nonce = group + 1, target_mae 0.017, default model). Secondary measurement (not the
-    headline line): profiles/s, roofline of the predictor kernel, reference CPU rate."""
+# ---------------------------------------------------------------------------------------------
+# secondary configs
+
+def sec_c3(args, D, ctx, n=16 * 1024 * 1024, steps=10):
+    """Config 3: batched noisy predictor on 16M synthetic MPS profiles per rank (7-column
+    groups, nonce = group + 1, target_mae 0.017, default model): profiles/s, the bound (the
+    FMA-heavy pipe: 3 IMADs per mt19937_64 seeding step), the reference's predictor chain on
+    all host threads over a sample, and that sample's outputs compared bit for bit."""
     import torch
-    import paper_2207_11428_b200 as miso
-    ctx = miso.Context(0)
-    n = 16 * 1024 * 1024
-    rng = np.random.default_rng(5)
+    rng = np.random.default_rng(5 + D.rank)
     f4 = rng.uniform(0.3, 1.0, n)
     f3 = f4 * rng.uniform(0.6, 1.0, n)
     truth = np.stack([np.ones(n), f4, f3], 1).reshape(-1)
     d_t = torch.from_numpy(truth).cuda()
     out = torch.empty(n * 5, dtype=torch.float64, device="cuda")
-    for _ in range(args.warmup):
+    st = torch.cuda.current_stream()
+    for _ in range(3):
         ctx.predict_batch(d_t, 7, 1, 42, 1, 0.017, out=out)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        ctx.predict_batch(d_t, 7, 1, 42, 1, 0.017, out=out)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / args.steps
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib
-    threads = oracle_lib.host_threads()
-    ref = oracle_lib.Ref() if oracle_lib.have_ref() and not args.no_cpu_baseline else None
-    cpu = None
-    if ref is not None:
-        k = 7 * 100_000
-        t0 = time.perf_counter()
-        ref.predict_batch(truth[: 3 * k], 7, 1, 42, 1, 0.017, threads=threads)
-        dt = time.perf_counter() - t0
-        cpu = {"value": k / dt, "unit": "profiles/s", "cores": threads, "kind": "reference",
-               "sample": f"{k} profiles, {threads} threads"}
-    peak, src = measured_peak()
+    D.barrier()
+    ms = cuda_time(st, lambda: ctx.predict_batch(d_t, 7, 1, 42, 1, 0.017, out=out), steps) / steps
+    ms = D.reduce([ms])[0]
+    res = {"metric": "MPS profiles predicted/sec (config 3, noisy, mae 0.017)",
+           "value": D.world * n / (ms / 1e3), "unit": "profiles/s", "ms_per_step": ms,
+           "steps": steps, "profiles_per_gpu": n, "n_gpus": D.world, "scaling": "weak",
+           "dtype": "f64", "data": "synthetic", "gpu_launches": steps}
+    peak, _ = measured_peak()
     gbs = n * 64 / (ms / 1e3) / 1e9
-    # the binding roof is the FMA-heavy pipe (every IMAD of the seeding chains): its busy
-    # fraction from the committed ncu capture of this kernel
-    compute = None
-    cap = ROOT / "profiles" / "predict_kernel_ncu.json"
-    if cap.exists():
-        l0 = json.loads(cap.read_text())["launches"][0]
-        pct = lambda k: float(str(l0.get(k, "nan")).split()[0]) / 100  # noqa: E731
-        compute = {"bound": "FMA-heavy pipe (IMAD: 3 integer multiplies per mt19937_64 seeding step, 158 steps x 2 entries per profile)",
-                   "ncu_pipe_busy": pct("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
-                   "ncu_issue_active": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-                   "source": "profiles/predict_kernel_ncu.json (ncu --set full of this kernel, 16M profiles)"}
-    print(json.dumps({"metric": "MPS profiles predicted/sec (config 3, noisy, mae 0.017)",
-                      "value": n / (ms / 1e3), "unit": "profiles/s", "ms_per_step": ms,
-                      "steps": args.steps, "warmup": args.warmup, "n_profiles": n,
-                      "dtype": "f64", "data": "synthetic",
-                      "roofline": {"bound": "int-issue (mt19937_64 seeding); hbm shown for scale",
-                                   "achieved_gbs": gbs, "peak_gbs": peak, "frac_hbm": gbs / peak,
-                                   "algorithmic_bytes_per_profile": 64},
-                      "compute_roofline": compute,
-                      "cpu_baseline": cpu}), flush=True)
+    cap = ncu_capture("predict_kernel_ncu.json")
+    bound = {"bound": "fma-heavy pipe (integer multiplies of the mt19937_64 seeding chains, 158 steps x 2 entries per profile)",
+             "hbm_for_scale": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                               "algorithmic_bytes_per_profile": 64}}
+    if cap:
+        l0 = cap["launches"][0]
+        cap_ms = ncu_val(l0, "gpu__time_duration.sum")
+        busy = ncu_val(l0, "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed") / 100
+        # the pipe's busy cycles per launch are fixed by the instruction mix (captured once for
+        # this n); scaled to this run's kernel duration they give its live busy fraction
+        bound.update({"achieved_pipe_busy_frac": busy * cap_ms / ms if ms > 0 else None,
+                      "frac": busy * cap_ms / ms if ms > 0 else None,
+                      "ncu_capture": {"pipe_busy": busy, "ms": cap_ms,
+                                      "issue_active": ncu_val(l0, "smsp__issue_active.avg.pct_of_peak_sustained_active") / 100,
+                                      "source": "profiles/predict_kernel_ncu.json"}})
+    res["roofline"] = bound
+    if D.rank == 0 and not args.no_cpu_baseline:
+        ol = oracle_lib()
+        if ol.have_ref():
+            ref, threads = ol.Ref(), ol.host_threads()
+            k = 7 * 60_000
+            t0 = time.perf_counter()
+            want = ref.predict_batch(truth[: 3 * k], 7, 1, 42, 1, 0.017, threads=threads)
+            dt = time.perf_counter() - t0
+            k1 = 7 * 4000
+            t0 = time.perf_counter()
+            ref.predict_batch(truth[: 3 * k1], 7, 1, 42, 1, 0.017, threads=1)
+            dt1 = time.perf_counter() - t0
+            got = out[: 5 * k].cpu().numpy()
+            res["cpu_baseline"] = {"value": k / dt, "unit": "profiles/s", "cores": threads,
+                                   "kind": "reference",
+                                   "sample": f"first {k} profiles of the rank-0 batch, {threads} threads",
+                                   "one_thread": {"value": k1 / dt1, "unit": "profiles/s", "cores": 1}}
+            res["parity"] = {"checked_against": "oracle/_ref predict_mig_speeds + extrapolate_small_slices",
+                             "profiles": k, "bits_equal": bits_equal(got, want),
+                             "mismatches": int((got.view(np.uint64) != want.view(np.uint64)).sum()),
+                             "ok": bits_equal(got, want)}
+    return res
 
 
-def bench_c1(args):
+def sec_c1(args, ctx):
     """Config 1 (BASELINE.json configs[0], the reference CPU example): one A100 with 3
     co-located jobs (generate_trace seed 7), noisy predictor (target MAE 0.017, rng_seed 7) ->
     default small-slice model -> effective_speed -> optimize_partition, through the C-ABI
-    host-pointer call miso_b200_decide made from C++ (tools/c1_latency.cpp): the roster goes
-    into a mapped pinned mailbox that a resident server warp polls, the fused predict+search
-    runs, the result record comes back through mapped memory. Latency metric: microseconds
-    per decision, call nonces 1..K; also reported: non-consecutive nonces (no draw-ahead), one
-    kernel launch per call, and the same call through ctypes / the Python API. Beside it the
-    reference's own chain (oracle/_ref) on one host thread over the same nonces."""
+    host-pointer call miso_b200_decide made from C++ (tools/c1_latency.cpp). Latency metric:
+    microseconds per decision, call nonces 1..K; also: non-consecutive nonces, one launch per
+    call, the scalar optimize_partition drop-in (miso_b200_optimize), ctypes / Python. Beside
+    it the reference's own chain (oracle/_ref) on one host thread over the same nonces."""
+    import ctypes as C
+    import subprocess
     import paper_2207_11428_b200 as miso
-    ctx = miso.Context(0)
     tr = miso.generate_trace(7, 3)
     jobs = [(f"j{i}", (tr.speeds5[i, 4], tr.speeds5[i, 3], tr.speeds5[i, 2]), int(tr.mem_gb[i]), None)
             for i in range(3)]
     K = max(args.steps, 1000)
-    # the C-ABI call a C++ host makes (ctypes, preallocated host buffers)
-    import ctypes as C
     t3 = np.ascontiguousarray([list(j[1]) for j in jobs], np.float64)
     mem = np.ascontiguousarray([j[2] for j in jobs], np.uint8)
     qos = np.full(3, -1, np.int8)
@@ -296,7 +581,7 @@ def bench_c1(args):
     fn = miso.lib.miso_b200_decide
     args_c = (ctx._h, t3.ctypes.data, mem.ctypes.data, qos.ctypes.data, 3)
     tail = (1, 0.017, C.byref(e), place.ctypes.data, C.byref(objv), None)
-    for r in range(max(args.warmup, 10)):
+    for r in range(10):
         fn(*args_c, r + 1, 7, *tail)
     lat = []
     acc = 0.0
@@ -310,125 +595,180 @@ def bench_c1(args):
     py_lat = []
     for r in range(200):
         t0 = time.perf_counter()
-        res, _ = ctx.decide(jobs, nonce=r + 1, rng_seed=7)
+        ctx.decide(jobs, nonce=r + 1, rng_seed=7)
         py_lat.append(time.perf_counter() - t0)
     first, _ = ctx.decide(jobs, nonce=1, rng_seed=7)
-    # the C++ caller (the drop-in binding's host language): _lib/c1_latency, same chain and
-    # inputs, nonces 1..K (+ non-consecutive nonces and one launch per call)
-    import subprocess
     exe = ROOT / "paper_2207_11428_b200" / "_lib" / "c1_latency"
     cpp = json.loads(subprocess.run([str(exe), str(K)], check=True, capture_output=True,
                                     text=True).stdout)
-    lat_us = np.array(lat) * 1e6
-    line = {"metric": "config-1 decision latency (MPS profile -> predictor -> best MIG partition, 3 jobs)",
-            "value": cpp["consecutive_us"], "unit": "us/decision", "higher_is_better": False,
-            "p99_us": cpp["consecutive_p99_us"],
-            "nonconsecutive_nonce_us": cpp["nonconsecutive_us"],
-            "launch_per_call_us": cpp["launch_per_call_us"],
-            "python_ctypes_us": float(np.median(lat_us)),
-            "python_api_us": float(np.median(py_lat) * 1e6), "steps": K, "warmup": max(args.warmup, 10),
-            "dtype": "f64", "data": "synthetic (generate_trace seed 7, 3 jobs; nonce 1..K)",
-            "config": {"workload": "config1: single A100 model, 3 co-located jobs",
-                       "api": "miso_b200_decide called from C++ (tools/c1_latency.cpp; host pointers; resident server kernel polling a mapped pinned mailbox, draw-ahead for consecutive nonces, results through mapped pinned memory)"},
-            "anchor": {"partition": first.partition_name if first else None,
-                       "objective": first.objective if first else None},
-            # per call: the 320-byte request mailbox the server fetches, the 4 + 5m word record
-            "e2e": {"value": cpp["consecutive_us"], "unit": "us/decision",
-                    "h2d_bytes_per_step": 320, "d2h_bytes_per_step": 8 * (4 + 5 * 3)}}
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib
-    if oracle_lib.have_ref() and not args.no_cpu_baseline:
-        sec, ref_acc = oracle_lib.Ref().c1_time(K)
-        line["cpu_baseline"] = {"value": sec / K * 1e6, "unit": "us/decision", "cores": 1,
-                                "kind": "reference", "sample": f"{K} decisions, nonce 1..{K}, 1 thread"}
+    res = {"metric": "config-1 decision latency (MPS profile -> predictor -> best MIG partition, 3 jobs)",
+           "value": cpp["consecutive_us"], "unit": "us/decision", "higher_is_better": False,
+           "p99_us": cpp["consecutive_p99_us"],
+           "nonconsecutive_nonce_us": cpp["nonconsecutive_us"],
+           "launch_per_call_us": cpp["launch_per_call_us"],
+           "python_ctypes_us": float(np.median(np.array(lat) * 1e6)),
+           "python_api_us": float(np.median(py_lat) * 1e6), "steps": K,
+           "dtype": "f64", "data": "synthetic (generate_trace seed 7, 3 jobs; nonce 1..K)",
+           "config": {"workload": "config1: single A100 model, 3 co-located jobs",
+                      "api": "miso_b200_decide called from C++ (tools/c1_latency.cpp; host pointers; resident server kernel polling a mapped pinned mailbox, draw-ahead for consecutive nonces, results through mapped pinned memory)"},
+           "anchor": {"partition": first.partition_name if first else None,
+                      "objective": first.objective if first else None},
+           "roofline": {"bound": "latency (PCIe round trip of one request; see DESIGN.md 4(a))"},
+           "e2e": {"value": cpp["consecutive_us"], "unit": "us/decision",
+                   "h2d_bytes_per_step": 320, "d2h_bytes_per_step": 8 * (4 + 5 * 3)}}
+    if "optimize_us" in cpp:
+        res["optimize_partition_us"] = cpp["optimize_us"]
+    ol = oracle_lib()
+    if ol.have_ref() and not args.no_cpu_baseline:
+        sec, ref_acc = ol.Ref().c1_time(K)
+        res["cpu_baseline"] = {"value": sec / K * 1e6, "unit": "us/decision", "cores": 1,
+                               "kind": "reference", "sample": f"{K} decisions, nonce 1..{K}, 1 thread"}
         rbits = int(np.float64(ref_acc).view(np.uint64))
-        line["parity"] = {"objective_sum_bit_equal": bool(int(np.float64(acc).view(np.uint64)) == rbits
-                                                          and int(cpp["obj_sum_hex"], 16) == rbits)}
-    print(json.dumps(line), flush=True)
+        ok = bool(int(np.float64(acc).view(np.uint64)) == rbits and int(cpp["obj_sum_hex"], 16) == rbits)
+        res["parity"] = {"checked_against": "oracle/_ref config-1 chain", "decisions": K,
+                         "objective_sum_bit_equal": ok, "ok": ok}
+    return res
 
 
-def bench_c4(args):
-    """Config 4 (BASELINE.json configs[3]): 100 GPUs, 1000-job Poisson traces (lambda 10 s),
-    seeds 0..S-1, default overheads; per trial the reference's run_trial_unit policy set:
-    nopart, optsta with best_static_partition (every feasible catalog entry, ~17 candidate
-    simulations per trace) and its re-run with the chosen partition, and miso (noisy predictor
-    0.017, rng_seed = seed); JCT normalised by the same trial's nopart. Everything runs on the
-    device on three streams (one warp per simulation). Secondary
-    measurement: trials/s beside the reference's trial on every host thread."""
-    import torch
-    import paper_2207_11428_b200 as miso
-    from concurrent.futures import ThreadPoolExecutor
-    S = args.seeds
-    ctx_a, ctx_b, ctx_c = miso.Context(0), miso.Context(0), miso.Context(0)
-    # the seeds' traces, generated on the device (bit-identical to generate_trace) and kept there
-    traces = miso.generate_traces_device(ctx_a, np.arange(S, dtype=np.uint64), 1000, lambda_s=10.0)
-    # three independent simulation sets run concurrently: one Context (simulation workspace)
-    # and one stream each; nopart and miso (1024 warps each, under-filling the GPU) overlap
-    # the best-static search (~17k warps) and the optsta re-run that depends on it
-    s_a, s_b, s_c = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+class TrialRunner:
+    """run_trial_unit's work per seed (experiment.hpp:299-362) for a batch of device-resident
+    traces: nopart, the best-static search (every feasible catalog entry, one launch), the
+    optsta re-run with the chosen partition, and miso (noisy predictor, rng_seed = seed). Three
+    contexts (one simulation workspace each) on three streams: nopart and miso overlap the
+    static search and the optsta re-run that depends on it."""
 
-    def trial_batch():
-        # run_trial_unit's work per seed (experiment.hpp:299-362): nopart, the best-static
-        # search (every feasible catalog entry, one launch), optsta re-run with the chosen
-        # partition (full metrics), miso
-        p_nop = miso.simulate_batch(ctx_a, traces, miso.SimOptions(policy="nopart", cluster_size=100),
-                                    stream=s_a, defer=True)
-        p_mis = miso.simulate_batch(ctx_c, traces, miso.SimOptions(policy="miso", cluster_size=100,
-                                                                   predictor="noisy"),
-                                    stream=s_c, defer=True)
-        # MISO_C4_PRUNED_STATIC=1: the chosen-only pruned search instead (same entries; 1.45x
-        # faster alone, but here miso is the critical path and the full search overlaps it
-        # better: 374 vs 399 ms per 1024 trials, tools/c4_timeline.py)
-        st = miso.best_static_partition(ctx_b, traces, cluster_size=100, stream=s_b,
+    def __init__(self, device):
+        import torch
+        import paper_2207_11428_b200 as miso
+        self.miso = miso
+        self.ctx = [miso.Context(device) for _ in range(3)]
+        self.st = [torch.cuda.Stream() for _ in range(3)]
+
+    def __call__(self, traces):
+        miso = self.miso
+        (ca, cb, cc), (sa, sb, sc) = self.ctx, self.st
+        p_nop = miso.simulate_batch(ca, traces, miso.SimOptions(policy="nopart", cluster_size=100),
+                                    stream=sa, defer=True)
+        p_mis = miso.simulate_batch(cc, traces, miso.SimOptions(policy="miso", cluster_size=100,
+                                                                predictor="noisy"),
+                                    stream=sc, defer=True)
+        # MISO_C4_PRUNED_STATIC=1: the chosen-only pruned search instead (same entries)
+        st = miso.best_static_partition(cb, traces, cluster_size=100, stream=sb,
                                         chosen_only=os.environ.get("MISO_C4_PRUNED_STATIC") == "1")
-        sta = miso.simulate_batch(ctx_b, traces, miso.SimOptions(policy="optsta", cluster_size=100),
+        sta = miso.simulate_batch(cb, traces, miso.SimOptions(policy="optsta", cluster_size=100),
                                   static_partitions=[miso.DEFAULT_CATALOG[e] for e, _ in st],
-                                  stream=s_b)
+                                  stream=sb)
         return p_nop(), st, sta, p_mis()
 
-    for _ in range(max(1, args.warmup)):
-        trial_batch()
+    def close(self):
+        for c in self.ctx:
+            c.close()
+
+
+def ref_trials(seeds):
+    """The reference's run_trial_unit-equivalent (oracle/_ref ref_trial) on every host thread:
+    (trials/s, threads, per-seed (static entry, [nopart, optsta, miso] avg JCT))."""
+    from concurrent.futures import ThreadPoolExecutor
+    ol = oracle_lib()
+    ref, threads = ol.Ref(), ol.host_threads()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        outs = list(ex.map(lambda s: ref.trial(int(s)), seeds))
+    return len(seeds) / (time.perf_counter() - t0), threads, outs
+
+
+def trial_parity(outs, seeds_idx, nop, st, sta, mis):
+    got = np.stack([nop.metrics["avg_jct_s"][seeds_idx], sta.metrics["avg_jct_s"][seeds_idx],
+                    mis.metrics["avg_jct_s"][seeds_idx]], 1)
+    want = np.stack([o for _, o in outs])
+    jct_eq = bits_equal(got, want)
+    ent_eq = bool(all(e == st[i][0] for i, (e, _) in zip(seeds_idx, outs)))
+    return {"trials_compared": len(outs), "avg_jct_bit_equal": jct_eq,
+            "static_entry_equal": ent_eq, "ok": jct_eq and ent_eq}
+
+
+def sec_c4(args, D, runner, seeds_per_rank=1024, steps=3):
+    """Config 4 (BASELINE.json configs[3]): 100 GPUs, 1000-job Poisson traces (lambda 10 s),
+    default overheads, 1024 seeds per rank; per seed the reference's run_trial_unit policy set.
+    Trials/s, the bound (one warp's dependent event chain: per-event time against the issue
+    floor and against one CPU core), the reference's trials on every host thread, parity of
+    16 trials."""
+    import torch
+    miso = runner.miso
+    seeds = np.arange(D.rank * seeds_per_rank, (D.rank + 1) * seeds_per_rank, dtype=np.uint64)
+    traces = miso.generate_traces_device(runner.ctx[0], seeds, 1000, lambda_s=10.0)
+    runner(traces)
     times = []
-    for _ in range(args.steps):
+    for _ in range(steps):
+        D.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        nop, st, sta, mis = trial_batch()
+        nop, st, sta, mis = runner(traces)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    dt = statistics.median(times)
-    j_nop = nop.metrics["avg_jct_s"]
-    j_sta = sta.metrics["avg_jct_s"]
-    assert np.array_equal(j_sta.view(np.uint64), np.array([tab[e] for e, tab in st]).view(np.uint64))
-    j_mis = mis.metrics["avg_jct_s"]
-    ev = int(mis.metrics["events"].sum())
-    n_cand = miso.sim.static_candidates(traces)[0]  # candidate runs launched (stopped or not)
-    cpu = None
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib
-    check = None
-    if oracle_lib.have_ref() and not args.no_cpu_baseline:
-        ref = oracle_lib.Ref()
-        threads = oracle_lib.host_threads()
-        k = min(S, threads)
+    dt = D.reduce([statistics.median(times)])[0]
+    # the miso simulations alone (the critical path): one launch, CUDA events on its stream
+    ctx_m, s_m = runner.ctx[2], runner.st[2]
+    opts = miso.SimOptions(policy="miso", cluster_size=100, predictor="noisy")
+    ms_m = []
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(s_m)
+        r = miso.simulate_batch(ctx_m, traces, opts, stream=s_m, defer=True)
+        b.record(s_m)
+        r = r()
+        ms_m.append(a.elapsed_time(b))
+    ms_miso = D.reduce([min(ms_m)])[0]
+    ev = float(mis.metrics["events"].mean())
+    S = len(seeds)
+    us_ev = ms_miso * 1e3 / ev  # each warp walks its seed's events one after another
+    res = {"metric": "cluster-simulation trials/sec (config 4: nopart + optsta(best static) + miso, 100 GPUs x 1000 jobs)",
+           "value": D.world * S / dt, "unit": "trials/s", "s_per_step": dt, "seeds_per_gpu": S,
+           "n_gpus": D.world, "scaling": "weak", "steps": steps,
+           "simulations_per_step": int(S * 3 + len(miso.sim.static_candidates(traces)[0])),
+           "miso_events_per_seed": ev, "dtype": "f64",
+           "data": "synthetic (generate_trace seeds, generated on the device)",
+           "median_jct_norm": {"optsta": float(np.median(sta.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"])),
+                               "miso": float(np.median(mis.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"]))},
+           "gpu_launches_per_step": "4 simulate_kernel + host-side upload/readback"}
+    cap = ncu_capture("sim_kernel_ncu.json")
+    bound = {"bound": "latency (one warp walks one seed's sequential event chain)",
+             "miso_ms": ms_miso, "miso_us_per_event_per_warp": us_ev,
+             "miso_events_per_s": S * ev / (ms_miso / 1e3)}
+    if cap:
+        l0 = cap["launches"][0]
+        inst = ncu_val(l0, "smsp__inst_executed.sum")
+        cap_ev = cap.get("events_total") or 1024 * 7510
+        ipe = inst / cap_ev
+        clk = (measured_peaks().get("sm_clock_max_mhz") or 1965.0) * 1e6
+        floor = ipe / clk * 1e6  # a warp issues at most one instruction per cycle
+        bound.update({"warp_instructions_per_event": ipe,
+                      "issue_floor_us_per_event": floor,
+                      "frac": floor / us_ev,
+                      "frac_note": "issue floor / achieved: the fraction of cycles a simulation warp issues",
+                      "ncu_capture": {"issue_active": ncu_val(l0, "smsp__issue_active.avg.pct_of_peak_sustained_active") / 100,
+                                      "source": "profiles/sim_kernel_ncu.json"}})
+    res["roofline"] = bound
+    if D.rank == 0 and not args.no_cpu_baseline and oracle_lib().have_ref():
+        k = min(S, max(16, oracle_lib().host_threads()))
+        rate, threads, outs = ref_trials(seeds[:k])
+        # the reference's miso simulation of seed 0 on one core: its time per (live) event
+        t0h = traces[0:1].to_host()[0]
+        ref = oracle_lib().Ref()
         t0 = time.perf_counter()
-        with ThreadPoolExecutor(threads) as ex:
-            outs = list(ex.map(lambda s: ref.trial(s), range(k)))
-        cdt = time.perf_counter() - t0
-        cpu = {"value": k / cdt, "unit": "trials/s", "cores": threads, "kind": "reference",
-               "sample": f"{k} trials (nopart + best static search + optsta + miso), {threads} threads"}
-        got = np.stack([j_nop[:k], j_sta[:k], j_mis[:k]], 1)
-        want = np.stack([o for _, o in outs])
-        check = {"trials_compared": k, "avg_jct_bit_equal": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64))),
-                 "static_entry_equal": bool(all(e == st[i][0] for i, (e, _) in enumerate(outs)))}
-    print(json.dumps({"metric": "cluster-simulation trials/sec (config 4: nopart + optsta(best static) + miso, 100 GPUs x 1000 jobs)",
-                      "value": S / dt, "unit": "trials/s", "s_per_step": dt, "seeds": S,
-                      "simulations_per_step": int(S * 3 + len(n_cand)),
-                      "static_candidates_completed": int(sum(np.isfinite(t).sum() for _, t in st)),
-                      "miso_events_per_seed": ev / S, "steps": args.steps, "warmup": args.warmup,
-                      "dtype": "f64", "data": "synthetic (generate_trace seeds 0..S-1)",
-                      "median_jct_norm": {"optsta": float(np.median(j_sta / j_nop)),
-                                          "miso": float(np.median(j_mis / j_nop))},
-                      "parity": check, "cpu_baseline": cpu}), flush=True)
+        ref.simulate_trace(t0h.arrival_s, t0h.duration_s, t0h.speeds5, t0h.mem_gb, None,
+                           seed=int(seeds[0]), cluster_size=100, policy=3, noisy=True,
+                           target_mae=0.017, rng_seed=int(seeds[0]))
+        ref_s = time.perf_counter() - t0
+        ev0 = float(mis.metrics["events"][0])
+        res["cpu_baseline"] = {"value": rate, "unit": "trials/s", "cores": threads,
+                               "kind": "reference",
+                               "sample": f"{k} trials (nopart + best static search + optsta + miso), {threads} threads",
+                               "one_core_miso_us_per_event": ref_s * 1e6 / ev0}
+        bound["cpu_one_core_us_per_event"] = ref_s * 1e6 / ev0
+        res["parity"] = trial_parity(outs, np.arange(k), nop, st, sta, mis)
+    return res
 
 
 def gen_mixes_device(chunk: int, n: int, device):
@@ -453,119 +793,127 @@ def gen_mixes_device(chunk: int, n: int, device):
     return sp.reshape(-1), offs.to(torch.int32), m
 
 
-def bench_c5(args):
+def sec_c5(args, D, ctx, runner, steps=10):
     """Config 5 (BASELINE.json configs[4]): scaling sweep. A FIXED workload -- 64M config-2 job
     mixes (64 chunks of 1M, generated on the device per chunk) and 8192 trace seeds (config-4
-    trials: nopart + best static + miso) -- is sharded over the ranks (strong scaling: rank r
-    owns a contiguous block of chunks and of seeds; no data-path collective). Search: K launches
-    over the rank's shard, CUDA events, max over ranks. Trials: one pass over the rank's seeds
-    in batches of 1024, max over ranks. Per-seed JCTs are gathered to rank 0 (dist.py) and
-    summarised there."""
+    trials: nopart + best static + miso + optsta re-run) -- sharded over the ranks (strong
+    scaling: rank r owns a contiguous block of chunks and of seeds; no data-path collective).
+    Search: K launches over the rank's whole shard, CUDA events, max over ranks. Trials: the
+    rank's seeds all in flight at once (one launch per policy), max over ranks. Per-seed JCTs
+    are gathered to rank 0 (dist.py). Parity: a sample of the last chunk and the last 16 seeds
+    against the reference."""
     import torch
-    import paper_2207_11428_b200 as miso
-    from paper_2207_11428_b200.dist import gather_to_rank0, shard_range
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    backend = os.environ.get("MISO_B200_DIST_BACKEND", "nccl")
-    coll_dev = torch.device("cpu") if backend == "gloo" else dev
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
-    ctx = miso.Context(local)
+    from paper_2207_11428_b200.dist import shard_range
+    miso = runner.miso
+    dev = D.device
     chunks, per_chunk, S = args.c5_chunks, 1_000_000, args.c5_seeds
-    c_lo, c_hi = shard_range(chunks, rank, world)
+    c_lo, c_hi = shard_range(chunks, D.rank, D.world)
     parts = [gen_mixes_device(c, per_chunk, dev) for c in range(c_lo, c_hi)]
-    jobs = sum(int(p[1][-1]) for p in parts)
     sp = torch.cat([p[0] for p in parts]) if parts else torch.zeros(0, dtype=torch.float64, device=dev)
     offs = torch.zeros(len(parts) * per_chunk + 1, dtype=torch.int32, device=dev)
     base = 0
     for i, p in enumerate(parts):
         offs[i * per_chunk + 1:(i + 1) * per_chunk + 1] = p[1][1:] + base
         base += int(p[1][-1])
-    mm = torch.cat([p[2] for p in parts]).cpu().numpy() if parts else np.zeros(0, np.int32)
+    n = len(parts) * per_chunk
+    # the last chunk's first instances (for parity on the last rank)
+    last = None
+    if parts and c_hi == chunks:
+        k = 50_000
+        lo_row = int(offs[n - per_chunk])
+        o_loc = (offs[n - per_chunk: n - per_chunk + k + 1] - lo_row).cpu().numpy().astype(np.uint32)
+        last = (sp[lo_row * 5: (lo_row + int(o_loc[-1])) * 5].cpu().numpy(), o_loc)
     del parts
-    n = len(mm)
     cand = torch.empty(n, dtype=torch.uint8, device=dev)
     obj = torch.empty(n, dtype=torch.float64, device=dev)
-    for _ in range(max(3, args.warmup)):
-        ctx.optimize_batch(sp, offs, cand, obj)
-    K = args.steps
     st = torch.cuda.current_stream()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    a.record(st)
-    for _ in range(K):
+    for _ in range(3):
         ctx.optimize_batch(sp, offs, cand, obj)
-    b.record(st)
-    torch.cuda.synchronize()
-    search_ms = a.elapsed_time(b) / K
+    D.barrier()
+    search_ms = cuda_time(st, lambda: ctx.optimize_batch(sp, offs, cand, obj), steps) / steps
     feasible = int((cand < 111).sum().item())
-    del sp, offs
-    # ---- trials ----
-    s_lo, s_hi = shard_range(S, rank, world)
-    t0 = time.perf_counter()
-    host_traces = miso.generate_traces(range(s_lo, min(s_hi, s_lo + 1024)), 1000, lambda_s=10.0)
-    host_gen_s = (time.perf_counter() - t0) * (s_hi - s_lo) / max(1, len(host_traces))
+    par_search = None
+    cpu_search = 0.0
+    if last is not None and not args.no_cpu_baseline and oracle_lib().have_ref():
+        ol = oracle_lib()
+        k = len(last[1]) - 1
+        t0 = time.perf_counter()
+        e, p, o = ol.Ref().optimize_batch(last[0], last[1], threads=ol.host_threads())
+        cpu_search = k / (time.perf_counter() - t0)
+        g_e, g_p = ctx.decode(cand[n - per_chunk: n - per_chunk + k].cpu().numpy(), last[1])
+        ok = bool(np.array_equal(g_e, e.astype(np.int32)) and
+                  bits_equal(obj[n - per_chunk: n - per_chunk + k].cpu().numpy(), o))
+        par_search = {"instances": k, "chunk": chunks - 1, "ok": ok}
+    del sp, offs, cand, obj
+    torch.cuda.empty_cache()
+    # ---- trials: every seed of this rank's shard in one launch per policy ----
+    s_lo, s_hi = shard_range(S, D.rank, D.world)
+    seeds = np.arange(s_lo, s_hi, dtype=np.uint64)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    traces = miso.generate_traces_device(ctx, np.arange(s_lo, s_hi, dtype=np.uint64), 1000, lambda_s=10.0)
+    traces = miso.generate_traces_device(runner.ctx[0], seeds, 1000, lambda_s=10.0)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
-    chk = traces[0:len(host_traces)].to_host()  # the device generator equals the host one, bit for bit
-    assert all(np.array_equal(a.arrival_s, b.arrival_s) and np.array_equal(a.speeds5, b.speeds5)
-               for a, b in zip(chk, host_traces))
-    rows = np.zeros((s_hi - s_lo, 3))
-    if dist is not None:
-        dist.barrier()
+    runner(traces[: min(len(traces), 64)])  # warm the three contexts' workspaces
+    D.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for i0 in range(0, len(traces), 1024):
-        tb = traces[i0:i0 + 1024]
-        nop = miso.simulate_batch(ctx, tb, miso.SimOptions(policy="nopart", cluster_size=100))
-        stc = miso.best_static_partition(ctx, tb, cluster_size=100)
-        mis = miso.simulate_batch(ctx, tb, miso.SimOptions(policy="miso", cluster_size=100,
-                                                           predictor="noisy"))
-        rows[i0:i0 + len(tb), 0] = nop.metrics["avg_jct_s"]
-        rows[i0:i0 + len(tb), 1] = [tab[e] for e, tab in stc]
-        rows[i0:i0 + len(tb), 2] = mis.metrics["avg_jct_s"]
+    nop, stc, sta, mis = runner(traces)
     torch.cuda.synchronize()
     trial_s = time.perf_counter() - t0
-    t = torch.tensor([search_ms, trial_s, float(feasible)], dtype=torch.float64, device=coll_dev)
-    if dist is not None:
-        dist.all_reduce(t[:2], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[2:], op=dist.ReduceOp.SUM)
-    search_ms, trial_s, feasible = t.tolist()
-    allrows = gather_to_rank0(rows.reshape(-1), S * 3, rank, world, device=coll_dev if world > 1 else None)
-    if rank == 0:
-        r = allrows.reshape(S, 3)
-        print(json.dumps({
-            "metric": "config-5 scaling sweep: 64M job mixes + 8192 trial seeds, fixed total, sharded",
-            "value": chunks * per_chunk / (search_ms / 1e3), "unit": "instances/s",
-            "n_gpus": world, "steps": K, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "strong", "dtype": "f64",
-            "data": "synthetic (device Philox per 1M chunk; generate_trace seeds 0..S-1 generated on the device)",
-            "config": {"workload": "config5", "mixes": chunks * per_chunk, "seeds": S,
-                       "parallelism": f"{world} shards, no data-path collective"},
-            "search_ms_per_pass": search_ms, "feasible_instances": int(feasible),
-            "trials": {"value": S / trial_s, "unit": "trials/s", "s": trial_s,
-                       "device_trace_gen_s_rank0": gen_s,
-                       "host_trace_gen_s_rank0_all_threads": host_gen_s},
-            "median_jct_norm": {"optsta": float(np.median(r[:, 1] / r[:, 0])),
-                                "miso": float(np.median(r[:, 2] / r[:, 0]))},
-        }), flush=True)
-    ctx.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    rows = np.stack([nop.metrics["avg_jct_s"], sta.metrics["avg_jct_s"], mis.metrics["avg_jct_s"]], 1)
+    par_trials = None
+    cpu_trials = 0.0
+    if s_hi == S and not args.no_cpu_baseline and oracle_lib().have_ref():
+        k = min(16, len(seeds))
+        cpu_trials, _, outs = ref_trials(seeds[-k:])
+        par_trials = trial_parity(outs, np.arange(len(seeds) - k, len(seeds)), nop, stc, sta, mis)
+    search_ms, trial_s = D.reduce([search_ms, trial_s], "max")
+    feasible = int(D.reduce([float(feasible)], "sum")[0])
+    allrows = D.gather(rows.reshape(-1), S * 3)
+    # parity results live on the last rank: bring them to rank 0
+    flags = D.reduce([0.0 if par_search is None else (1.0 if par_search["ok"] else -1.0),
+                      0.0 if par_trials is None else (1.0 if par_trials["ok"] else -1.0),
+                      cpu_search, cpu_trials], "sum")
+    if D.rank != 0:
+        return None
+    r = allrows.reshape(S, 3)
+    peak, _ = measured_peak()
+    gbs = 173.07e6 * chunks / (search_ms / 1e3) / 1e9 / D.world  # per GPU
+    res = {
+        "metric": "config-5 scaling sweep: 64M job mixes + 8192 trial seeds, fixed total, sharded",
+        "value": chunks * per_chunk / (search_ms / 1e3), "unit": "instances/s",
+        "n_gpus": D.world, "steps": steps, "higher_is_better": True, "scaling": "strong",
+        "dtype": "f64",
+        "data": "synthetic (device Philox per 1M chunk; generate_trace seeds 0..S-1 generated on the device)",
+        "config": {"workload": "config5", "mixes": chunks * per_chunk, "seeds": S,
+                   "parallelism": f"{D.world} shards, no data-path collective"},
+        "search_ms_per_pass": search_ms, "feasible_instances": feasible,
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                     "frac": gbs / peak,
+                     "note": "per GPU; algorithmic bytes ~173.07 MB per 1M mixes (41m+13 B per mix, E[m]=4)"},
+        "trials": {"value": S / trial_s, "unit": "trials/s", "s": trial_s,
+                   "seeds_in_flight_per_gpu": s_hi - s_lo,
+                   "device_trace_gen_s_rank0": gen_s},
+        "median_jct_norm": {"optsta": float(np.median(r[:, 1] / r[:, 0])),
+                            "miso": float(np.median(r[:, 2] / r[:, 0]))},
+        "gpu_launches": steps,
+    }
+    if flags[0] != 0 or flags[1] != 0:
+        res["parity"] = {"search_sample_of_last_chunk_ok": None if flags[0] == 0 else bool(flags[0] > 0),
+                         "last_16_trials_ok": None if flags[1] == 0 else bool(flags[1] > 0),
+                         "checked_against": "oracle/_ref (optimize_partition on 50k mixes of the last chunk; run_trial_unit-equivalent trials of the last 16 seeds)",
+                         "ok": bool(flags[0] >= 0 and flags[1] >= 0)}
+        threads = oracle_lib().host_threads()
+        res["cpu_baseline"] = {"value": flags[2], "unit": "instances/s", "cores": threads,
+                               "kind": "reference",
+                               "sample": f"50k mixes of the last chunk, {threads} threads",
+                               "trials": {"value": flags[3], "unit": "trials/s", "cores": threads,
+                                          "sample": f"the last 16 seeds, {threads} threads"}}
+    return res
 
+
+# ---------------------------------------------------------------------------------------------
 
 def main():
     ap = argparse.ArgumentParser()
@@ -574,188 +922,62 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="headline (config 2) only; skip configs 1/3/4/5")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2",
-                    help="c2 = headline (config 2); c1 / c3 / c4 / c5 = secondary measurements")
+                    help="c2 = headline (config 2, + secondary); c1 / c3 / c4 / c5 alone")
     ap.add_argument("--c5-chunks", type=int, default=64, help="c5: 1M-mix chunks in total")
     ap.add_argument("--c5-seeds", type=int, default=8192, help="c5: trial seeds in total")
-    ap.add_argument("--seeds", type=int, default=1024, help="c4: trace seeds per launch")
+    ap.add_argument("--seeds", type=int, default=1024, help="c4: trace seeds per GPU")
     args = ap.parse_args()
-    if args.config == "c1":
-        bench_c1(args)
-        return
-    if args.config == "c3":
-        bench_c3(args)
-        return
-    if args.config == "c4":
-        bench_c4(args)
-        return
-    if args.config == "c5":
-        bench_c5(args)
-        return
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        sys.exit(spawn_ranks(args))
 
+    D = Dist()
     if args.impl == "reference":
-        run_reference_arm(args, rank, world)
+        # the reference's own CPU implementation: rank 0 alone (n_gpus as launched)
+        if "WORLD_SIZE" not in os.environ:
+            D.world = args.gpus
+        run_reference_arm(args, D)
         return
 
-    import torch
-    # one process per GPU; MISO_B200_DIST_BACKEND=gloo (with local % device_count) lets the
-    # multi-rank path be exercised on a single-GPU box
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    backend = os.environ.get("MISO_B200_DIST_BACKEND", "nccl")
-    coll_dev = torch.device("cpu") if backend == "gloo" else torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-
+    D.init()
     import paper_2207_11428_b200 as miso
-    from paper_2207_11428_b200._native import host_alloc, host_free
-    ctx = miso.Context(local)
-
-    speeds, offs, m = gen_mixes(1000 + rank, N_PER_GPU)
-    n = len(m)
-    d_speeds = torch.from_numpy(speeds).cuda()
-    d_offs = torch.from_numpy(offs.view(np.int32)).cuda()
-    d_cand = torch.empty(n, dtype=torch.uint8, device="cuda")
-    d_obj = torch.empty(n, dtype=torch.float64, device="cuda")
-    stream = torch.cuda.current_stream()
-
-    # Steps are independent batches: they alternate over S streams, each with its own copy of
-    # the input and its own outputs, so one step's ramp-up overlaps the previous step's tail
-    # (the copies keep any step from reading another's data out of L2). The single-stream
-    # rate (programmatic dependent launch between steps) is reported beside it.
-    S = 2
-    streams = [torch.cuda.Stream() for _ in range(S)]
-    bufs = [(d_speeds, d_offs, d_cand, d_obj)] + [
-        (d_speeds.clone(), d_offs.clone(), torch.empty_like(d_cand), torch.empty_like(d_obj))
-        for _ in range(S - 1)]
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    for _ in range(max(3, args.warmup)):
-        for k in range(S):
-            ctx.optimize_batch(*bufs[k], stream=streams[k].cuda_stream)
-    torch.cuda.synchronize()
-
-    K = args.steps
-
-    def timed(n_streams):
-        # K launches between ONE event pair on the launching stream(s): an event between
-        # launches would serialise them, so the per-step time is the timed region / K.
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        barrier(); torch.cuda.synchronize()
-        t0.record(stream)
-        for st in streams[:n_streams]:
-            st.wait_stream(stream)
-        for i in range(K):
-            k = i % n_streams
-            ctx.optimize_batch(*bufs[k], stream=streams[k].cuda_stream)
-        for st in streams[:n_streams]:
-            stream.wait_stream(st)
-        t1.record(stream)
-        torch.cuda.synchronize(); barrier()
-        return t0.elapsed_time(t1)
-
-    single_ms = timed(1)
-    total_ms = timed(S)
-    kern_ms = total_ms / K
-    for k in range(1, S):  # every stream computed the same decisions
-        assert torch.equal(bufs[k][2], d_cand) and torch.equal(bufs[k][3].view(torch.int64), d_obj.view(torch.int64))
-
-    # --- e2e: the C-ABI host-pointer call, pinned buffers, H2D + search + D2H timed ---
-    import ctypes as C
-    nb_s, nb_o = speeds.nbytes, offs.nbytes
-    p_s, p_o, p_c, p_b = host_alloc(nb_s), host_alloc(nb_o), host_alloc(n), host_alloc(8 * n)
-    C.memmove(p_s, speeds.ctypes.data, nb_s)
-    C.memmove(p_o, offs.ctypes.data, nb_o)
-    lib = miso.lib
-    for _ in range(2):
-        lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
-    E = max(3, min(K, 20))
-    barrier(); torch.cuda.synchronize()
-    w0 = time.perf_counter()
-    for _ in range(E):
-        rc = lib.miso_b200_optimize_batch_host(ctx._h, p_s, p_o, n, p_c, p_b)
-        assert rc == 0, lib.miso_b200_last_error()
-    e2e_s = time.perf_counter() - w0
-    barrier()
-    clk = clocks.stop()
-    h_c = np.ctypeslib.as_array((C.c_uint8 * n).from_address(p_c)).copy()
-    h_b = np.ctypeslib.as_array((C.c_double * n).from_address(p_b)).copy()
-    d_c = d_cand.cpu().numpy()
-    assert np.array_equal(h_c, d_c) and np.array_equal(h_b.view(np.uint64), d_obj.cpu().numpy().view(np.uint64))
-    for p in (p_s, p_o, p_c, p_b):
-        host_free(p)
-
-    # max over ranks
-    t = torch.tensor([total_ms, kern_ms, e2e_s, single_ms], dtype=torch.float64, device=coll_dev)
-    gather = None
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        # final result gather (untimed): every rank's decisions and objectives to rank 0 in
-        # global instance order (dist.gather_to_rank0: all_gather of equal shards, byte-exact)
-        from paper_2207_11428_b200.dist import gather_to_rank0
-        g0 = time.perf_counter()
-        all_c = gather_to_rank0(d_c, world * n, rank, world, device=coll_dev)
-        all_o = gather_to_rank0(d_obj.cpu().numpy(), world * n, rank, world, device=coll_dev)
-        g_s = time.perf_counter() - g0
-        if rank == 0:
-            assert np.array_equal(all_c[:n], d_c) and np.array_equal(all_o[:n].view(np.uint64), d_obj.cpu().numpy().view(np.uint64))
-            gather = {"instances": int(len(all_c)), "bytes": int(all_c.nbytes + all_o.nbytes),
-                      "feasible": int((all_c < 111).sum()), "s": g_s, "backend": backend}
-    total_ms, kern_ms, e2e_s, single_ms = t.tolist()
-
-    if rank == 0:
-        value = world * n * K / (total_ms / 1e3)
-        cands = candidates_of(m)
-        alg = algorithmic_bytes(m)
-        achieved = alg / (kern_ms / 1e3) / 1e9
-        peak, peak_src = measured_peak()
-        traffic = ncu_traffic()
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "instances_per_gpu": n, "jobs_per_gpu": int(m.sum()),
-                       "candidates_per_gpu_step": cands,
-                       "l2": "inputs %.0f MB per GPU > 126 MB L2; no flush" % ((speeds.nbytes + offs.nbytes) / 1e6),
-                       "parallelism": f"{world} independent shards",
-                       "streams": f"{S} streams per GPU, steps alternate (independent batches, per-stream input copies and outputs)"},
-            "configs_scored_per_s": world * cands * K / (total_ms / 1e3),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "optimize_pipe_kernel", "kernel_ms": kern_ms,
-                         "kernel_ms_note": f"timed region / K: K launches alternating over {S} streams between one event pair (steady state; the kernel is 100% of the step)",
-                         "single_stream": {"kernel_ms": single_ms / K,
-                                           "achieved": alg / (single_ms / K / 1e3) / 1e9,
-                                           "frac": alg / (single_ms / K / 1e3) / 1e9 / peak},
-                         "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
-            "e2e": {"value": world * n * E / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": world * (nb_s + nb_o), "d2h_bytes_per_step": world * n * 9,
-                    "api": "miso_b200_optimize_batch_host (pinned host buffers)", "steps": E},
-            "clocks": clk,
-            "gpu_launches": K,
-        }
-        if gather is not None:
-            line["result_gather"] = gather
-        if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_reference_rate(speeds, offs, m)
-        print(json.dumps(line), flush=True)
+    ctx = miso.Context(D.local)
+    out = None
+    if args.config == "c1":
+        out = sec_c1(args, ctx) if D.rank == 0 else None
+    elif args.config == "c3":
+        out = sec_c3(args, D, ctx, steps=args.steps)
+    elif args.config in ("c4", "c5"):
+        runner = TrialRunner(D.local)
+        out = sec_c4(args, D, runner, args.seeds, steps=max(1, args.steps)) if args.config == "c4" \
+            else sec_c5(args, D, ctx, runner, steps=args.steps)
+        runner.close()
+    else:
+        clocks = ClockSampler(D.local).start()
+        line, (speeds, offs, m, h_cand, h_obj) = run_c2(args, D, ctx, clocks)
+        if D.rank == 0 and not args.no_cpu_baseline:
+            line["cpu_baseline"], line["parity"] = c2_cpu_baseline(speeds, offs, m, ctx, h_cand, h_obj)
+        if not args.no_secondary:
+            sec = {}
+            if D.rank == 0:
+                sec["c1"] = sec_c1(args, ctx)
+            clocks.timed(True)
+            sec["c3"] = sec_c3(args, D, ctx)
+            runner = TrialRunner(D.local)
+            sec["c4"] = sec_c4(args, D, runner, args.seeds)
+            clocks.timed(False)
+            sec["c5"] = sec_c5(args, D, ctx, runner)
+            runner.close()
+            line["secondary"] = sec
+        line["clocks"] = clocks.stop()
+        out = line if D.rank == 0 else None
+    if out is not None and D.rank == 0:
+        print(json.dumps(out), flush=True)
     ctx.close()
-    if dist is not None:
-        dist.destroy_process_group()
+    D.close()
 
 
 if __name__ == "__main__":

@@ -159,8 +159,29 @@ int miso_b200_max_spare_slice(miso_b200_ctx* ctx, const uint8_t* min_kinds, int 
 #define MISO_B200_SIM_INVARIANT 1         /* work conservation / accounting / plan mismatch */
 #define MISO_B200_SIM_NO_PARTITION 2      /* "no feasible partition for admitted roster" */
 #define MISO_B200_SIM_INFEASIBLE_SLICE 3  /* "placed on infeasible slice" */
-#define MISO_B200_SIM_EVENT_BUDGET 4      /* max_events exceeded (counts live events) */
+#define MISO_B200_SIM_EVENT_BUDGET 4      /* "event budget exhausted" (sim.hpp:224): the events
+                                             pushed (= popped by the reference, stale ones
+                                             included) exceed max_events */
 #define MISO_B200_SIM_PRUNED 5            /* stopped by miso_b200_simulate_batch_pruned's bound */
+#define MISO_B200_SIM_BAD_INPUT 6         /* the reference's std::invalid_argument for this
+                                             task's trace or options; metrics.detail says which:
+                                             MISO_B200_BAD_* | (job index << 8) */
+
+/* metrics.detail codes of MISO_B200_SIM_BAD_INPUT. Per trace job, in the reference's order
+ * (validate_profile, profiles.hpp:67-87; init_jobs, sim.hpp:246-254): */
+#define MISO_B200_BAD_BASE 1              /* "base duration must be positive" */
+#define MISO_B200_BAD_MEM 2               /* "memory demand must be in (0, 40] GB" */
+#define MISO_B200_BAD_SPEED_RANGE 3       /* + kind 0..4: "speed on <kind> outside (0,1]" */
+#define MISO_B200_BAD_SPEED_7G 8          /* "speed on 7g must be exactly 1" */
+#define MISO_B200_BAD_MONOTONE 9          /* "speed table not monotone in gpc count" */
+#define MISO_B200_BAD_INSTANCES 10        /* "instance count must be >= 1" */
+#define MISO_B200_BAD_FIRST_ARRIVAL 11    /* "first arrival must be at t=0" */
+#define MISO_B200_BAD_ARRIVAL_ORDER 12    /* "arrival times must be non-decreasing" */
+/* per task: */
+#define MISO_B200_BAD_NO_JOBS 13          /* "trace has no jobs" (sim.hpp:210) */
+#define MISO_B200_BAD_TASK_TRACE 14       /* task_trace entry outside [0, n_traces) */
+#define MISO_B200_BAD_STATIC 15           /* static partition is not a feasible partition */
+#define MISO_B200_BAD_CAPACITY 16         /* trace jobs + clones exceed the call's max_jobs */
 
 /* SimOptions (sim.hpp:81-96) + OverheadSpec (:62-67) + PredictorSpec (profiles.hpp:173-178).
  * Durations in seconds are converted with us_from_s = llround(s * 1e6) (sim.hpp:136). */
@@ -176,11 +197,16 @@ typedef struct {
   int check_invariants;            /* default 1 */
   double reprofile_drift_threshold;/* default 0 (off) */
   uint64_t max_events;             /* default 100000000 */
+  /* SimOptions::small_slice_model (sim.hpp:88, 894-896): fitted != 0 uses w2/w1 (weights over
+   * (f7, f4, f3, 1), LinearMap profiles.hpp:259-273); 0 uses the shared default model. */
+  int small_slice_model_fitted;
+  double small_slice_w2[4], small_slice_w1[4];
 } miso_b200_sim_options;
 
 /* MetricsReport (sim.hpp:106-122) scalars, per seed. */
 typedef struct {
-  int status, completed, job_count, completed_count, repartitions, migrations, mps_sessions, pad;
+  int status, completed, job_count, completed_count, repartitions, migrations, mps_sessions;
+  int detail;  /* MISO_B200_SIM_BAD_INPUT: MISO_B200_BAD_* | (job index << 8); else 0 */
   double avg_jct_s, makespan_s, stp_time_avg, jct_sum_s;
   double queue_frac, mps_frac, checkpoint_frac, run_frac, idle_frac;
   int64_t events, log_records, stp_points;
@@ -248,24 +274,31 @@ int miso_b200_generate_traces_device_host(miso_b200_ctx* ctx, const uint64_t* se
                                           int* mem_gb);
 
 /* run_simulation (sim.hpp:976-979) for n_seeds independent tasks at once, one warp per task,
- * DEVICE pointers. Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r owns
- * jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in
- * TraceJob, converted with us_from_s on the device; must be non-decreasing with the first at 0,
- * sim.hpp:251-254; base duration s; truth speeds; memory GB; QoS kind or -1). rng_seed[s] seeds the noisy predictor (experiment.hpp:305 sets it to the trace
- * seed). Policy optsta needs static_counts (5 per task: the static partition's per-kind counts,
- * a feasible partition; SimOptions::static_partition, sim.hpp:86) -- one launch can evaluate
- * every candidate of best_static_partition (sim.hpp:1031-1066) for many traces.
- * Outputs: metrics[s]; optional job_jct_us (completion - arrival, -1 if unfinished; only with
- * task_trace == NULL), event log (log_cap records per task) and STP series (stp_cap (t, stp)
- * pairs per task). */
+ * DEVICE pointers, stream-ordered (no host synchronisation; the library reads no device array
+ * back). Task s simulates trace task_trace[s] (task_trace NULL: trace s); trace r (< n_traces)
+ * owns jobs job_offsets[r]..job_offsets[r+1]-1 (arrival_s as in TraceJob, converted with
+ * us_from_s on the device; must be non-decreasing with the first at 0, sim.hpp:251-254; base
+ * duration s; truth speeds; memory GB; QoS kind or -1). max_jobs: an upper bound on any task's
+ * job count including multi-instance clones (it sizes the per-task workspace). rng_seed[s]
+ * seeds the noisy predictor (experiment.hpp:305 sets it to the trace seed). Policy optsta needs
+ * static_counts (5 per task: the static partition's per-kind counts, a feasible partition;
+ * SimOptions::static_partition, sim.hpp:86) -- one launch can evaluate every candidate of
+ * best_static_partition (sim.hpp:1031-1066) for many traces. Invalid inputs (the reference's
+ * std::invalid_argument: validate_profile, init_jobs) are reported per task as
+ * MISO_B200_SIM_BAD_INPUT with metrics.detail.
+ * Outputs: metrics[s]; optional job_jct_us (completion - arrival, -1 if unfinished; indexed by
+ * trace job, so only with task_trace == NULL, else -2), event log (log_cap records per task)
+ * and STP series (stp_cap (t, stp) pairs per task).
+ * Tasks on one context share its workspace: calls on different streams must use different
+ * contexts (or be ordered). */
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                             const int32_t* task_trace, const uint8_t* static_counts,
-                             const int32_t* job_offsets, const double* arrival_s,
-                             const double* base_s, const double* speeds5, const uint8_t* mem_gb,
-                             const int8_t* qos_kind, const uint64_t* rng_seed,
-                             miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
-                             miso_b200_log_record* log, int64_t log_cap, double* stp_series,
-                             int64_t stp_cap, void* stream);
+                             int n_traces, int max_jobs, const int32_t* task_trace,
+                             const uint8_t* static_counts, const int32_t* job_offsets,
+                             const double* arrival_s, const double* base_s, const double* speeds5,
+                             const uint8_t* mem_gb, const int8_t* qos_kind,
+                             const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                             int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
+                             double* stp_series, int64_t stp_cap, void* stream);
 
 /* miso_b200_simulate_batch with multi-instance jobs, flags and per-job outputs.
  * instances (optional, per trace job): JobProfile::instance_count (>= 1; NULL = all 1). A job
@@ -282,20 +315,19 @@ int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* op
  * the job's completion time in us (-1 if it never finished), its per-phase accumulated us
  * (queued, mps, checkpoint, running, idle), its parent job index (-1 for trace jobs) and clone
  * ordinal k: the inputs of MetricsReport::per_job (sim.hpp:916-929). Jobs are in SimEngine
- * order (trace jobs, then clones in spawn order); max_jobs = the largest per-trace sum of
- * instance counts of the batch. */
+ * order (trace jobs, then clones in spawn order). */
 #define MISO_B200_SIM_JCT_ONLY 1u
 #define MISO_B200_JOB_OUT_FIELDS 8
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                                const int32_t* task_trace, const uint8_t* static_counts,
-                                const int32_t* job_offsets, const double* arrival_s,
-                                const double* base_s, const double* speeds5,
-                                const uint8_t* mem_gb, const int8_t* qos_kind,
-                                const uint8_t* instances, const uint64_t* rng_seed,
-                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
-                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
-                                double* stp_series, int64_t stp_cap, unsigned flags,
-                                void* stream);
+                                int n_traces, int max_jobs, const int32_t* task_trace,
+                                const uint8_t* static_counts, const int32_t* job_offsets,
+                                const double* arrival_s, const double* base_s,
+                                const double* speeds5, const uint8_t* mem_gb,
+                                const int8_t* qos_kind, const uint8_t* instances,
+                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
+                                int64_t log_cap, double* stp_series, int64_t stp_cap,
+                                unsigned flags, void* stream);
 
 /* Chosen-only best-static search (run_trial_unit reads only best_static_partition(...).chosen,
  * experiment.hpp:337): optsta candidate runs as miso_b200_simulate_batch_ex (task_trace
@@ -307,9 +339,13 @@ int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options*
  * carry status MISO_B200_SIM_PRUNED and avg_jct_s = +inf. Its true avg_jct_s is strictly
  * greater than that completed candidate's, so the first minimum over the catalog (sim.hpp:1058)
  * is unchanged. Launch likely winners first (or in an earlier call with the same bound) so
- * the rest stop early. */
+ * the rest stop early. A stopped candidate is not run to its end: an invariant failure or an
+ * event-budget exhaustion it would meet later (where the reference's best_static_partition
+ * throws) goes unseen, so the chosen entry equals the reference's whenever the reference's
+ * search completes without throwing. */
 int miso_b200_simulate_batch_pruned(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
-                                    int n_tasks, const int32_t* task_trace,
+                                    int n_tasks, int n_traces, int max_jobs,
+                                    const int32_t* task_trace,
                                     const uint8_t* static_counts, const int32_t* job_offsets,
                                     const double* arrival_s, const double* base_s,
                                     const double* speeds5, const uint8_t* mem_gb,
@@ -333,6 +369,37 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
                                   const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
                                   int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
                                   double* stp_series, int64_t stp_cap, unsigned flags);
+
+/* ---- several devices (one context each) ------------------------------------------------ */
+
+/* Number of visible CUDA devices (0 if none). */
+int miso_b200_device_count(void);
+
+/* miso_b200_optimize_batch_host over n_ctx contexts (normally one per device): instances are
+ * split into n_ctx contiguous ranges, each context runs its range's H2D -> search -> D2H
+ * pipeline on its own host thread, and every decision lands at its instance's index in
+ * cand/obj -- the same bytes as one context's call (instances are
+ * independent). HOST pointers, synchronous. */
+int miso_b200_optimize_batch_sharded(miso_b200_ctx* const* ctxs, int n_ctx, const double* speeds,
+                                     const uint32_t* offsets, uint64_t n, uint8_t* cand,
+                                     double* obj);
+
+/* miso_b200_simulate_batch_host over n_ctx contexts: traces are split into n_ctx contiguous
+ * ranges of about equal task counts; each context uploads only its traces and runs their tasks
+ * (a trace's tasks stay on one device, so a pruned best-static search keeps its per-trace
+ * bound) on its own host thread; outputs land at each task's index with the layout of one
+ * miso_b200_simulate_batch_host call (job_out stride = the largest instance total of ALL
+ * traces). The results equal one context's call byte for byte. Same arguments and flags. */
+int miso_b200_simulate_batch_sharded(miso_b200_ctx* const* ctxs, int n_ctx,
+                                     const miso_b200_sim_options* opt, int n_tasks, int n_traces,
+                                     const int32_t* task_trace, const uint8_t* static_counts,
+                                     const int32_t* job_offsets, const double* arrival_s,
+                                     const double* base_s, const double* speeds5,
+                                     const uint8_t* mem_gb, const int8_t* qos_kind,
+                                     const uint8_t* instances, const uint64_t* rng_seed,
+                                     miso_b200_sim_metrics* metrics, int64_t* job_out,
+                                     miso_b200_log_record* log, int64_t log_cap,
+                                     double* stp_series, int64_t stp_cap, unsigned flags);
 
 /* Pinned host memory for the *_host paths. */
 int miso_b200_host_alloc(size_t bytes, void** out);

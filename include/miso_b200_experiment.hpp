@@ -7,6 +7,7 @@
 // Header-only; include after "miso/experiment.hpp".
 #pragma once
 
+#include <fstream>
 #include <map>
 #include <optional>
 #include <string>
@@ -144,6 +145,39 @@ inline ExperimentResult run_experiment_in_memory(const ExperimentConfig& config)
     }
   }
   return res;
+}
+
+// Drop-in for run_experiment (experiment.hpp:417-431): the trials on the device, then the
+// reference's own CSV and summary writers.
+inline ExperimentResult run_experiment(const ExperimentConfig& config) {
+  ExperimentResult res = b200::run_experiment_in_memory(config);
+  {
+    std::ofstream out(config.csv_path);
+    if (!out) throw IoError("cannot open csv output: " + config.csv_path);
+    write_csv(res, out);
+  }
+  {
+    std::ofstream out(config.json_path);
+    if (!out) throw IoError("cannot open json output: " + config.json_path);
+    out << summarize(res).dump(2) << '\n';
+    if (!out) throw IoError("json write failed");
+  }
+  return res;
+}
+
+// Drop-in for optsta_search (experiment.hpp:434-446): the offline static-partition search on
+// the experiment's trace (trial 0 seed), trace generation and every candidate on the device.
+inline StaticSearchResult optsta_search(const ExperimentConfig& config) {
+  validate_experiment_config(config);
+  JobTrace trace;
+  if (!config.trace_path.empty()) {
+    trace = load_trace(config.trace_path);
+  } else {
+    TraceSpec spec = config.trace_spec;
+    spec.seed = config.base_seed;
+    trace = b200::generate_trace(spec);
+  }
+  return b200::best_static_partition(trace, config.cluster_size, config.overheads);
 }
 
 }  // namespace b200

@@ -11,8 +11,11 @@
 // assignment is valid (:102), std::runtime_error for device failures.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <optional>
 #include <stdexcept>
@@ -25,24 +28,52 @@
 namespace miso {
 namespace b200 {
 
+// One context per CUDA device, created on first use and shared by every caller in the process
+// (a context serves one host thread at a time: callers hold mu()). Batch calls spread their
+// work over all() -- every visible device, or the first MISO_B200_DEVICES of them.
 class Device {
  public:
+  static constexpr int kMaxDevices = 64;
+
   static Device& get(int device = 0) {
-    static Device d(device);
-    return d;
+    if (device < 0 || device >= kMaxDevices) throw std::invalid_argument("miso_b200: device index");
+    static std::mutex reg_mu;
+    static std::unique_ptr<Device> reg[kMaxDevices];
+    std::lock_guard<std::mutex> lock(reg_mu);
+    if (!reg[device]) reg[device].reset(new Device(device));
+    return *reg[device];
   }
+
+  static int count() {
+    static const int n = [] {
+      int d = miso_b200_device_count();
+      if (const char* e = std::getenv("MISO_B200_DEVICES")) d = std::min(d, std::max(1, std::atoi(e)));
+      return std::max(1, std::min(d, kMaxDevices));
+    }();
+    return n;
+  }
+
+  static std::vector<Device*> all() {
+    std::vector<Device*> v;
+    for (int i = 0; i < count(); ++i) v.push_back(&get(i));
+    return v;
+  }
+
   miso_b200_ctx* ctx() { return ctx_; }
   std::mutex& mu() { return mu_; }
 
-  // Installs `catalog` on the context when it differs from the active one.
-  void use_catalog(const PartitionCatalog& catalog) {
+  // Installs `catalog` on the context when it differs from the active one. Returns false for
+  // an empty catalog (nothing installed: callers answer it as the reference does -- no entry).
+  bool use_catalog(const PartitionCatalog& catalog) {
+    if (catalog.entries.empty()) return false;
     std::vector<uint8_t> counts;
     counts.reserve(catalog.entries.size() * 5);
     for (const auto& e : catalog.entries)
       for (int k = 0; k < 5; ++k) counts.push_back(e.counts()[k]);
-    if (counts == active_) return;
+    if (counts == active_) return true;
     check(miso_b200_set_catalog(ctx_, counts.data(), static_cast<int>(catalog.entries.size())));
     active_ = std::move(counts);
+    return true;
   }
 
   static void check(int rc) {
@@ -50,12 +81,38 @@ class Device {
     if (rc < 0) throw std::runtime_error(std::string("miso_b200: ") + miso_b200_last_error());
   }
 
- private:
-  explicit Device(int device) { check(miso_b200_create(device, &ctx_)); }
   ~Device() { miso_b200_destroy(ctx_); }
+
+ private:
+  explicit Device(int device) {
+    check(miso_b200_create(device, &ctx_));
+    uint8_t c[36 * 5];  // the context's real active catalog
+    const int n = miso_b200_get_catalog(ctx_, c);
+    active_.assign(c, c + 5 * std::max(0, n));
+  }
   miso_b200_ctx* ctx_ = nullptr;
   std::vector<uint8_t> active_;
   std::mutex mu_;
+};
+
+// Holds every device's lock (in index order) for a call spread over Device::all(), with the
+// catalog installed on each. contexts() lists their contexts in the same order.
+class AllDevices {
+ public:
+  explicit AllDevices(const PartitionCatalog& catalog) : devs_(Device::all()) {
+    for (Device* d : devs_) locks_.emplace_back(d->mu());
+    for (Device* d : devs_) ok_ = d->use_catalog(catalog);
+    for (Device* d : devs_) ctxs_.push_back(d->ctx());
+  }
+  bool catalog_ok() const { return ok_; }
+  miso_b200_ctx* const* contexts() const { return ctxs_.data(); }
+  int size() const { return static_cast<int>(ctxs_.size()); }
+
+ private:
+  std::vector<Device*> devs_;
+  std::vector<std::unique_lock<std::mutex>> locks_;
+  std::vector<miso_b200_ctx*> ctxs_;
+  bool ok_ = true;
 };
 
 namespace detail {
@@ -94,7 +151,7 @@ inline std::optional<AssignmentVector> optimize_partition(const std::vector<JobS
     throw std::invalid_argument("optimize_partition needs 1..7 jobs, got " + std::to_string(m));
   Device& d = Device::get();
   std::lock_guard<std::mutex> lock(d.mu());
-  d.use_catalog(catalog);
+  if (!d.use_catalog(catalog)) return std::nullopt;  // no entry can host the jobs (:102)
   double speeds[35];
   for (size_t i = 0; i < m; ++i) std::memcpy(speeds + 5 * i, jobs[i].speeds.v.data(), 40);
   int entry = -1;
@@ -116,13 +173,22 @@ inline std::optional<AssignmentVector> optimize_partition(const std::vector<JobS
   return out;
 }
 
-// Many independent rosters in one launch (host buffers; H2D/search/D2H pipelined inside).
-// Rosters with m outside 1..7 throw std::invalid_argument like the scalar call.
+// Many independent rosters in one call (host buffers; H2D/search/D2H pipelined inside), spread
+// over every device (miso_b200_optimize_batch_sharded: contiguous instance ranges, one host
+// thread per device). Rosters with m outside 1..7 throw std::invalid_argument like the scalar
+// call.
 inline std::vector<std::optional<AssignmentVector>> optimize_partition_batch(
     const std::vector<std::vector<JobSpeeds>>& batch, const PartitionCatalog& catalog) {
-  Device& d = Device::get();
-  std::lock_guard<std::mutex> lock(d.mu());
-  d.use_catalog(catalog);
+  AllDevices all(catalog);
+  if (!all.catalog_ok()) {  // empty catalog: every roster is nullopt (or invalid_argument)
+    std::vector<std::optional<AssignmentVector>> out;
+    for (const auto& r : batch) {
+      if (r.empty() || r.size() > 7)
+        throw std::invalid_argument("optimize_partition needs 1..7 jobs, got " + std::to_string(r.size()));
+      out.push_back(std::nullopt);
+    }
+    return out;
+  }
   std::vector<uint32_t> offsets(batch.size() + 1, 0);
   for (size_t i = 0; i < batch.size(); ++i)
     offsets[i + 1] = offsets[i] + static_cast<uint32_t>(batch[i].size());
@@ -132,12 +198,13 @@ inline std::vector<std::optional<AssignmentVector>> optimize_partition_batch(
       std::memcpy(&speeds[(offsets[i] + j) * 5], batch[i][j].speeds.v.data(), 40);
   std::vector<uint8_t> cand(batch.size());
   std::vector<double> obj(batch.size());
-  Device::check(miso_b200_optimize_batch_host(d.ctx(), speeds.data(), offsets.data(), batch.size(),
-                                              cand.data(), obj.data()));
+  Device::check(miso_b200_optimize_batch_sharded(all.contexts(), all.size(), speeds.data(),
+                                                 offsets.data(), batch.size(), cand.data(),
+                                                 obj.data()));
   std::vector<std::optional<AssignmentVector>> out;
   out.reserve(batch.size());
   for (size_t i = 0; i < batch.size(); ++i)
-    out.push_back(detail::decode(d.ctx(), batch[i], catalog, cand[i], obj[i]));
+    out.push_back(detail::decode(all.contexts()[0], batch[i], catalog, cand[i], obj[i]));
   return out;
 }
 
@@ -150,7 +217,7 @@ inline std::optional<Slice> max_spare_slice_for(const PartitionCatalog& catalog,
   for (Slice s : pinned_min_kinds) kinds.push_back(static_cast<uint8_t>(slice_index(s)));
   Device& d = Device::get();
   std::lock_guard<std::mutex> lock(d.mu());
-  d.use_catalog(catalog);
+  if (!d.use_catalog(catalog)) return std::nullopt;  // no entry to spare a slice in
   int kind = -1;
   Device::check(miso_b200_max_spare_slice(d.ctx(), kinds.data(), static_cast<int>(kinds.size()), &kind));
   if (kind < 0) return std::nullopt;

@@ -18,8 +18,9 @@
 // for bad options/traces (validated with the reference's own validators, in its order),
 // SimInvariantError for engine failures, InfeasibleError from the static search.
 // Multi-instance jobs (JobProfile::instance_count > 1) spawn their clones on the device as in
-// SimEngine::spawn_instances. Not supported (std::invalid_argument): a caller-fitted small-slice
-// model (SimOptions::small_slice_model; the shared default model is used).
+// SimEngine::spawn_instances. A caller-fitted SimOptions::small_slice_model is used as the
+// reference uses it (sim.hpp:894-896). Batches are spread over every device
+// (miso_b200_simulate_batch_sharded; Device::all()).
 #pragma once
 
 #include <algorithm>
@@ -84,8 +85,6 @@ inline void validate(const JobTrace& trace, const SimOptions& opt) {
     if (t.profile.instance_count > 255)
       throw std::invalid_argument("miso_b200: instance_count above 255");
   }
-  if (opt.small_slice_model.fitted)
-    throw std::invalid_argument("miso_b200: the device engine uses the shared default small-slice model");
   if (opt.cluster_size > 32767) throw std::invalid_argument("miso_b200: cluster_size above 32767");
 }
 
@@ -105,11 +104,41 @@ inline miso_b200_sim_options to_c(const SimOptions& o) {
   c.check_invariants = o.check_invariants ? 1 : 0;
   c.reprofile_drift_threshold = o.reprofile_drift_threshold;
   c.max_events = o.max_events;
+  c.small_slice_model_fitted = o.small_slice_model.fitted ? 1 : 0;  // sim.hpp:894-896
+  for (int i = 0; i < 4; ++i) {
+    c.small_slice_w2[i] = o.small_slice_model.w_2g[static_cast<size_t>(i)];
+    c.small_slice_w1[i] = o.small_slice_model.w_1g[static_cast<size_t>(i)];
+  }
   return c;
 }
 
-[[noreturn]] inline void throw_status(int status) {
+// MISO_B200_SIM_BAD_INPUT's detail as the reference's std::invalid_argument text.
+inline std::string bad_input_message(const JobTrace* trace, int detail) {
+  const int code = detail & 0xFF, job = detail >> 8;
+  std::string id = trace && static_cast<size_t>(job) < trace->jobs.size()
+                       ? trace->jobs[static_cast<size_t>(job)].profile.job_id
+                       : "j" + std::to_string(job);
+  const std::string pre = "job '" + id + "': ";
+  static const char* kinds[5] = {"1g", "2g", "3g", "4g", "7g"};
+  if (code >= MISO_B200_BAD_SPEED_RANGE && code < MISO_B200_BAD_SPEED_RANGE + 5)
+    return pre + "speed on " + kinds[code - MISO_B200_BAD_SPEED_RANGE] + " outside (0,1]";
+  switch (code) {
+    case MISO_B200_BAD_BASE: return pre + "base duration must be positive";
+    case MISO_B200_BAD_MEM: return pre + "memory demand must be in (0, 40] GB";
+    case MISO_B200_BAD_SPEED_7G: return pre + "speed on 7g must be exactly 1";
+    case MISO_B200_BAD_MONOTONE: return pre + "speed table not monotone in gpc count";
+    case MISO_B200_BAD_INSTANCES: return pre + "instance count must be >= 1";
+    case MISO_B200_BAD_FIRST_ARRIVAL: return "first arrival must be at t=0";
+    case MISO_B200_BAD_ARRIVAL_ORDER: return "arrival times must be non-decreasing";
+    case MISO_B200_BAD_NO_JOBS: return "trace has no jobs";
+    case MISO_B200_BAD_STATIC: return "static partition is not a feasible partition";
+    default: return "miso_b200: invalid simulation input (detail " + std::to_string(detail) + ")";
+  }
+}
+
+[[noreturn]] inline void throw_status(int status, int detail = 0, const JobTrace* trace = nullptr) {
   switch (status) {
+    case MISO_B200_SIM_BAD_INPUT: throw std::invalid_argument(bad_input_message(trace, detail));
     case MISO_B200_SIM_EVENT_BUDGET: throw SimInvariantError("event budget exhausted");
     case MISO_B200_SIM_NO_PARTITION: throw SimInvariantError("no feasible partition for admitted roster");
     case MISO_B200_SIM_INFEASIBLE_SLICE: throw SimInvariantError("job placed on infeasible slice");
@@ -278,9 +307,9 @@ inline std::vector<MetricsReport> run_simulation_batch(
     max_jobs = std::max(max_jobs, cap);
   }
   const miso_b200_sim_options c = detail::to_c(options);
-  Device& d = Device::get();
-  std::lock_guard<std::mutex> lock(d.mu());
-  d.use_catalog(options.catalog);
+  AllDevices all(options.catalog);
+  if (!all.catalog_ok() && (options.policy == Policy::miso || options.policy == Policy::oracle))
+    throw SimInvariantError("no feasible partition for admitted roster on gpu 0");  // sim.hpp:728
   std::vector<miso_b200_sim_metrics> met(n);
   std::vector<int64_t> job_out(full ? n * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : 0);
   const bool want_log = full && options.event_log != nullptr;
@@ -291,8 +320,9 @@ inline std::vector<MetricsReport> run_simulation_batch(
   for (int attempt = 0; attempt < 2; ++attempt) {
     log.assign(want_log ? n * size_t(log_cap) : 0, miso_b200_log_record{});
     stp.assign(full ? n * 2 * size_t(stp_cap) : 0, 0.0);
-    Device::check(miso_b200_simulate_batch_host(
-        d.ctx(), &c, static_cast<int>(n), static_cast<int>(n), nullptr, optsta ? sc.data() : nullptr,
+    Device::check(miso_b200_simulate_batch_sharded(
+        all.contexts(), all.size(), &c, static_cast<int>(n), static_cast<int>(n), nullptr,
+        optsta ? sc.data() : nullptr,
         ta.offsets.data(), ta.arrival.data(), ta.base.data(), ta.speeds.data(), ta.mem.data(),
         ta.qos.data(), ta.inst.data(), seeds.data(), met.data(), full ? job_out.data() : nullptr,
         want_log ? log.data() : nullptr, log_cap, full ? stp.data() : nullptr, stp_cap,
@@ -308,7 +338,7 @@ inline std::vector<MetricsReport> run_simulation_batch(
   }
   out.reserve(n);
   for (size_t i = 0; i < n; ++i) {
-    if (met[i].status) detail::throw_status(met[i].status);
+    if (met[i].status) detail::throw_status(met[i].status, met[i].detail, traces[i]);
     const int64_t* jo = full ? job_out.data() + i * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : nullptr;
     std::vector<std::string> ids;
     if (full) ids = detail::job_ids(*traces[i], jo, met[i].job_count);
@@ -469,11 +499,9 @@ inline std::vector<PartitionConfig> best_static_chosen_batch(
   if (n) {
     std::vector<uint64_t> seeds(n, opt.predictor.rng_seed);
     const miso_b200_sim_options c = detail::to_c(opt);
-    Device& d = Device::get();
-    std::lock_guard<std::mutex> lock(d.mu());
-    d.use_catalog(catalog);
-    Device::check(miso_b200_simulate_batch_host(
-        d.ctx(), &c, static_cast<int>(n), static_cast<int>(traces.size()), probe_tt.data(),
+    AllDevices all(catalog);
+    Device::check(miso_b200_simulate_batch_sharded(
+        all.contexts(), all.size(), &c, static_cast<int>(n), static_cast<int>(traces.size()), probe_tt.data(),
         probe_sc.data(), ta.offsets.data(), ta.arrival.data(), ta.base.data(), ta.speeds.data(),
         ta.mem.data(), ta.qos.data(), nullptr, seeds.data(), met.data(), nullptr, nullptr, 0,
         nullptr, 0, MISO_B200_SIM_JCT_ONLY | MISO_B200_SIM_PRUNE));
@@ -481,7 +509,8 @@ inline std::vector<PartitionConfig> best_static_chosen_batch(
   std::vector<std::vector<double>> table(traces.size(),
                                          std::vector<double>(E, std::numeric_limits<double>::infinity()));
   for (size_t i = 0; i < n; ++i) {
-    if (met[i].status && met[i].status != MISO_B200_SIM_PRUNED) detail::throw_status(met[i].status);
+    if (met[i].status && met[i].status != MISO_B200_SIM_PRUNED)
+      detail::throw_status(met[i].status, met[i].detail, traces[size_t(probe_tt[i])]);
     table[size_t(probe_tt[i])][size_t(probe_e[i])] = met[i].avg_jct_s;
   }
   for (size_t ti = 0; ti < traces.size(); ++ti) {

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -52,6 +53,12 @@ struct miso_b200_ctx {
   bool h_lut_valid = false;
   unsigned char* d_sim_ws = nullptr;
   size_t sim_ws_bytes = 0;
+  double* d_sim_draws = nullptr;  // the noisy predictor's precomputed draws (SimBatch::draws)
+  size_t sim_draws_bytes = 0;
+  // device staging arena of the synchronous *_host simulator / predictor / trace calls (grown
+  // stream-ordered, reused across calls)
+  unsigned char* d_arena = nullptr;
+  size_t arena_bytes = 0;
 };
 
 namespace {
@@ -238,6 +245,8 @@ void miso_b200_destroy(miso_b200_ctx* ctx) {
   cudaFree(ctx->d_obj);
   cudaFree(ctx->d_spare_lut);
   cudaFree(ctx->d_sim_ws);
+  cudaFree(ctx->d_sim_draws);
+  cudaFree(ctx->d_arena);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   for (auto& s : ctx->streams)
     if (s) cudaStreamDestroy(s);
@@ -601,22 +610,24 @@ int miso_b200_generate_traces_device(miso_b200_ctx* ctx, const uint64_t* seeds, 
 static int64_t us_from_s_host(double s) { return static_cast<int64_t>(std::llround(s * 1e6)); }
 
 int miso_b200_simulate_batch(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                             const int32_t* task_trace, const uint8_t* static_counts,
-                             const int32_t* job_offsets, const double* arrival_s,
-                             const double* base_s, const double* speeds5, const uint8_t* mem_gb,
-                             const int8_t* qos_kind, const uint64_t* rng_seed,
-                             miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
-                             miso_b200_log_record* log, int64_t log_cap, double* stp_series,
-                             int64_t stp_cap, void* stream) {
-  return miso_b200_simulate_batch_ex(ctx, opt, n_seeds, task_trace, static_counts, job_offsets,
-                                     arrival_s, base_s, speeds5, mem_gb, qos_kind, nullptr,
-                                     rng_seed, metrics, job_jct_us, nullptr, log, log_cap,
-                                     stp_series, stp_cap, 0u, stream);
+                             int n_traces, int max_jobs, const int32_t* task_trace,
+                             const uint8_t* static_counts, const int32_t* job_offsets,
+                             const double* arrival_s, const double* base_s, const double* speeds5,
+                             const uint8_t* mem_gb, const int8_t* qos_kind,
+                             const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                             int64_t* job_jct_us, miso_b200_log_record* log, int64_t log_cap,
+                             double* stp_series, int64_t stp_cap, void* stream) {
+  return miso_b200_simulate_batch_ex(ctx, opt, n_seeds, n_traces, max_jobs, task_trace,
+                                     static_counts, job_offsets, arrival_s, base_s, speeds5,
+                                     mem_gb, qos_kind, nullptr, rng_seed, metrics, job_jct_us,
+                                     nullptr, log, log_cap, stp_series, stp_cap, 0u, stream);
 }
 
 namespace {
-int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                  const int32_t* task_trace, const uint8_t* static_counts,
+// Stream-ordered: every check below is on host-side arguments; per-task input errors (the
+// reference's invalid_argument cases) are found by the kernel and reported per task.
+int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds, int n_traces,
+                  int max_jobs, const int32_t* task_trace, const uint8_t* static_counts,
                   const int32_t* job_offsets, const double* arrival_s, const double* base_s,
                   const double* speeds5, const uint8_t* mem_gb, const int8_t* qos_kind,
                   const uint8_t* instances, const uint64_t* rng_seed,
@@ -629,6 +640,9 @@ int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_se
     return fail(MISO_B200_E_INVALID, "JCT_ONLY runs keep no STP series");
   if (n_seeds < 0) return fail(MISO_B200_E_INVALID, "n_seeds < 0");
   if (n_seeds == 0) return MISO_B200_OK;
+  if (n_traces < 1) return fail(MISO_B200_E_INVALID, "n_traces must be >= 1");
+  if (!task_trace && n_traces < n_seeds) return fail(MISO_B200_E_INVALID, "fewer traces than tasks");
+  if (max_jobs < 1) return fail(MISO_B200_E_INVALID, "max_jobs must be >= 1");
   if (opt->policy != MISO_B200_POLICY_NOPART && opt->policy != MISO_B200_POLICY_ORACLE &&
       opt->policy != MISO_B200_POLICY_MISO && opt->policy != MISO_B200_POLICY_OPTSTA)
     return fail(MISO_B200_E_INVALID, "unknown policy");
@@ -642,64 +656,26 @@ int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_se
   if (!(opt->interference > 0.0 && opt->interference <= 1.0))
     return fail(MISO_B200_E_INVALID, "interference must be in (0, 1]");
   if (int rc = check_predictor(opt->predictor_noisy ? 1 : 0, opt->target_mae)) return rc;
+  if (job_jct_us && task_trace)
+    return fail(MISO_B200_E_INVALID, "job_jct_us is indexed by trace job: not with task_trace (use job_out)");
   if (!job_offsets || !arrival_s || !base_s || !speeds5 || !mem_gb || !qos_kind || !rng_seed ||
       !metrics)
     return fail(MISO_B200_E_INVALID, "null buffer");
   DeviceGuard g(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // max jobs per task (device arrays: read the index arrays back once)
-  int n_traces = n_seeds;
-  std::vector<int32_t> tt;
-  if (task_trace) {
-    tt.resize(size_t(n_seeds));
-    CUDA_TRY(cudaMemcpyAsync(tt.data(), task_trace, tt.size() * 4, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    n_traces = 0;
-    for (int v : tt) {
-      if (v < 0) return fail(MISO_B200_E_INVALID, "negative task_trace entry");
-      n_traces = std::max(n_traces, v + 1);
-    }
-  }
-  std::vector<int32_t> offs(size_t(n_traces) + 1);
-  CUDA_TRY(cudaMemcpyAsync(offs.data(), job_offsets, offs.size() * 4, cudaMemcpyDeviceToHost, s));
-  if (static_counts && opt->policy == MISO_B200_POLICY_OPTSTA) {
-    std::vector<uint8_t> sc(size_t(n_seeds) * 5);
-    CUDA_TRY(cudaMemcpyAsync(sc.data(), static_counts, sc.size(), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-    for (int i = 0; i < n_seeds; ++i)
-      if (!feasible(&sc[size_t(i) * 5]))
-        return fail(MISO_B200_E_INVALID, "static partition of task " + std::to_string(i) + " is not feasible");
-  }
-  CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<uint8_t> inst;
-  if (instances && offs[size_t(n_traces)] > offs[0]) {  // capacity includes every clone
-    inst.resize(size_t(offs[size_t(n_traces)]));
-    CUDA_TRY(cudaMemcpyAsync(inst.data(), instances, inst.size(), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
-  }
-  int max_jobs = 0;
-  for (int i = 0; i < n_traces; ++i) {
-    int J = offs[i + 1] - offs[i];
-    if (J < 1) return fail(MISO_B200_E_INVALID, "trace has no jobs");  // sim.hpp:210
-    for (int q = offs[i]; !inst.empty() && q < offs[i + 1]; ++q) {
-      if (inst[size_t(q)] < 1) return fail(MISO_B200_E_INVALID, "instance count must be >= 1");
-      J += inst[size_t(q)] - 1;
-    }
-    max_jobs = std::max(max_jobs, J);
-  }
-  if (!ctx->lut_valid) {
+  if (!ctx->lut_valid) {  // (host_lut persists in the context: the async copy may lag)
     const std::vector<int8_t>& lut = host_lut(ctx);
-    if (!ctx->d_spare_lut) CUDA_TRY(cudaMalloc(&ctx->d_spare_lut, lut.size()));
-    CUDA_TRY(cudaMemcpy(ctx->d_spare_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice));
+    if (!ctx->d_spare_lut) CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ctx->d_spare_lut), lut.size(), s));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_spare_lut, lut.data(), lut.size(), cudaMemcpyHostToDevice, s));
     ctx->lut_valid = true;
   }
   const size_t stride = sim_workspace_stride(max_jobs, opt->cluster_size);
   const size_t need = stride * size_t(n_seeds);
-  if (need > ctx->sim_ws_bytes) {
-    if (int rc = stop_server(ctx)) return rc;
-    cudaFree(ctx->d_sim_ws);
+  if (need > ctx->sim_ws_bytes) {  // grown in stream order (no device-wide synchronisation)
+    if (ctx->d_sim_ws) CUDA_TRY(cudaFreeAsync(ctx->d_sim_ws, s));
     ctx->d_sim_ws = nullptr;
-    CUDA_TRY(cudaMalloc(&ctx->d_sim_ws, need));
+    ctx->sim_ws_bytes = 0;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ctx->d_sim_ws), need, s));
     ctx->sim_ws_bytes = need;
   }
   SimParams p{};
@@ -713,16 +689,17 @@ int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_se
   p.interference = opt->interference;
   p.target_mae = opt->target_mae;
   p.drift_threshold = opt->reprofile_drift_threshold;
-  p.max_events = opt->max_events ? opt->max_events : 100000000ull;
+  p.max_events = opt->max_events;
   p.track_stp = (flags & MISO_B200_SIM_JCT_ONLY) ? 0 : 1;
   p.en0 = ctx->en0;
   p.en1 = ctx->en1;
   SimBatch b{};
   b.n_seeds = n_seeds;
+  b.n_traces = n_traces;
   b.max_jobs = max_jobs;
   b.job_offsets = job_offsets;
   b.task_trace = task_trace;
-  b.static_counts = static_counts;
+  b.static_counts = opt->policy == MISO_B200_POLICY_OPTSTA ? static_counts : nullptr;
   b.arrival_s = arrival_s;
   b.base_s = base_s;
   b.speeds5 = speeds5;
@@ -742,60 +719,108 @@ int simulate_impl(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_se
   b.stp_cap = stp_series ? stp_cap : 0;
   b.prune_bound = prune_bound;
   double w2[4], w1[4];
-  default_model(w2, w1);
+  if (opt->small_slice_model_fitted) {  // SimOptions::small_slice_model (sim.hpp:88, 894-896)
+    std::memcpy(w2, opt->small_slice_w2, sizeof(w2));
+    std::memcpy(w1, opt->small_slice_w1, sizeof(w1));
+  } else {
+    default_model(w2, w1);
+  }
+  // miso with the noisy predictor: every task's draws for call nonces 1..max_jobs computed
+  // ahead by a throughput kernel (a session caches estimates for at least one job, so without
+  // re-profiling there are at most max_jobs calls; later nonces are drawn in the event loop)
+  static const bool draws_on = [] {
+    const char* e = getenv("MISO_B200_SIM_DRAWS");  // (tuning: 0 = draw inside the event loop)
+    return !(e && atoi(e) == 0);
+  }();
+  if (draws_on && opt->policy == MISO_B200_POLICY_MISO && p.noisy && p.target_mae > 0.0) {
+    const size_t need_d = size_t(n_seeds) * size_t(max_jobs) * 14 * sizeof(double);
+    if (need_d > ctx->sim_draws_bytes) {
+      if (ctx->d_sim_draws) CUDA_TRY(cudaFreeAsync(ctx->d_sim_draws, s));
+      ctx->d_sim_draws = nullptr;
+      ctx->sim_draws_bytes = 0;
+      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ctx->d_sim_draws), need_d, s));
+      ctx->sim_draws_bytes = need_d;
+    }
+    CUDA_TRY(launch_sim_draws(rng_seed, n_seeds, max_jobs, ctx->d_sim_draws, s));
+    b.draws = ctx->d_sim_draws;
+    b.draws_k = max_jobs;
+  }
   CUDA_TRY(launch_simulate(b, p, w2, w1, s));
   return MISO_B200_OK;
 }
 }  // namespace
 
 int miso_b200_simulate_batch_ex(miso_b200_ctx* ctx, const miso_b200_sim_options* opt, int n_seeds,
-                                const int32_t* task_trace, const uint8_t* static_counts,
-                                const int32_t* job_offsets, const double* arrival_s,
-                                const double* base_s, const double* speeds5,
-                                const uint8_t* mem_gb, const int8_t* qos_kind,
-                                const uint8_t* instances, const uint64_t* rng_seed,
-                                miso_b200_sim_metrics* metrics, int64_t* job_jct_us,
-                                int64_t* job_out, miso_b200_log_record* log, int64_t log_cap,
-                                double* stp_series, int64_t stp_cap, unsigned flags,
-                                void* stream) {
-  return simulate_impl(ctx, opt, n_seeds, task_trace, static_counts, job_offsets, arrival_s,
-                       base_s, speeds5, mem_gb, qos_kind, instances, rng_seed, metrics,
-                       job_jct_us, job_out, log, log_cap, stp_series, stp_cap, flags, nullptr,
-                       stream);
+                                int n_traces, int max_jobs, const int32_t* task_trace,
+                                const uint8_t* static_counts, const int32_t* job_offsets,
+                                const double* arrival_s, const double* base_s,
+                                const double* speeds5, const uint8_t* mem_gb,
+                                const int8_t* qos_kind, const uint8_t* instances,
+                                const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                int64_t* job_jct_us, int64_t* job_out, miso_b200_log_record* log,
+                                int64_t log_cap, double* stp_series, int64_t stp_cap,
+                                unsigned flags, void* stream) {
+  return simulate_impl(ctx, opt, n_seeds, n_traces, max_jobs, task_trace, static_counts,
+                       job_offsets, arrival_s, base_s, speeds5, mem_gb, qos_kind, instances,
+                       rng_seed, metrics, job_jct_us, job_out, log, log_cap, stp_series, stp_cap,
+                       flags, nullptr, stream);
 }
 
 int miso_b200_simulate_batch_pruned(miso_b200_ctx* ctx, const miso_b200_sim_options* opt,
-                                    int n_tasks, const int32_t* task_trace,
-                                    const uint8_t* static_counts, const int32_t* job_offsets,
-                                    const double* arrival_s, const double* base_s,
-                                    const double* speeds5, const uint8_t* mem_gb,
-                                    const int8_t* qos_kind, const uint64_t* rng_seed,
-                                    miso_b200_sim_metrics* metrics, int64_t* bound,
-                                    unsigned flags, void* stream) {
+                                    int n_tasks, int n_traces, int max_jobs,
+                                    const int32_t* task_trace, const uint8_t* static_counts,
+                                    const int32_t* job_offsets, const double* arrival_s,
+                                    const double* base_s, const double* speeds5,
+                                    const uint8_t* mem_gb, const int8_t* qos_kind,
+                                    const uint64_t* rng_seed, miso_b200_sim_metrics* metrics,
+                                    int64_t* bound, unsigned flags, void* stream) {
   if (!opt || opt->policy != MISO_B200_POLICY_OPTSTA)
     return fail(MISO_B200_E_INVALID, "pruned runs are optsta candidate searches");
   if (!task_trace || !bound) return fail(MISO_B200_E_INVALID, "task_trace and bound are required");
-  return simulate_impl(ctx, opt, n_tasks, task_trace, static_counts, job_offsets, arrival_s,
-                       base_s, speeds5, mem_gb, qos_kind, nullptr, rng_seed, metrics, nullptr,
-                       nullptr, nullptr, 0, nullptr, 0, flags, bound, stream);
+  return simulate_impl(ctx, opt, n_tasks, n_traces, max_jobs, task_trace, static_counts,
+                       job_offsets, arrival_s, base_s, speeds5, mem_gb, qos_kind, nullptr,
+                       rng_seed, metrics, nullptr, nullptr, nullptr, 0, nullptr, 0, flags, bound,
+                       stream);
 }
 
 extern "C++" {
 namespace {
-struct DevBuf {  // owning device allocation for the synchronous host-pointer calls
-  void* p = nullptr;
-  ~DevBuf() { cudaFree(p); }
+// The synchronous host-pointer calls stage their device copies in one per-context arena,
+// carved with 256-byte alignment and grown in stream order (no per-call cudaMalloc/cudaFree).
+struct Arena {
+  size_t used = 0;
+  std::vector<std::pair<void**, size_t>> parts;
+  template <class T>
+  void add(T** p, size_t n) {
+    parts.emplace_back(reinterpret_cast<void**>(p), n * sizeof(T));
+    *p = nullptr;
+  }
+  int commit(miso_b200_ctx* ctx, cudaStream_t s) {
+    size_t total = 0;
+    for (auto& pr : parts) total += (pr.second + 255) & ~size_t(255);
+    if (total > ctx->arena_bytes) {
+      if (ctx->d_arena) CUDA_TRY(cudaFreeAsync(ctx->d_arena, s));
+      ctx->d_arena = nullptr;
+      ctx->arena_bytes = 0;
+      CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&ctx->d_arena), total, s));
+      ctx->arena_bytes = total;
+    }
+    size_t off = 0;
+    for (auto& pr : parts) {
+      *pr.first = pr.second ? ctx->d_arena + off : nullptr;
+      off += (pr.second + 255) & ~size_t(255);
+    }
+    return MISO_B200_OK;
+  }
 };
 template <class T>
-int upload(DevBuf& d, const T* src, size_t n, cudaStream_t s) {
+int upload(T* d, const T* src, size_t n, cudaStream_t s) {
   if (!src || n == 0) return MISO_B200_OK;
-  CUDA_TRY(cudaMalloc(&d.p, n * sizeof(T)));
-  CUDA_TRY(cudaMemcpyAsync(d.p, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
   return MISO_B200_OK;
 }
-int alloc_out(DevBuf& d, size_t bytes) {
-  if (bytes == 0) return MISO_B200_OK;
-  CUDA_TRY(cudaMalloc(&d.p, bytes));
+int ensure_stream0(miso_b200_ctx* ctx) {
+  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
   return MISO_B200_OK;
 }
 }  // namespace
@@ -813,13 +838,10 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if (!ctx || !opt) return fail(MISO_B200_E_INVALID, "null argument");
   if (n_tasks < 0 || n_traces < 0) return fail(MISO_B200_E_INVALID, "negative count");
   if (n_tasks == 0) return MISO_B200_OK;
-  {
-    DeviceGuard g(ctx->device);
-    if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
-  }
   if (!job_offsets || !arrival_s || !base_s || !speeds5 || !mem_gb || !qos_kind || !rng_seed ||
       !metrics)
     return fail(MISO_B200_E_INVALID, "null buffer");
+  if (n_traces < 1) return fail(MISO_B200_E_INVALID, "n_traces must be >= 1");
   if (!task_trace && n_traces < n_tasks) return fail(MISO_B200_E_INVALID, "fewer traces than tasks");
   const bool prune = (flags & MISO_B200_SIM_PRUNE) != 0;
   flags &= ~MISO_B200_SIM_PRUNE;
@@ -836,22 +858,47 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if (task_trace)
     for (int t = 0; t < n_tasks; ++t)
       if (task_trace[t] < 0 || task_trace[t] >= n_traces) return fail(MISO_B200_E_INVALID, "task_trace out of range");
-  int max_jobs = 0;
+  int max_jobs = 1;
   for (int i = 0; i < n_traces; ++i) {
     int Jt = job_offsets[i + 1] - job_offsets[i];
-    for (int q = job_offsets[i]; instances && q < job_offsets[i + 1]; ++q) {
-      if (instances[q] < 1) return fail(MISO_B200_E_INVALID, "instance count must be >= 1");
-      Jt += instances[q] - 1;
-    }
+    for (int q = job_offsets[i]; instances && q < job_offsets[i + 1]; ++q)
+      Jt += instances[q] > 1 ? instances[q] - 1 : 0;  // (< 1: the kernel reports the task)
     max_jobs = std::max(max_jobs, Jt);
   }
   const size_t J = size_t(job_offsets[n_traces]);
   DeviceGuard g(ctx->device);
-  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  if (int rc = ensure_stream0(ctx)) return rc;
   cudaStream_t s = ctx->streams[0];
-  DevBuf d_tt, d_sc, d_off, d_arr, d_base, d_sp, d_mem, d_qos, d_inst, d_seed, d_met, d_jo, d_log,
-      d_stp;
+  int32_t *d_tt, *d_off;
+  uint8_t *d_sc, *d_mem, *d_inst;
+  double *d_arr, *d_base, *d_sp, *d_stp;
+  int8_t* d_qos;
+  uint64_t* d_seed;
+  miso_b200_sim_metrics* d_met;
+  int64_t *d_jo, *d_bound;
+  miso_b200_log_record* d_log;
+  const size_t jo_n = job_out ? size_t(n_tasks) * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : 0;
+  const size_t log_n = log ? size_t(n_tasks) * size_t(std::max<int64_t>(log_cap, 0)) : 0;
+  const size_t stp_n = stp_series ? size_t(n_tasks) * 2 * size_t(std::max<int64_t>(stp_cap, 0)) : 0;
+  Arena ar;
+  ar.add(&d_tt, task_trace ? size_t(n_tasks) : 0);
+  ar.add(&d_sc, static_counts ? size_t(n_tasks) * 5 : 0);
+  ar.add(&d_off, size_t(n_traces) + 1);
+  ar.add(&d_arr, J);
+  ar.add(&d_base, J);
+  ar.add(&d_sp, J * 5);
+  ar.add(&d_mem, J);
+  ar.add(&d_qos, J);
+  ar.add(&d_inst, instances ? J : 0);
+  ar.add(&d_seed, size_t(n_tasks));
+  ar.add(&d_met, size_t(n_tasks));
+  ar.add(&d_jo, jo_n);
+  ar.add(&d_log, log_n);
+  ar.add(&d_stp, stp_n);
+  ar.add(&d_bound, prune ? size_t(n_traces) : 0);
   int rc;
+  if ((rc = ar.commit(ctx, s))) return rc;
+  std::vector<int64_t> b0(prune ? size_t(n_traces) : 0, INT64_MAX);  // no completed candidate yet
   if ((rc = upload(d_tt, task_trace, task_trace ? size_t(n_tasks) : 0, s))) return rc;
   if ((rc = upload(d_sc, static_counts, static_counts ? size_t(n_tasks) * 5 : 0, s))) return rc;
   if ((rc = upload(d_off, job_offsets, size_t(n_traces) + 1, s))) return rc;
@@ -862,32 +909,17 @@ int miso_b200_simulate_batch_host(miso_b200_ctx* ctx, const miso_b200_sim_option
   if ((rc = upload(d_qos, qos_kind, J, s))) return rc;
   if ((rc = upload(d_inst, instances, instances ? J : 0, s))) return rc;
   if ((rc = upload(d_seed, rng_seed, size_t(n_tasks), s))) return rc;
-  if ((rc = alloc_out(d_met, sizeof(miso_b200_sim_metrics) * size_t(n_tasks)))) return rc;
-  const size_t jo_n = job_out ? size_t(n_tasks) * size_t(max_jobs) * MISO_B200_JOB_OUT_FIELDS : 0;
-  if ((rc = alloc_out(d_jo, jo_n * sizeof(int64_t)))) return rc;
-  const size_t log_n = log ? size_t(n_tasks) * size_t(std::max<int64_t>(log_cap, 0)) : 0;
-  if ((rc = alloc_out(d_log, log_n * sizeof(miso_b200_log_record)))) return rc;
-  const size_t stp_n = stp_series ? size_t(n_tasks) * 2 * size_t(std::max<int64_t>(stp_cap, 0)) : 0;
-  if ((rc = alloc_out(d_stp, stp_n * sizeof(double)))) return rc;
-  DevBuf d_bound;
-  std::vector<int64_t> b0(prune ? size_t(n_traces) : 0, INT64_MAX);  // no completed candidate yet
   if ((rc = upload(d_bound, b0.data(), b0.size(), s))) return rc;
-  rc = simulate_impl(
-      ctx, opt, n_tasks, static_cast<const int32_t*>(d_tt.p), static_cast<const uint8_t*>(d_sc.p),
-      static_cast<const int32_t*>(d_off.p), static_cast<const double*>(d_arr.p),
-      static_cast<const double*>(d_base.p), static_cast<const double*>(d_sp.p),
-      static_cast<const uint8_t*>(d_mem.p), static_cast<const int8_t*>(d_qos.p),
-      prune ? nullptr : static_cast<const uint8_t*>(d_inst.p), static_cast<const uint64_t*>(d_seed.p),
-      static_cast<miso_b200_sim_metrics*>(d_met.p),
-      nullptr, static_cast<int64_t*>(d_jo.p), static_cast<miso_b200_log_record*>(d_log.p),
-      log ? log_cap : 0, static_cast<double*>(d_stp.p), stp_series ? stp_cap : 0, flags,
-      prune ? static_cast<int64_t*>(d_bound.p) : nullptr, s);
+  rc = simulate_impl(ctx, opt, n_tasks, n_traces, max_jobs, d_tt, d_sc, d_off, d_arr, d_base,
+                     d_sp, d_mem, d_qos, prune ? nullptr : d_inst, d_seed, d_met, nullptr, d_jo,
+                     d_log, log ? log_cap : 0, d_stp, stp_series ? stp_cap : 0, flags,
+                     prune ? d_bound : nullptr, s);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(metrics, d_met.p, sizeof(miso_b200_sim_metrics) * size_t(n_tasks),
+  CUDA_TRY(cudaMemcpyAsync(metrics, d_met, sizeof(miso_b200_sim_metrics) * size_t(n_tasks),
                            cudaMemcpyDeviceToHost, s));
-  if (jo_n) CUDA_TRY(cudaMemcpyAsync(job_out, d_jo.p, jo_n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  if (log_n) CUDA_TRY(cudaMemcpyAsync(log, d_log.p, log_n * sizeof(miso_b200_log_record), cudaMemcpyDeviceToHost, s));
-  if (stp_n) CUDA_TRY(cudaMemcpyAsync(stp_series, d_stp.p, stp_n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (jo_n) CUDA_TRY(cudaMemcpyAsync(job_out, d_jo, jo_n * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (log_n) CUDA_TRY(cudaMemcpyAsync(log, d_log, log_n * sizeof(miso_b200_log_record), cudaMemcpyDeviceToHost, s));
+  if (stp_n) CUDA_TRY(cudaMemcpyAsync(stp_series, d_stp, stp_n * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return MISO_B200_OK;
 }
@@ -899,18 +931,19 @@ int miso_b200_predict_host(miso_b200_ctx* ctx, const double* truth3, uint64_t nc
   if (ncols == 0) return MISO_B200_OK;
   if (!truth3 || !out5) return fail(MISO_B200_E_INVALID, "null buffer");
   DeviceGuard g(ctx->device);
-  if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
-  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  if (int rc = ensure_stream0(ctx)) return rc;
   cudaStream_t s = ctx->streams[0];
-  DevBuf d_in, d_out;
+  double *d_in, *d_out;
+  Arena ar;
+  ar.add(&d_in, size_t(ncols) * 3);
+  ar.add(&d_out, size_t(ncols) * 5);
   int rc;
+  if ((rc = ar.commit(ctx, s))) return rc;
   if ((rc = upload(d_in, truth3, size_t(ncols) * 3, s))) return rc;
-  if ((rc = alloc_out(d_out, size_t(ncols) * 5 * sizeof(double)))) return rc;
-  rc = miso_b200_predict_batch(ctx, static_cast<const double*>(d_in.p), ncols, cols_per_group,
-                               first_nonce, rng_seed, mode, target_mae, w2, w1,
-                               static_cast<double*>(d_out.p), s);
+  rc = miso_b200_predict_batch(ctx, d_in, ncols, cols_per_group, first_nonce, rng_seed, mode,
+                               target_mae, w2, w1, d_out, s);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out5, d_out.p, size_t(ncols) * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(out5, d_out, size_t(ncols) * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return MISO_B200_OK;
 }
@@ -929,26 +962,28 @@ int miso_b200_generate_traces_device_host(miso_b200_ctx* ctx, const uint64_t* se
                                             arrival_s, duration_s, speeds5, mem_gb, nullptr);
   if (!seeds || !arrival_s || !duration_s || !speeds5 || !mem_gb) return fail(MISO_B200_E_INVALID, "null buffer");
   DeviceGuard g(ctx->device);
-  if (int rc = stop_server(ctx)) return rc;  // the staging buffers below are cudaFree'd
-  if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
+  if (int rc = ensure_stream0(ctx)) return rc;
   cudaStream_t s = ctx->streams[0];
   const size_t J = size_t(n_traces) * size_t(job_count);
-  DevBuf d_seed, d_a, d_d, d_sp, d_m;
+  uint64_t* d_seed;
+  double *d_a, *d_d, *d_sp;
+  int* d_m;
+  Arena ar;
+  ar.add(&d_seed, size_t(n_traces));
+  ar.add(&d_a, J);
+  ar.add(&d_d, J);
+  ar.add(&d_sp, J * 5);
+  ar.add(&d_m, J);
   int rc;
+  if ((rc = ar.commit(ctx, s))) return rc;
   if ((rc = upload(d_seed, seeds, size_t(n_traces), s))) return rc;
-  if ((rc = alloc_out(d_a, J * sizeof(double)))) return rc;
-  if ((rc = alloc_out(d_d, J * sizeof(double)))) return rc;
-  if ((rc = alloc_out(d_sp, J * 5 * sizeof(double)))) return rc;
-  if ((rc = alloc_out(d_m, J * sizeof(int)))) return rc;
-  rc = miso_b200_generate_traces_device(
-      ctx, static_cast<const uint64_t*>(d_seed.p), n_traces, job_count, lambda_s, max_duration_s,
-      dist, sigma, fixed_s, lo_s, hi_s, static_cast<double*>(d_a.p), static_cast<double*>(d_d.p),
-      static_cast<double*>(d_sp.p), static_cast<int*>(d_m.p), s);
+  rc = miso_b200_generate_traces_device(ctx, d_seed, n_traces, job_count, lambda_s, max_duration_s,
+                                        dist, sigma, fixed_s, lo_s, hi_s, d_a, d_d, d_sp, d_m, s);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(arrival_s, d_a.p, J * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(duration_s, d_d.p, J * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(speeds5, d_sp.p, J * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(cudaMemcpyAsync(mem_gb, d_m.p, J * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(arrival_s, d_a, J * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(duration_s, d_d, J * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(speeds5, d_sp, J * 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(mem_gb, d_m, J * sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   return MISO_B200_OK;
 }
@@ -965,6 +1000,165 @@ int miso_b200_max_spare_slice(miso_b200_ctx* ctx, const uint8_t* min_kinds, int 
   }
   *kind = host_lut(ctx)[size_t((((cnt[0] * 7 + cnt[1]) * 7 + cnt[2]) * 7 + cnt[3]) * 7 + cnt[4])];
   return MISO_B200_OK;
+}
+
+int miso_b200_device_count(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
+}  // extern "C"
+
+namespace {
+// One host thread per context (a context serves one host thread at a time); the first failing
+// shard's status and message are reported on the caller's thread.
+int run_shards(int n_ctx, const std::function<int(int)>& f) {
+  std::vector<int> rc(static_cast<size_t>(n_ctx), 0);
+  std::vector<std::string> errs(static_cast<size_t>(n_ctx), std::string());
+  auto one = [&rc, &errs, &f](int k) {
+    const int r = f(k);
+    rc[size_t(k)] = r;
+    if (r) errs[size_t(k)].assign(miso_b200_last_error());
+  };
+  std::vector<std::thread> th;
+  for (int k = 1; k < n_ctx; ++k) th.emplace_back(one, k);
+  one(0);
+  for (auto& t : th) t.join();
+  for (int k = 0; k < n_ctx; ++k)
+    if (rc[size_t(k)]) return fail(rc[size_t(k)], "shard " + std::to_string(k) + ": " + errs[size_t(k)]);
+  return MISO_B200_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int miso_b200_optimize_batch_sharded(miso_b200_ctx* const* ctxs, int n_ctx, const double* speeds,
+                                     const uint32_t* offsets, uint64_t n, uint8_t* cand,
+                                     double* obj) {
+  if (!ctxs || n_ctx < 1) return fail(MISO_B200_E_INVALID, "need at least one context");
+  for (int k = 0; k < n_ctx; ++k)
+    if (!ctxs[k]) return fail(MISO_B200_E_INVALID, "null context");
+  if (n == 0) return MISO_B200_OK;
+  if (!speeds || !offsets || !cand || !obj) return fail(MISO_B200_E_INVALID, "null buffer");
+  if (offsets[n] < offsets[0]) return fail(MISO_B200_E_MALFORMED, "offsets must be non-decreasing");
+  if (n_ctx == 1) return miso_b200_optimize_batch_host(ctxs[0], speeds, offsets, n, cand, obj);
+  return run_shards(n_ctx, [&](int k) -> int {
+    const uint64_t lo = n * uint64_t(k) / uint64_t(n_ctx), hi = n * uint64_t(k + 1) / uint64_t(n_ctx);
+    if (hi == lo) return MISO_B200_OK;
+    const uint32_t base = offsets[lo];
+    std::vector<uint32_t> off(hi - lo + 1);  // the shard's offsets, rebased to its first row
+    for (uint64_t i = 0; i <= hi - lo; ++i) {
+      if (offsets[lo + i] < base) return fail(MISO_B200_E_MALFORMED, "offsets must be non-decreasing");
+      off[i] = offsets[lo + i] - base;
+    }
+    return miso_b200_optimize_batch_host(ctxs[k], speeds + size_t(base) * 5, off.data(), hi - lo,
+                                         cand + lo, obj + lo);
+  });
+}
+
+int miso_b200_simulate_batch_sharded(miso_b200_ctx* const* ctxs, int n_ctx,
+                                     const miso_b200_sim_options* opt, int n_tasks, int n_traces,
+                                     const int32_t* task_trace, const uint8_t* static_counts,
+                                     const int32_t* job_offsets, const double* arrival_s,
+                                     const double* base_s, const double* speeds5,
+                                     const uint8_t* mem_gb, const int8_t* qos_kind,
+                                     const uint8_t* instances, const uint64_t* rng_seed,
+                                     miso_b200_sim_metrics* metrics, int64_t* job_out,
+                                     miso_b200_log_record* log, int64_t log_cap,
+                                     double* stp_series, int64_t stp_cap, unsigned flags) {
+  if (!ctxs || n_ctx < 1) return fail(MISO_B200_E_INVALID, "need at least one context");
+  for (int k = 0; k < n_ctx; ++k)
+    if (!ctxs[k]) return fail(MISO_B200_E_INVALID, "null context");
+  if (n_ctx == 1 || n_tasks <= 1)
+    return miso_b200_simulate_batch_host(ctxs[0], opt, n_tasks, n_traces, task_trace, static_counts,
+                                         job_offsets, arrival_s, base_s, speeds5, mem_gb, qos_kind,
+                                         instances, rng_seed, metrics, job_out, log, log_cap,
+                                         stp_series, stp_cap, flags);
+  if (!opt) return fail(MISO_B200_E_INVALID, "null argument");
+  if (n_tasks < 0 || n_traces < 1) return fail(MISO_B200_E_INVALID, "negative count");
+  if (!job_offsets || !metrics || !rng_seed) return fail(MISO_B200_E_INVALID, "null buffer");
+  if (!task_trace && n_traces < n_tasks) return fail(MISO_B200_E_INVALID, "fewer traces than tasks");
+  for (int t = 0; task_trace && t < n_tasks; ++t)
+    if (task_trace[t] < 0 || task_trace[t] >= n_traces) return fail(MISO_B200_E_INVALID, "task_trace out of range");
+  for (int i = 0; i < n_traces; ++i)
+    if (job_offsets[i + 1] < job_offsets[i]) return fail(MISO_B200_E_INVALID, "job_offsets must be non-decreasing");
+  // the single-call layout: job_out stride = the largest instance total of all traces
+  int max_jobs = 1;
+  for (int i = 0; i < n_traces; ++i) {
+    int Jt = job_offsets[i + 1] - job_offsets[i];
+    for (int q = job_offsets[i]; instances && q < job_offsets[i + 1]; ++q)
+      Jt += instances[q] > 1 ? instances[q] - 1 : 0;
+    max_jobs = std::max(max_jobs, Jt);
+  }
+  // tasks per trace -> contiguous trace ranges of about n_tasks / n_ctx tasks each
+  const int used = task_trace ? n_traces : n_tasks;
+  std::vector<int64_t> cum(static_cast<size_t>(used) + 1, 0);
+  for (int t = 0; t < n_tasks; ++t) ++cum[size_t(task_trace ? task_trace[t] : t) + 1];
+  for (int i = 0; i < used; ++i) cum[size_t(i) + 1] += cum[size_t(i)];
+  std::vector<int> cut(static_cast<size_t>(n_ctx) + 1, used);
+  cut[0] = 0;
+  for (int k = 1; k < n_ctx; ++k) {
+    const int64_t goal = int64_t(n_tasks) * k / n_ctx;
+    cut[size_t(k)] = int(std::lower_bound(cum.begin(), cum.end(), goal) - cum.begin());
+    cut[size_t(k)] = std::max(cut[size_t(k) - 1], std::min(cut[size_t(k)], used));
+  }
+  return run_shards(n_ctx, [&](int k) -> int {
+    const int t0 = cut[size_t(k)], t1 = cut[size_t(k) + 1];  // this shard's traces
+    std::vector<int> idx;  // its tasks, in task order
+    for (int t = 0; t < n_tasks; ++t) {
+      const int tr = task_trace ? task_trace[t] : t;
+      if (tr >= t0 && tr < t1) idx.push_back(t);
+    }
+    if (idx.empty()) return MISO_B200_OK;
+    const int nt = int(idx.size()), ntr = t1 - t0;
+    const int32_t j0 = job_offsets[t0];
+    std::vector<int32_t> off(static_cast<size_t>(ntr) + 1), tt(static_cast<size_t>(nt));
+    for (int i = 0; i <= ntr; ++i) off[size_t(i)] = job_offsets[t0 + i] - j0;
+    std::vector<uint8_t> sc(static_counts ? size_t(nt) * 5 : 0);
+    std::vector<uint64_t> seeds(static_cast<size_t>(nt));
+    for (int i = 0; i < nt; ++i) {
+      const int t = idx[size_t(i)];
+      tt[size_t(i)] = (task_trace ? task_trace[t] : t) - t0;
+      seeds[size_t(i)] = rng_seed[t];
+      if (static_counts) std::memcpy(&sc[size_t(i) * 5], static_counts + size_t(t) * 5, 5);
+    }
+    int mj = 1;  // this shard's job_out stride
+    for (int i = 0; i < ntr; ++i) {
+      int Jt = off[size_t(i) + 1] - off[size_t(i)];
+      for (int q = j0 + off[size_t(i)]; instances && q < j0 + off[size_t(i) + 1]; ++q)
+        Jt += instances[q] > 1 ? instances[q] - 1 : 0;
+      mj = std::max(mj, Jt);
+    }
+    const size_t F = MISO_B200_JOB_OUT_FIELDS;
+    std::vector<miso_b200_sim_metrics> met(static_cast<size_t>(nt));
+    std::vector<int64_t> jo(job_out ? size_t(nt) * size_t(mj) * F : 0);
+    std::vector<miso_b200_log_record> lg(log ? size_t(nt) * size_t(std::max<int64_t>(log_cap, 0)) : 0);
+    std::vector<double> stp(stp_series ? size_t(nt) * 2 * size_t(std::max<int64_t>(stp_cap, 0)) : 0);
+    const size_t J0 = size_t(j0);
+    const int rc = miso_b200_simulate_batch_host(
+        ctxs[k], opt, nt, ntr, tt.data(), static_counts ? sc.data() : nullptr, off.data(),
+        arrival_s ? arrival_s + J0 : nullptr, base_s ? base_s + J0 : nullptr,
+        speeds5 ? speeds5 + 5 * J0 : nullptr, mem_gb ? mem_gb + J0 : nullptr,
+        qos_kind ? qos_kind + J0 : nullptr, instances ? instances + J0 : nullptr, seeds.data(),
+        met.data(), job_out ? jo.data() : nullptr, log ? lg.data() : nullptr, log_cap,
+        stp_series ? stp.data() : nullptr, stp_cap, flags);
+    if (rc) return rc;
+    for (int i = 0; i < nt; ++i) {  // scatter to the tasks' indices, single-call layout
+      const size_t t = size_t(idx[size_t(i)]);
+      metrics[t] = met[size_t(i)];
+      if (job_out) {
+        int64_t* dst = job_out + t * size_t(max_jobs) * F;
+        std::memcpy(dst, &jo[size_t(i) * size_t(mj) * F], size_t(mj) * F * sizeof(int64_t));
+      }
+      if (log)
+        std::memcpy(log + t * size_t(log_cap), &lg[size_t(i) * size_t(log_cap)],
+                    size_t(log_cap) * sizeof(miso_b200_log_record));
+      if (stp_series)
+        std::memcpy(stp_series + t * 2 * size_t(stp_cap), &stp[size_t(i) * 2 * size_t(stp_cap)],
+                    2 * size_t(stp_cap) * sizeof(double));
+    }
+    return MISO_B200_OK;
+  });
 }
 
 int miso_b200_host_alloc(size_t bytes, void** out) {

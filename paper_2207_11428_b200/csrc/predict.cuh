@@ -197,6 +197,52 @@ __device__ __forceinline__ void predict_column(double f7, double f4, double f3, 
   out5[4] = v0;
 }
 
+// predict_column with the call's two noise draws given (4g entry d4, 3g entry d3): the
+// perturbation, re-anchoring and extrapolation of predict_column in the same operations.
+__device__ __forceinline__ void predict_column_drawn(double f7, double f4, double f3,
+                                                     NoiseDraw d4, NoiseDraw d3, double target_mae,
+                                                     const ModelW& w, double out5[5]) {
+  double v0 = f7;
+  double v1 = perturb_apply(f4, target_mae, d4);
+  double v2 = perturb_apply(f3, target_mae, d3);
+  double mx = v0;  // std::max({a, b, c})
+  if (mx < v1) mx = v1;
+  if (mx < v2) mx = v2;
+  v0 = clampd(v0 / mx, kSpeedFloor, 1.0);
+  v1 = clampd(v1 / mx, kSpeedFloor, 1.0);
+  v2 = clampd(v2 / mx, kSpeedFloor, 1.0);
+  const double p2 = w.w2[0] * v0 + w.w2[1] * v1 + w.w2[2] * v2 + w.w2[3];
+  const double p1 = w.w1[0] * v0 + w.w1[1] * v1 + w.w1[2] * v2 + w.w1[3];
+  const double f2 = clampd(p2, kSpeedFloor, v2);
+  const double f1 = clampd(p1, kSpeedFloor, f2);
+  out5[0] = f1;
+  out5[1] = f2;
+  out5[2] = v2;
+  out5[3] = v1;
+  out5[4] = v0;
+}
+
+// A NoiseDraw packed in one double: |n01| with the sign bit clear iff the coin is heads.
+// perturb_apply reads only fabs(n01) and the coin, so the pair round-trips exactly.
+__device__ __forceinline__ double pack_draw(NoiseDraw d) {
+  const double a = fabs(d.n01);
+  return d.coin ? a : -a;
+}
+__device__ __forceinline__ NoiseDraw unpack_draw(double x) {
+  NoiseDraw d;
+  d.n01 = fabs(x);
+  d.coin = !signbit(x);
+  return d;
+}
+
+// The draws of predictor call `nonce`, column c, entry e (0 = 4g, 1 = 3g) for rng_seed
+// (profiles.hpp:234-244: entry seed mix_seed(mix_seed(rng_seed, nonce), 8c + 1 + e)).
+__device__ __forceinline__ NoiseDraw column_draw(uint64_t rng_seed, uint64_t nonce, int c, int e) {
+  uint64_t r[3];
+  mt64_first3(mix_seed(mix_seed(rng_seed, nonce), static_cast<uint64_t>(c) * 8 + 1 + e), r);
+  return noise_draw(r);
+}
+
 // profiles.hpp:60-65 with kind tables (topology.hpp:39-45). qos_kind < 0: no QoS floor.
 __host__ __device__ __forceinline__ int kind_mem_gb(int kind) {
   return kind < 2 ? (kind == 0 ? 5 : 10) : (kind < 4 ? 20 : 40);

@@ -85,4 +85,69 @@ __device__ __forceinline__ uint8_t search_any(Ptr row, int m, uint64_t en0, uint
   }
 }
 
+// optimize_partition for one roster, warp-parallel (rows: m x 5 in shared memory; all 32 lanes
+// call it). Lane l scores candidates kCandBase[m] + l (+ 32): the job-order DADD sum of search_rows with
+// invalid speeds poisoned to -inf; the winner is the largest objective, ties to the lowest
+// candidate id (= OptKey rank, optimizer.hpp:46-51), and NaN / -inf sums never win -- the
+// rank-ordered scan's rule, so the result is the same bits as search_any.
+template <int M>
+__device__ __forceinline__ void warp_score(const double* rows, const uint8_t (*place)[7], int c0,
+                                           int c1, uint64_t en0, uint64_t en1, double& best,
+                                           int& bc) {
+  for (int c = c0 + static_cast<int>(threadIdx.x & 31); c < c1; c += 32) {
+    const bool en = c < 64 ? ((en0 >> c) & 1ull) : ((en1 >> (c - 64)) & 1ull);
+    uint8_t p[M];
+#pragma unroll
+    for (int i = 0; i < M; ++i) p[i] = place[c][i];
+    double sum = poison(rows[p[0]]);
+#pragma unroll
+    for (int i = 1; i < M; ++i) sum = sum + poison(rows[i * 5 + p[i]]);
+    if (en && sum > best) {  // ids rise within a lane: strict '>' keeps the lowest
+      best = sum;
+      bc = c;
+    }
+  }
+}
+
+__device__ __forceinline__ uint8_t warp_search(const double* rows, int m, uint64_t en0,
+                                               uint64_t en1, const uint8_t (*place)[7],
+                                               double* obj) {
+  if (m < 1 || m > 7) {
+    *obj = 0.0;
+    return kCandBadM;  // optimizer.hpp:65-66 invalid_argument
+  }
+  double best = __longlong_as_double(0xFFF0000000000000ll);
+  int bc = kCandInfeasible;
+  // kCandBase[m], kCandBase[m + 1] packed one byte per m
+  constexpr uint64_t kBase = uint64_t(kCandBase[1]) | uint64_t(kCandBase[2]) << 8 |
+                             uint64_t(kCandBase[3]) << 16 | uint64_t(kCandBase[4]) << 24 |
+                             uint64_t(kCandBase[5]) << 32 | uint64_t(kCandBase[6]) << 40 |
+                             uint64_t(kCandBase[7]) << 48 | uint64_t(kCandBase[8]) << 56;
+  const int c0 = static_cast<int>((kBase >> (8 * (m - 1))) & 0xff);
+  const int c1 = static_cast<int>((kBase >> (8 * m)) & 0xff);
+  switch (m) {
+    case 1: warp_score<1>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 2: warp_score<2>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 3: warp_score<3>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 4: warp_score<4>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 5: warp_score<5>(rows, place, c0, c1, en0, en1, best, bc); break;
+    case 6: warp_score<6>(rows, place, c0, c1, en0, en1, best, bc); break;
+    default: warp_score<7>(rows, place, c0, c1, en0, en1, best, bc); break;
+  }
+  // Warp argmax on the objective's bits: a valid objective is positive (+inf included), where
+  // the IEEE order is the unsigned order of the bit patterns and equality is bit equality;
+  // no valid candidate = key 0. Then the lowest id among the lanes holding the maximum.
+  const uint64_t key = bc == kCandInfeasible ? 0ull : static_cast<uint64_t>(__double_as_longlong(best));
+  const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const unsigned id = __reduce_min_sync(0xffffffffu, hi == mhi && lo == mlo ? unsigned(bc) : 0xffu);
+  if ((mhi | mlo) == 0u) {
+    *obj = 0.0;
+    return kCandInfeasible;
+  }
+  *obj = __longlong_as_double(static_cast<long long>((uint64_t(mhi) << 32) | mlo));
+  return static_cast<uint8_t>(id);
+}
+
 }  // namespace miso_b200

@@ -1,1482 +1,43 @@
-// sim_kernel.cu -- kernel (c): batched event-step cluster simulator, one warp per trace seed.
-//
-// Restates SimEngine (sim.hpp:202-972) for the nopart, oracle and miso policies. Every event
-// of one seed is processed by one warp in lockstep: all 32 lanes execute the (sequential)
-// event logic redundantly -- uniform loads are warp broadcasts, uniform stores are idempotent
-// -- and split only for the data-parallel parts:
-//   * next event: warp argmin over the per-job and per-GPU event slots (below);
-//   * placement (place_dynamic, sim.hpp:581-607): warp argmin over GPUs, with
-//     max_spare_slice_for (topology.hpp:227-252) replaced by a LUT over the roster's min-kind
-//     counts, cached per GPU;
-//   * predictor (finish_profiling, sim.hpp:691-714): one lane per roster column (mt19937_64
-//     seeding + glibc-exact log/cos, predict.cuh), results exchanged by shuffles;
-//   * next event: per-lane register minima over owned slots, one warp argmin per event;
-//   * STP refresh (sim.hpp:353-361): a dense per-job effective-rate array summed sequentially
-//     over the window of arrived, unfinished jobs (bit-exact STP series).
-// The partition search of reopt_and_apply (sim.hpp:716-733) is search.cuh's straight-line
-// search, executed redundantly by all lanes.
-//
-// Event queue: the reference keeps a binary heap with lazy deletion (stale events are popped
-// and skipped, sim.hpp:284-299). Each job has at most one live job-scoped event and each GPU
-// at most one live GPU-scoped event (every push is preceded by an epoch bump), so this engine
-// keeps one slot per job and per GPU holding that live event's (t, prio, seq) key, with `seq`
-// the same global push counter (sim.hpp:280-282); the next event is the minimum live key --
-// the same total order the heap pops. A slot is cleared whenever its epoch is bumped.
+// sim_kernel.cu -- kernel (c)'s host side: workspace sizing and the per-policy launch dispatch.
+// The engine (sim_engine.cuh) is instantiated once per policy in sim_pol_*.cu.
 #include <cuda_runtime.h>
-#include <cstdlib>
 
-#include <cstdint>
+#include <algorithm>
 
-#include "../../include/miso_b200.h"
-#include "internal.h"
-#include "predict.cuh"
-#include "search.cuh"
-#include "sim_types.h"
-
-#ifndef MISO_SIM_PRUNE
-#define MISO_SIM_PRUNE 0  // sim_kernel_prune.cu builds this file again with 1
-#endif
-#if MISO_SIM_PRUNE
-#define MISO_SIM_NS sim_prune
-#else
-#define MISO_SIM_NS sim
-#endif
+#include "sim_engine.cuh"
 
 namespace miso_b200 {
-namespace MISO_SIM_NS {
-
-enum Phase : uint8_t { kQueued = 0, kMps = 1, kCkpt = 2, kRunning = 3, kIdle = 4 };
-enum Mode : uint8_t { kGpuIdle = 0, kGpuMig = 1, kGpuMps = 2, kGpuReconfig = 3 };
-enum EvKind : uint32_t { kEvArrival = 0, kEvMpsEnd = 1, kEvReconfigDone = 2, kEvCkptDone = 3,
-                         kEvCompletion = 4 };
-enum JobFlag : uint8_t { kRunState = 1, kDone = 2, kHasEst = 4, kSpawned = 8 };
-
-constexpr int64_t kNoEvent = INT64_MAX;
-
-struct DJob {
-  double remaining, consumed, rate, base;
-  double truth[5];
-  double est[5];
-  int64_t arrival_us, last_update_us, first_progress_us, completion_us;
-  int64_t acc[5];
-  uint32_t epoch;
-  int16_t gpu;
-  uint8_t phase, slice, mem, min_kind, flags;
-  int8_t qos;
-  int8_t slot;      // optsta slot index on its GPU
-  uint8_t inst;     // JobProfile::instance_count (clones: 1)
-  int16_t clone_k;  // clones: k of "parent#k"; trace jobs: 0
-  int32_t parent;   // clones: parent job index; trace jobs: -1
-  double lbp;       // pruned search: this job's term of Ctx::lb_p while started and unfinished
-};
-
-struct DGpu {
-  double objective, plan_obj;
-  double plan_speed[7];
-  int32_t roster[7];
-  int32_t plan_job[7];
-  uint32_t epoch;
-  uint8_t mode, mps_level, nroster, plan_n, plan_valid;
-  uint8_t part[5], plan_part[5], kind_cnt[5];
-  int8_t spare;
-  uint8_t plan_slice[7];
-  uint8_t nslots;           // optsta: fixed slots of the static partition (sim.hpp:167-170)
-  uint8_t slot_kind[7];
-  int32_t slot_job[7];
-  uint8_t fcnt[5];          // optsta: free slots per kind
-};
-
-static_assert(sizeof(DJob) <= kSimJobBytes, "workspace job stride");
-static_assert(sizeof(DGpu) <= kSimGpuBytes, "workspace gpu stride");
-
-struct Slot {
-  int64_t t;
-  uint64_t pk;  // prio << 62 | seq << 3 | kind
-};
-
-struct Ctx {  // warp-uniform engine state (registers, identical in every lane)
-  DJob* jobs;
-  DGpu* gpus;
-  Slot* slots;          // [J job slots][G gpu slots]
-  int32_t* queue;       // FCFS order (arrival_us, idx), qhead..qtail
-  double* rate_eff;     // [J] rate if progressing and not done, else 0.0 (refresh_stp)
-  double* stp_prefix;   // [J] cached sequential partial sums of rate_eff over the window
-  int stp_cmin;         // smallest job index whose rate_eff changed since the last refresh
-  int stp_lo, n_arrived; // jobs < stp_lo are done; jobs >= n_arrived have not arrived
-  // per-lane minimum of the event slots this lane owns (slot % 32 == lane); lazily rescanned
-  int64_t lmin_t;
-  uint64_t lmin_pk;
-  int lmin_idx;
-  bool lmin_valid;
-  int chunk;            // slots per lane: lane l owns [l*chunk, (l+1)*chunk)
-  int own_lo;           // this lane's chunk start, lane * chunk (per lane)
-  uint8_t* jst;         // [J] SoA job state for warp scans: phase | slice << 3 | done << 6
-  uint32_t* freemask;   // optsta: [5][W] bit g set iff GPU g has a free slot of that kind
-  double* efftruth;     // [5][J]: effective_speed(truth[k], k, mem, qos) per job (static)
-  int64_t* arr_us;      // [J]: arrival_us per job (dense copy for coalesced scans)
-  int W;                // words per freemask row
-  LogRec* log;
-  int64_t log_cap, log_n;
-  int J, G;             // J: job capacity (trace jobs + every possible clone)
-  int J_used;           // trace jobs + clones spawned so far (jobs_.size() in the reference)
-  // admission memo (optsta / nopart): capacity only grows when a slot / GPU is freed, so a
-  // failed admission of the queue head stays failed until cap_gen moves
-  uint32_t cap_gen, fail_gen;
-  int fail_job;
-  int qhead, qtail;
-  int64_t now;
-  uint64_t seq;
-  uint64_t nonce;
-  double stp_cur, stp_integral;
-  int64_t stp_last;
-  int64_t stp_points;
-  double* stp_series;  // optional (t_s, stp) pairs
-  int64_t stp_cap;
-  bool stp_dirty;
-  int repartitions, migrations, mps_sessions, done_count;
-  int64_t first_progress, last_completion;
-  int status;
-  uint64_t processed;
-  // chosen-only best-static search (SimBatch::prune_bound): a lower bound on this run's exact
-  // JCT sum (us) = finished JCTs + (now - arrival) of arrived unfinished jobs + a runtime floor
-  // for every job that has not started (see prune_lb)
-#if MISO_SIM_PRUNE
-  bool prune;
-  int64_t lb_fin, lb_narr, lb_arrsum, lb_unstarted;
-  // started, unfinished jobs: sum of remaining_work / max_speed in seconds, kept as
-  // lb_p - lb_v * now_s with per-job terms (remaining + rate * t_update) / mx and rate / mx
-  double lb_p, lb_v;
-#endif
-  // options
-  const SimParams* p;
-  const int8_t* spare_lut;
-  uint64_t rng_seed;
-  ModelW w;
-};
-
-__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
-
-__device__ __forceinline__ double s_from_us(int64_t us) { return static_cast<double>(us) * 1e-6; }
-__device__ __forceinline__ int64_t us_from_s(double s) {  // llround: half away from zero
-  return static_cast<int64_t>(llround(s * 1e6));
-}
-
-__device__ __forceinline__ bool progressing(uint8_t ph) { return ph == kMps || ph == kRunning; }
-
-__device__ __forceinline__ void sync_jst(Ctx& c, int ji, const DJob& j) {
-  c.jst[ji] = static_cast<uint8_t>(j.phase | (j.slice << 3) | ((j.flags & 2) ? 64 : 0));
-}
-
-__device__ __forceinline__ void fail(Ctx& c, int code) {
-  if (c.status == 0) c.status = code;
-}
-
-// ---- event log (optional) -------------------------------------------------------------
-__device__ __forceinline__ void log_rec(Ctx& c, uint8_t kind, int gpu, int job, uint8_t x,
-                                        uint32_t a, uint32_t b, double v) {
-  if (!c.log) return;
-  if (c.log_n < c.log_cap && lane_id() == 0) {
-    LogRec r;
-    r.t = c.now;
-    r.kind = kind;
-    r.x = x;
-    r.gpu = static_cast<uint16_t>(gpu < 0 ? 0xFFFF : gpu);
-    r.job = job;
-    r.a = a;
-    r.b = b;
-    r.v = v;
-    c.log[c.log_n] = r;
-  }
-  __syncwarp();
-  ++c.log_n;
-}
-
-__device__ __forceinline__ uint32_t pack_part(const uint8_t* p) {
-  return p[0] | (p[1] << 4) | (p[2] << 8) | (p[3] << 12) | (p[4] << 16);
-}
-
-// ---- event slots -----------------------------------------------------------------------
-__device__ __forceinline__ void push_event(Ctx& c, int slot, int64_t t, uint32_t prio,
-                                           uint32_t kind) {
-  Slot s;
-  s.t = t;
-  s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
-  ++c.seq;
-  c.slots[slot] = s;
-  if (static_cast<unsigned>(slot - c.own_lo) < static_cast<unsigned>(c.chunk)) {  // owner lane
-    // keeps its minimum current
-    if (c.lmin_idx == slot) c.lmin_valid = false;
-    else if (c.lmin_valid && (t < c.lmin_t || (t == c.lmin_t && s.pk < c.lmin_pk))) {
-      c.lmin_t = t;
-      c.lmin_pk = s.pk;
-      c.lmin_idx = slot;
-    }
-  }
-}
-
-__device__ __forceinline__ void clear_slot(Ctx& c, int slot) {
-  c.slots[slot].t = kNoEvent;
-  if (c.lmin_idx == slot) c.lmin_valid = false;  // a lane's lmin_idx lies in its own chunk
-}
-
-// Next event = minimum live (t, prio, seq) key. Lane l owns the contiguous slot chunk
-// [l*chunk, (l+1)*chunk) and keeps its minimum in registers (updated on push, invalidated when
-// that slot is cleared or overwritten). Invalid chunks are rescanned by the whole warp (one
-// coalesced load per lane + a warp argmin); the event is then one warp argmin over the 32
-// lane minima.
-__device__ int next_event(Ctx& c, Slot* out) {
-  const int n = c.J + c.G;
-  const int lane = lane_id();
-  unsigned inval = __ballot_sync(0xffffffffu, !c.lmin_valid);
-  while (inval) {
-    const int owner = __ffs(inval) - 1;
-    inval &= inval - 1;
-    const int lo = owner * c.chunk;
-    int hi = lo + c.chunk;
-    if (hi > n) hi = n;
-    int64_t bt = kNoEvent;
-    uint64_t bk = ~0ull;
-    int bi = -1;
-    for (int i = lo + lane; i < hi; i += 32) {
-      const Slot s = c.slots[i];
-      if (s.t < bt || (s.t == bt && s.pk < bk)) {
-        bt = s.t;
-        bk = s.pk;
-        bi = i;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
-      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ot < bt || (ot == bt && ok < bk)) {
-        bt = ot;
-        bk = ok;
-        bi = oi;
-      }
-    }
-    if (lane == owner) {
-      c.lmin_t = bt;
-      c.lmin_pk = bk;
-      c.lmin_idx = bi;
-      c.lmin_valid = true;
-    }
-  }
-  __syncwarp();
-  int64_t bt = c.lmin_t;
-  uint64_t bk = c.lmin_pk;
-  int bi = c.lmin_idx;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
-    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-    if (ot < bt || (ot == bt && ok < bk)) {
-      bt = ot;
-      bk = ok;
-      bi = oi;
-    }
-  }
-  out->t = bt;
-  out->pk = bk;
-  return bt == kNoEvent ? -1 : bi;
-}
-
-// ---- job state ---------------------------------------------------------------------------
-// sim.hpp:319-329
-__device__ void advance_job(Ctx& c, DJob& j) {
-  const int64_t dt = c.now - j.last_update_us;
-  j.last_update_us = c.now;
-  if (dt <= 0 || (j.flags & kDone)) return;
-  j.acc[j.phase] += dt;
-  if (progressing(j.phase)) {
-    const double w = j.rate * s_from_us(dt);
-    j.remaining -= w;
-    j.consumed += w;
-  }
-}
-
-// Pruned best-static search (SimBatch::prune_bound). A job can never run faster than
-// max_speed (every rate is an effective true speed, <= truth[k]), so from any moment it needs
-// at least remaining / max_speed more seconds (migrations only add checkpoint pauses), and a
-// job that has not started needs at least base / max_speed (completions are scheduled
-// llround(remaining / rate * 1e6) us ahead: rounded down with margin).
-__device__ __forceinline__ double max_speed(const DJob& j) {  // >= any rate the job can get
-  double mx = 1.0;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) mx = j.truth[k] > mx ? j.truth[k] : mx;
-  return mx;
-}
-__device__ __forceinline__ int64_t runtime_floor_us(const DJob& j) {
-  const double us = j.base / max_speed(j) * 1e6 * (1.0 - 1e-12) - 2.0;
-  return us > 0.0 ? static_cast<int64_t>(us) : 0;
-}
-
-// sim.hpp:333-343 (+ slot invalidation: every epoch bump retires the job's pending event)
-__device__ void set_phase(Ctx& c, int ji, uint8_t phase, double rate) {
-  DJob& j = c.jobs[ji];
-  advance_job(c, j);
-#if MISO_SIM_PRUNE
-  if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // retire the old-rate term
-    c.lb_p -= j.lbp;
-    c.lb_v -= j.rate / max_speed(j);
-  }
-#endif
-  j.phase = phase;
-  j.rate = progressing(phase) ? rate : 0.0;
-  ++j.epoch;
-  clear_slot(c, ji);
-  if (progressing(phase)) {
-    j.flags |= kRunState;
-    if (j.first_progress_us < 0) j.first_progress_us = c.now;
-    if (c.first_progress < 0) c.first_progress = c.now;
-  }
-  // the STP window's sums only need redoing from ji if the job's term actually changed
-  const double re = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
-  if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
-    c.rate_eff[ji] = re;
-    c.stp_dirty = true;
-    if (ji < c.stp_cmin) c.stp_cmin = ji;
-  }
-  sync_jst(c, ji, j);
-#if MISO_SIM_PRUNE
-  if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // remaining / mx, from now
-    const double mx = max_speed(j);
-    j.lbp = (j.remaining + j.rate * s_from_us(c.now)) / mx;
-    c.lb_p += j.lbp;
-    c.lb_v += j.rate / mx;
-  }
-#endif
-}
-
-// sim.hpp:345-351
-__device__ void schedule_completion(Ctx& c, int ji) {
-  DJob& j = c.jobs[ji];
-  if ((j.flags & kDone) || !(j.rate > 0)) return;
-  const double dt_s = (j.remaining > 0.0 ? j.remaining : 0.0) / j.rate;  // std::max(0.0, r)
-  int64_t dt = us_from_s(dt_s);
-  if (dt < 0) dt = 0;
-  push_event(c, ji, c.now + dt, 0, kEvCompletion);
-}
-
-// sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). Only
-// jobs in [stp_lo, n_arrived) can progress; rate_eff holds 0.0 for the others, and s + 0.0 == s
-// for the non-negative partial sums, so the sequential FP64 sum over that window is
-// bit-identical to the reference's loop over all jobs. Partial sums are cached per index and
-// the chain restarts at the smallest index changed since the previous refresh.
-__device__ void refresh_stp(Ctx& c) {
-  if (!c.stp_dirty || !c.p->track_stp) return;
-  c.stp_dirty = false;
-  const double* r = c.rate_eff;
-  double* P = c.stp_prefix;  // P[q]: the sum through index 8q + 7, cached at block ends
-  const int lo = c.stp_lo, hi = c.n_arrived;
-  int i0 = c.stp_cmin > lo ? c.stp_cmin : lo;
-  if (i0 > hi) i0 = hi;  // changes at not-yet-arrived indices: the window's sum is unchanged
-  c.stp_cmin = INT32_MAX;
-  // restart at i0's 8-aligned block from the cached sum before it: the block's terms below i0
-  // are unchanged, so re-adding them reproduces the same partial sums (and jobs below lo are
-  // done, contributing +0.0, so a start below lo is exact too)
-  int i = i0 & ~7;
-  double s = (i > 0 && i - 1 >= lo) ? P[(i >> 3) - 1] : 0.0;
-  for (; i + 8 <= hi; i += 8) {  // 64-byte aligned: four 16-byte loads per block
-    const double2* r2 = reinterpret_cast<const double2*>(r + i);
-    const double2 a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
-    s = s + a01.x;
-    s = s + a01.y;
-    s = s + a23.x;
-    s = s + a23.y;
-    s = s + a45.x;
-    s = s + a45.y;
-    s = s + a67.x;
-    s = s + a67.y;
-    if (lane_id() == 0) P[i >> 3] = s;
-  }
-  for (; i < hi; ++i) s = s + r[i];
-  __syncwarp();
-  if (hi <= lo) s = 0.0;
-  if (s != c.stp_cur) {
-    c.stp_cur = s;
-    if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
-      c.stp_series[2 * c.stp_points] = s_from_us(c.now);
-      c.stp_series[2 * c.stp_points + 1] = s;
-    }
-    __syncwarp();
-    ++c.stp_points;
-  }
-}
-
-__device__ __forceinline__ double true_rate(const DJob& j, int k) {
-  return effective_speed(j.truth[k], k, j.mem, j.qos);
-}
-__device__ __forceinline__ double est_rate(const DJob& j, int k) {
-  return effective_speed(j.est[k], k, j.mem, j.qos);
-}
-
-// ---- queue (std::set ordered by (arrival_us, entry_seq == idx)) -------------------------
-__device__ void enqueue(Ctx& c, int ji) {
-  const int64_t a = c.jobs[ji].arrival_us;
-  int pos = c.qtail;
-  while (pos > c.qhead) {  // sorted insert; arrivals append at the tail
-    const int prev = c.queue[pos - 1];
-    const int64_t pa = c.jobs[prev].arrival_us;
-    if (pa < a || (pa == a && prev < ji)) break;
-    __syncwarp();
-    c.queue[pos] = prev;
-    __syncwarp();
-    --pos;
-  }
-  c.queue[pos] = ji;
-  __syncwarp();
-  ++c.qtail;
-}
-
-// ---- GPU roster helpers -----------------------------------------------------------------
-__device__ __forceinline__ int lut_index(const uint8_t* k) {
-  return (((k[0] * 7 + k[1]) * 7 + k[2]) * 7 + k[3]) * 7 + k[4];
-}
-
-__device__ void roster_push(Ctx& c, DGpu& g, int ji) {
-  g.roster[g.nroster] = ji;
-  __syncwarp();
-  ++g.nroster;
-  ++g.kind_cnt[c.jobs[ji].min_kind];
-  g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
-}
-
-__device__ void roster_erase(Ctx& c, DGpu& g, int ji) {
-  int i = 0;
-  while (i < g.nroster && g.roster[i] != ji) ++i;
-  for (int k = i; k + 1 < g.nroster; ++k) {
-    const int v = g.roster[k + 1];
-    __syncwarp();
-    g.roster[k] = v;
-    __syncwarp();
-  }
-  --g.nroster;
-  --g.kind_cnt[c.jobs[ji].min_kind];
-  g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
-}
-
-// ---- forward declarations of the mutually recursive steps ---------------------------------
-__device__ __noinline__ void reopt_and_apply(Ctx& c, int gi, bool force);
-__device__ void finish_profiling(Ctx& c, int gi);
-
-// sim.hpp:480-489
-__device__ void start_running(Ctx& c, int ji, int s) {
-  DJob& j = c.jobs[ji];
-#if MISO_SIM_PRUNE
-  if (c.prune && j.first_progress_us < 0) c.lb_unstarted -= runtime_floor_us(j);
-#endif
-  const double r = c.efftruth[size_t(s) * c.J + ji];  // == true_rate(j, s)
-  if (c.p->check_invariants && !(r > 0)) fail(c, MISO_B200_SIM_INFEASIBLE_SLICE);
-  j.slice = static_cast<uint8_t>(s);
-  set_phase(c, ji, kRunning, r);  // also syncs jst
-  schedule_completion(c, ji);
-  log_rec(c, kLogStart, j.gpu, ji, static_cast<uint8_t>(s), 0, 0, r);
-}
-
-// sim.hpp:432-455: a multi-instance job's clones are appended at its first admission (nopart,
-// optsta) or estimate caching (miso, oracle): copies of the profile ("parent#k"), the parent's
-// arrival as FCFS position and JCT baseline, the parent's estimates, queued in FCFS order
-// (arrival_us, index == entry_seq). The STP window grows to the clone's index; jobs in between
-// that have not arrived yet contribute +0.0 (exact).
-__device__ void spawn_instances(Ctx& c, int pi) {
-  DJob& par = c.jobs[pi];
-  if ((par.flags & kSpawned) || par.inst <= 1) return;
-  par.flags |= kSpawned;
-  for (int k = 1; k < par.inst; ++k) {
-    const int ci = c.J_used;
-    if (ci >= c.J) {  // capacity is the trace's instance total; cannot happen
-      fail(c, MISO_B200_SIM_INVARIANT);
-      return;
-    }
-    DJob& j = c.jobs[ci];
-    j.base = par.base;
-    j.remaining = par.base;
-    j.consumed = 0;
-    j.rate = 0;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-      j.truth[q] = par.truth[q];
-      j.est[q] = par.est[q];
-      j.acc[q] = 0;
-    }
-    j.arrival_us = par.arrival_us;
-    j.last_update_us = par.arrival_us;
-    j.first_progress_us = -1;
-    j.completion_us = -1;
-    j.epoch = 0;
-    j.gpu = -1;
-    j.phase = kQueued;
-    j.slice = 4;
-    j.mem = par.mem;
-    j.min_kind = par.min_kind;
-    j.qos = par.qos;
-    j.flags = static_cast<uint8_t>((par.flags & kHasEst) | kSpawned);
-    j.slot = -1;
-    j.inst = 1;
-    j.clone_k = static_cast<int16_t>(k);
-    j.parent = pi;
-#pragma unroll
-    for (int q = 0; q < 5; ++q) c.efftruth[size_t(q) * c.J + ci] = c.efftruth[size_t(q) * c.J + pi];
-    c.arr_us[ci] = par.arrival_us;
-    __syncwarp();
-    c.J_used = ci + 1;
-    sync_jst(c, ci, j);
-    if (ci + 1 > c.n_arrived) {
-      if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;
-      c.n_arrived = ci + 1;
-    }
-    log_rec(c, kLogSpawn, -1, ci, 0, static_cast<uint32_t>(pi), 0, 0);
-    enqueue(c, ci);
-  }
-}
-
-// sim.hpp:457-461
-__device__ void cache_estimates(Ctx& c, int ji, const double* est) {
-  DJob& j = c.jobs[ji];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) j.est[k] = est[k];
-  j.flags |= kHasEst;
-  spawn_instances(c, ji);
-}
-
-// sim.hpp:670-680 with simulate_mps_rates / interp_speed (profiles.hpp:391-431)
-__device__ void rate_roster_mps(Ctx& c, int gi, int level) {
-  DGpu& g = c.gpus[gi];
-  const int n = g.nroster;
-  double share = static_cast<double>(level);
-  const double eq = 100.0 / static_cast<double>(n);
-  if (eq < share) share = eq;  // std::min(level, 100/n)
-  const double gpc = clampd(share / 100.0 * 7.0, 1.0, 7.0);
-  for (int i = 0; i < n; ++i) {
-    const int ji = g.roster[i];
-    const DJob& j = c.jobs[ji];
-    double sp;
-    if (gpc <= 1.0) {
-      sp = j.truth[0];
-    } else if (gpc >= 7.0) {
-      sp = j.truth[4];
-    } else {
-      const double knots[5] = {1, 2, 3, 4, 7};
-      int k = 1;
-      while (!(gpc <= knots[k])) ++k;
-      const double wgt = (gpc - knots[k - 1]) / (knots[k] - knots[k - 1]);
-      sp = j.truth[k - 1] + wgt * (j.truth[k] - j.truth[k - 1]);
-    }
-    const double rate = clampd(c.p->interference * sp, kSpeedFloor, 1.0);
-    set_phase(c, ji, kMps, rate);
-    schedule_completion(c, ji);
-  }
-}
-
-// sim.hpp:660-666
-__device__ void start_mps_window(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  const int level = g.mps_level == 0 ? 100 : (g.mps_level == 1 ? 50 : 14);  // kMpsLevels
-  rate_roster_mps(c, gi, level);
-  ++g.epoch;
-  push_event(c, c.J + gi, c.now + c.p->window_us, 2, kEvMpsEnd);
-  log_rec(c, kLogMpsWindow, gi, -1, 0, static_cast<uint32_t>(level), 0, 0);
-}
-
-// sim.hpp:654-658
-__device__ void begin_mps_windows(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  g.mps_level = 0;
-  log_rec(c, kLogMpsStart, gi, -1, 0, g.nroster, 0, 0);
-  start_mps_window(c, gi);
-}
-
-// sim.hpp:625-652
-__device__ void start_profiling_session(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  g.mode = kGpuMps;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) g.part[k] = 0;
-  g.objective = 0;
-  if (c.p->window_us == 0) {
-    finish_profiling(c, gi);
-    return;
-  }
-  ++c.mps_sessions;
-  bool need_ckpt = false;
-  if (c.p->ckpt_us > 0)
-    for (int i = 0; i < g.nroster; ++i)
-      if (c.jobs[g.roster[i]].flags & kRunState) need_ckpt = true;
-  if (need_ckpt) {
-    for (int i = 0; i < g.nroster; ++i) {
-      const int ji = g.roster[i];
-      set_phase(c, ji, (c.jobs[ji].flags & kRunState) ? kCkpt : kQueued, 0.0);
-    }
-    ++g.epoch;
-    push_event(c, c.J + gi, c.now + c.p->ckpt_us, 2, kEvCkptDone);
-    log_rec(c, kLogCkptStart, gi, -1, 0, g.nroster, 0, 0);
-  } else {
-    begin_mps_windows(c, gi);
-  }
-}
-
-// sim.hpp:691-714. Noisy mode: lane c predicts roster column c (predict_mig_speeds with call
-// nonce ++predictor_nonce_, then extrapolate_small_slices); columns are exchanged by shuffles.
-__device__ void finish_profiling(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  const int n = g.nroster;
-  if (!c.p->noisy) {
-    for (int i = 0; i < n; ++i) {
-      const int ji = g.roster[i];
-      cache_estimates(c, ji, c.jobs[ji].truth);
-    }
-  } else {
-    const uint64_t nonce = ++c.nonce;
-    double e[5] = {0, 0, 0, 0, 0};
-    const int ln = lane_id();
-    if (ln < n) {
-      const DJob& j = c.jobs[g.roster[ln]];
-      predict_column(j.truth[4], j.truth[3], j.truth[2], ln, c.rng_seed, nonce, true,
-                     c.p->target_mae, c.w, e);
-    }
-    __syncwarp();  // reconverge before the column exchange
-    for (int i = 0; i < n; ++i) {
-      double ei[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) ei[k] = __shfl_sync(0xffffffffu, e[k], i);
-      cache_estimates(c, g.roster[i], ei);
-    }
-  }
-  reopt_and_apply(c, gi, true);
-}
-
-// sim.hpp:765-794
-__device__ void apply_assignment(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  if (!g.plan_valid) {
-    fail(c, MISO_B200_SIM_INVARIANT);
-    return;
-  }
-  g.plan_valid = 0;
-  if (g.plan_n != g.nroster) {
-    fail(c, MISO_B200_SIM_INVARIANT);
-    return;
-  }
-#pragma unroll
-  for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k];
-  g.objective = g.plan_obj;
-  g.mode = kGpuMig;
-  int cnt = 0;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) cnt += g.plan_part[k];
-  if (c.p->check_invariants && cnt != g.nroster) fail(c, MISO_B200_SIM_INVARIANT);
-  for (int i = 0; i < g.nroster; ++i)
-    if (g.plan_job[i] != g.roster[i]) fail(c, MISO_B200_SIM_INVARIANT);
-  log_rec(c, kLogPartition, gi, -1, static_cast<uint8_t>(g.nroster), pack_part(g.part), 0, 0);
-  for (int i = 0; i < g.nroster; ++i)
-    log_rec(c, kLogAssign, gi, g.roster[i], g.plan_slice[i], 0, 0, 0);
-  for (int i = 0; i < g.nroster; ++i) {
-    const int ji = g.roster[i];
-    const DJob& j = c.jobs[ji];
-    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-    start_running(c, ji, g.plan_slice[i]);
-  }
-}
-
-// sim.hpp:739-763
-__device__ void begin_reconfig(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  bool any = false, restart = false;
-  for (int i = 0; i < g.nroster; ++i) {
-    const DJob& j = c.jobs[g.roster[i]];
-    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-    any = true;
-    if (j.flags & kRunState) restart = true;
-  }
-  const int64_t pause = c.p->reconfig_us + (restart ? c.p->ckpt_us : 0);
-  g.plan_valid = 1;
-  if (!any || pause == 0) {
-    apply_assignment(c, gi);
-    return;
-  }
-  g.mode = kGpuReconfig;
-  for (int i = 0; i < g.nroster; ++i) {
-    const int ji = g.roster[i];
-    const DJob& j = c.jobs[ji];
-    if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-    set_phase(c, ji, (j.flags & kRunState) ? kCkpt : kQueued, 0.0);
-  }
-  ++g.epoch;
-  push_event(c, c.J + gi, c.now + pause, 2, kEvReconfigDone);
-  log_rec(c, kLogReconfigStart, gi, -1, 0, static_cast<uint32_t>(pause & 0xFFFFFFFF),
-          static_cast<uint32_t>(pause >> 32), 0);
-}
-
-// sim.hpp:716-733
-__device__ __noinline__ void reopt_and_apply(Ctx& c, int gi, bool force) {
-  DGpu& g = c.gpus[gi];
-  const int m = g.nroster;
-  double rows[7 * 5];
-  for (int i = 0; i < m; ++i) {
-    const DJob& j = c.jobs[g.roster[i]];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) rows[i * 5 + k] = est_rate(j, k);
-  }
-  double obj = 0.0;
-  const uint8_t cand = search_any<false>(rows, m, c.p->en0, c.p->en1, &obj);
-  if (cand >= kNumCands) {  // nullopt (or m out of range): SimInvariantError
-    fail(c, MISO_B200_SIM_NO_PARTITION);
-    return;
-  }
-  if (!force && !(obj > g.objective + 1e-12)) return;
-  ++c.repartitions;
-  g.plan_obj = obj;
-  g.plan_n = static_cast<uint8_t>(m);
-#pragma unroll
-  for (int k = 0; k < 5; ++k) g.plan_part[k] = 0;
-  for (int i = 0; i < m; ++i) {
-    const int s = kCandPlaceD[cand][i];
-    g.plan_slice[i] = static_cast<uint8_t>(s);
-    g.plan_job[i] = g.roster[i];
-    g.plan_speed[i] = rows[i * 5 + s];
-    ++g.plan_part[s];
-  }
-  begin_reconfig(c, gi);
-}
-
-// sim.hpp:612-623
-__device__ void settle_admissions(Ctx& c, int gi) {
-  DGpu& g = c.gpus[gi];
-  if (c.p->policy == MISO_B200_POLICY_ORACLE)
-    for (int i = 0; i < g.nroster; ++i) {
-      const int ji = g.roster[i];
-      if (!(c.jobs[ji].flags & kHasEst)) cache_estimates(c, ji, c.jobs[ji].truth);
-    }
-  bool all_est = true;
-  for (int i = 0; i < g.nroster; ++i) all_est = all_est && (c.jobs[g.roster[i]].flags & kHasEst);
-  if (all_est) reopt_and_apply(c, gi, true);
-  else start_profiling_session(c, gi);
-}
-
-// sim.hpp:581-607: least-loaded GPU whose spare slice covers the job's minimum (ties: id)
-__device__ int place_dynamic(Ctx& c, int ji) {
-  const int need = c.jobs[ji].min_kind;
-  int best = -1, best_cnt = 8;
-  for (int gi = lane_id(); gi < c.G; gi += 32) {
-    const DGpu& g = c.gpus[gi];
-    if (g.mode != kGpuIdle && g.mode != kGpuMig) continue;
-    if (g.nroster >= 7) continue;
-    if (g.nroster > 0 && (g.spare < 0 || g.spare < need)) continue;
-    if (g.nroster < best_cnt) {
-      best = gi;
-      best_cnt = g.nroster;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const int ob = __shfl_xor_sync(0xffffffffu, best, off);
-    const int oc = __shfl_xor_sync(0xffffffffu, best_cnt, off);
-    if (ob >= 0 && (best < 0 || oc < best_cnt || (oc == best_cnt && ob < best))) {
-      best = ob;
-      best_cnt = oc;
-    }
-  }
-  if (best < 0) return -1;
-  ++c.qhead;  // pop_queue: the placed job is always the queue head
-  DGpu& g = c.gpus[best];
-  roster_push(c, g, ji);
-  c.jobs[ji].gpu = static_cast<int16_t>(best);
-  log_rec(c, kLogAdmit, best, ji, 0, 0, 0, 0);
-  return best;
-}
-
-// optsta free-slot bookkeeping: per GPU and kind a free count, per kind a GPU bitmask.
-__device__ __forceinline__ void occupy_slot(Ctx& c, int gi, int i, int ji) {
-  DGpu& g = c.gpus[gi];
-  const int k = g.slot_kind[i];
-  g.slot_job[i] = ji;
-  if (--g.fcnt[k] == 0) {
-    uint32_t* w = c.freemask + k * c.W + (gi >> 5);
-    const uint32_t v = *w & ~(1u << (gi & 31));
-    __syncwarp();
-    *w = v;
-  }
-}
-
-__device__ __forceinline__ void free_slot(Ctx& c, int gi, int i) {
-  ++c.cap_gen;
-  DGpu& g = c.gpus[gi];
-  const int k = g.slot_kind[i];
-  g.slot_job[i] = -1;
-  if (g.fcnt[k]++ == 0) {
-    uint32_t* w = c.freemask + k * c.W + (gi >> 5);
-    const uint32_t v = *w | (1u << (gi & 31));
-    __syncwarp();
-    *w = v;
-  }
-}
-
-// sim.hpp:495-520: the largest free slot the job can use, ties to the first (gpu, slot). Kinds
-// have distinct GPC counts, so this is: the largest feasible kind with a free slot anywhere,
-// on the lowest-numbered GPU having one, at that GPU's first free slot of the kind.
-__device__ bool admit_optsta(Ctx& c, int ji) {
-  if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // nothing freed since
-  int bg = -1, bk = -1;
-  for (int k = 4; k >= 0 && bg < 0; --k) {
-    if (!(c.efftruth[size_t(k) * c.J + ji] > 0)) continue;  // == true_rate(j, k)
-    for (int w0 = 0; w0 < c.W && bg < 0; w0 += 32) {
-      const int wi = w0 + lane_id();
-      const uint32_t word = wi < c.W ? c.freemask[k * c.W + wi] : 0u;
-      const unsigned nz = __ballot_sync(0xffffffffu, word != 0);
-      if (nz) {
-        const int l = __ffs(nz) - 1;
-        const uint32_t wv = __shfl_sync(0xffffffffu, word, l);
-        bg = ((w0 + l) << 5) + __ffs(wv) - 1;
-        bk = k;
-      }
-    }
-  }
-  if (bg < 0) {
-    c.fail_job = ji;
-    c.fail_gen = c.cap_gen;
-    return false;
-  }
-  DGpu& g = c.gpus[bg];
-  int bi = 0;
-  while (!(g.slot_kind[bi] == bk && g.slot_job[bi] == -1)) ++bi;
-  ++c.qhead;
-  occupy_slot(c, bg, bi, ji);
-  roster_push(c, g, ji);
-  DJob& jm = c.jobs[ji];
-  jm.gpu = static_cast<int16_t>(bg);
-  jm.slot = static_cast<int8_t>(bi);
-  log_rec(c, kLogAdmitSlot, bg, ji, static_cast<uint8_t>(bi), 0, 0, 0);
-  start_running(c, ji, g.slot_kind[bi]);
-  spawn_instances(c, ji);
-  return true;
-}
-
-// sim.hpp:465-478
-__device__ bool admit_nopart(Ctx& c, int ji) {
-  if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // no GPU went idle since
-  int best = -1;
-  for (int gi = lane_id(); gi < c.G; gi += 32)
-    if (c.gpus[gi].mode == kGpuIdle) {
-      best = gi;
-      break;
-    }
-  const unsigned any = __ballot_sync(0xffffffffu, best >= 0);
-  if (!any) {
-    c.fail_job = ji;
-    c.fail_gen = c.cap_gen;
-    return false;
-  }
-  // lowest id among lanes' first idle GPUs
-  int b = best >= 0 ? best : INT32_MAX;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, off));
-  ++c.qhead;
-  DGpu& g = c.gpus[b];
-  g.mode = kGpuMig;
-  roster_push(c, g, ji);
-  c.jobs[ji].gpu = static_cast<int16_t>(b);
-  log_rec(c, kLogAdmit, b, ji, 0, 0, 0, 0);
-  start_running(c, ji, 4);
-  spawn_instances(c, ji);
-  return true;
-}
-
-// sim.hpp:398-418
-__device__ void drain_queue(Ctx& c) {
-  if (c.p->policy == MISO_B200_POLICY_NOPART) {
-    while (c.qhead < c.qtail && c.status == 0)
-      if (!admit_nopart(c, c.queue[c.qhead])) break;
-    return;
-  }
-  if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
-    while (c.qhead < c.qtail && c.status == 0)
-      if (!admit_optsta(c, c.queue[c.qhead])) break;
-    return;
-  }
-  for (;;) {
-    int touched[32];
-    int nt = 0;
-    while (c.qhead < c.qtail && c.status == 0) {
-      const int gi = place_dynamic(c, c.queue[c.qhead]);
-      if (gi < 0) break;
-      bool seen = false;
-      for (int i = 0; i < nt; ++i) seen = seen || touched[i] == gi;
-      if (!seen) {
-        if (nt == 32) {  // flush early (rare: > 32 GPUs touched at one instant)
-          for (int i = 0; i < nt; ++i) settle_admissions(c, touched[i]);
-          nt = 0;
-        }
-        touched[nt++] = gi;
-      }
-    }
-    if (nt == 0) return;
-    for (int i = 0; i < nt && c.status == 0; ++i) settle_admissions(c, touched[i]);
-  }
-}
-
-// sim.hpp:837-890
-__device__ void complete_dynamic(Ctx& c, int gi, int ji) {
-  DGpu& g = c.gpus[gi];
-  const DJob& j = c.jobs[ji];
-  if (g.mode == kGpuMps) {
-    if (g.nroster == 0) {
-      ++g.epoch;
-      clear_slot(c, c.J + gi);
-      g.mode = kGpuIdle;
-      return;
-    }
-    const int lv = g.mps_level == 0 ? 100 : (g.mps_level == 1 ? 50 : 14);
-    rate_roster_mps(c, gi, lv);
-    return;
-  }
-  if (g.mode == kGpuReconfig) {
-    for (int i = 0; i < g.plan_n; ++i) {
-      if (g.plan_job[i] != ji) continue;
-      g.plan_obj -= g.plan_speed[i];
-      --g.plan_part[g.plan_slice[i]];
-      for (int k = i; k + 1 < g.plan_n; ++k) {
-        g.plan_job[k] = g.plan_job[k + 1];
-        g.plan_slice[k] = g.plan_slice[k + 1];
-        g.plan_speed[k] = g.plan_speed[k + 1];
-        __syncwarp();
-      }
-      --g.plan_n;
-      break;
-    }
-    if (g.part[j.slice] == 0) fail(c, MISO_B200_SIM_INVARIANT);
-    else --g.part[j.slice];
-    log_rec(c, kLogShrink, gi, -1, 0, pack_part(g.part), 0, 0);
-    return;
-  }
-  if (g.part[j.slice] == 0) fail(c, MISO_B200_SIM_INVARIANT);
-  else --g.part[j.slice];
-  if (g.nroster == 0) {
-    g.mode = kGpuIdle;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) g.part[k] = 0;
-    g.objective = 0;
-    return;
-  }
-  log_rec(c, kLogShrink, gi, -1, 0, pack_part(g.part), 0, 0);
-  double obj = 0;
-  for (int i = 0; i < g.nroster; ++i) {
-    const DJob& r = c.jobs[g.roster[i]];
-    obj += est_rate(r, r.slice);
-  }
-  g.objective = obj;
-  if (c.p->drift_threshold > 0 && c.p->policy == MISO_B200_POLICY_MISO && c.p->window_us > 0) {
-    for (int i = 0; i < g.nroster; ++i) {
-      const DJob& r = c.jobs[g.roster[i]];
-      const double est = est_rate(r, r.slice);
-      const double truth = true_rate(r, r.slice);
-      if (est > 0 && fabs(truth - est) / est > c.p->drift_threshold) {
-        start_profiling_session(c, gi);
-        return;
-      }
-    }
-  }
-  reopt_and_apply(c, gi, false);
-}
-
-// sim.hpp:526-572: one migration per freed slot -- the running job with the largest strictly
-// positive true-speed gain on a strictly larger slot kind (ties: earliest arrival, then entry
-// order) moves in and checkpoint-restarts; its old slot joins the worklist. The job scan is a
-// warp argmin over the window of arrived, unfinished jobs.
-__device__ void process_freed_slots(Ctx& c, int gi0, int si0) {
-  int wl_g[64], wl_s[64];
-  int nw = 1;
-  wl_g[0] = gi0;
-  wl_s[0] = si0;
-  while (nw > 0 && c.status == 0) {
-    --nw;
-    const int gi = wl_g[nw], si = wl_s[nw];
-    drain_queue(c);
-    DGpu& g = c.gpus[gi];
-    if (g.slot_job[si] != -1) continue;
-    const int kind = g.slot_kind[si];
-    const int kg = kind_gpc(kind);
-    int best = -1;
-    double bgain = 0.0;
-    int64_t barr = 0;
-    const double* eff_k = c.efftruth + size_t(kind) * c.J;
-    for (int mi = c.stp_lo + lane_id(); mi < c.n_arrived; mi += 32) {
-      // dense arrays only (coalesced): state byte, effective true speed on `kind`, the
-      // running rate (rate_eff == rate for a running job), arrival time
-      const uint8_t st = c.jst[mi];
-      if ((st & 64) || (st & 7) != kRunning) continue;
-      if (kind_gpc((st >> 3) & 7) >= kg) continue;
-      const double ns = eff_k[mi];
-      if (!(ns > 0)) continue;
-      const double gain = ns - c.rate_eff[mi];
-      if (gain <= 0) continue;
-      const int64_t arr = c.arr_us[mi];
-      if (best < 0 || gain > bgain || (gain == bgain && (arr < barr || (arr == barr && mi < best)))) {
-        best = mi;
-        bgain = gain;
-        barr = arr;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int ob = __shfl_xor_sync(0xffffffffu, best, off);
-      const double og = __shfl_xor_sync(0xffffffffu, bgain, off);
-      const int64_t oa = __shfl_xor_sync(0xffffffffu, barr, off);
-      if (ob >= 0 && (best < 0 || og > bgain ||
-                      (og == bgain && (oa < barr || (oa == barr && ob < best))))) {
-        best = ob;
-        bgain = og;
-        barr = oa;
-      }
-    }
-    if (best < 0) continue;
-    DJob& m = c.jobs[best];
-    DGpu& og = c.gpus[m.gpu];
-    free_slot(c, m.gpu, m.slot);
-    if (nw == 64) {
-      fail(c, MISO_B200_SIM_INVARIANT);
-      return;
-    }
-    wl_g[nw] = m.gpu;
-    wl_s[nw] = m.slot;
-    ++nw;
-    roster_erase(c, og, best);
-    roster_push(c, g, best);
-    occupy_slot(c, gi, si, best);
-    m.gpu = static_cast<int16_t>(gi);
-    m.slot = static_cast<int8_t>(si);
-    m.slice = static_cast<uint8_t>(kind);
-    sync_jst(c, best, m);
-    ++c.migrations;
-    log_rec(c, kLogMigrate, gi, best, static_cast<uint8_t>(kind), static_cast<uint32_t>(si), 0, 0);
-    if (c.p->ckpt_us > 0) {
-      set_phase(c, best, kCkpt, 0.0);
-      push_event(c, best, c.now + c.p->ckpt_us, 2, kEvCkptDone);
-    } else {
-      start_running(c, best, m.slice);
-    }
-  }
-}
-
-// sim.hpp:798-835
-__device__ void on_completion(Ctx& c, int ji) {
-  DJob& j = c.jobs[ji];
-#if MISO_SIM_PRUNE
-  if (c.prune) {  // the job's remaining-work term leaves with it
-    c.lb_p -= j.lbp;
-    c.lb_v -= j.rate / max_speed(j);
-  }
-#endif
-  advance_job(c, j);
-  if (c.p->check_invariants) {
-    const double base = j.base;
-    if (fabs(j.consumed - base) > 1e-6 * base + 1e-9) fail(c, MISO_B200_SIM_INVARIANT);
-  }
-  j.remaining = 0;
-  j.flags |= kDone;
-  ++j.epoch;
-  clear_slot(c, ji);
-  c.rate_eff[ji] = 0.0;
-  c.stp_dirty = true;
-  if (ji < c.stp_cmin) c.stp_cmin = ji;
-  sync_jst(c, ji, j);
-  while (c.stp_lo < c.n_arrived && (c.jst[c.stp_lo] & 64)) ++c.stp_lo;  // done bit, dense
-  j.completion_us = c.now;
-  ++c.done_count;
-  if (c.now > c.last_completion) c.last_completion = c.now;
-  if (c.p->check_invariants) {
-    int64_t total = 0;
-#pragma unroll
-    for (int b = 0; b < 5; ++b) total += j.acc[b];
-    if (total != c.now - j.arrival_us) fail(c, MISO_B200_SIM_INVARIANT);
-  }
-  const int64_t jct = c.now - j.arrival_us;
-#if MISO_SIM_PRUNE
-  if (c.prune) {
-    c.lb_fin += jct;
-    --c.lb_narr;
-    c.lb_arrsum -= j.arrival_us;
-  }
-#endif
-  log_rec(c, kLogComplete, -1, ji, 0, static_cast<uint32_t>(jct & 0xFFFFFFFF),
-          static_cast<uint32_t>(jct >> 32), 0);
-  const int gi = j.gpu;
-  DGpu& g = c.gpus[gi];
-  roster_erase(c, g, ji);
-  if (c.p->policy == MISO_B200_POLICY_NOPART) {
-    g.mode = kGpuIdle;
-    ++c.cap_gen;
-    return;
-  }
-  if (c.p->policy == MISO_B200_POLICY_OPTSTA) {
-    free_slot(c, gi, j.slot);
-    process_freed_slots(c, gi, j.slot);
-    return;
-  }
-  complete_dynamic(c, gi, ji);
-}
-
-// sim.hpp:301-313
-__device__ void dispatch(Ctx& c, int slot, uint32_t kind) {
-  if (slot < c.J) {
-    const int ji = slot;
-    if (kind == kEvArrival) {
-      if (ji + 1 > c.n_arrived) {
-        if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;  // new window entries need sums
-        c.n_arrived = ji + 1;
-      }
-      log_rec(c, kLogArrival, -1, ji, 0, 0, 0, 0);
-#if MISO_SIM_PRUNE
-      if (c.prune) {
-        ++c.lb_narr;
-        c.lb_arrsum += c.now;  // == arrival_us
-      }
-#endif
-      enqueue(c, ji);
-    } else if (kind == kEvCompletion) {
-      on_completion(c, ji);
-    } else if (kind == kEvCkptDone) {  // on_migration_restart, sim.hpp:574
-      start_running(c, ji, c.jobs[ji].slice);
-    }
-    return;
-  }
-  const int gi = slot - c.J;
-  DGpu& g = c.gpus[gi];
-  if (kind == kEvMpsEnd) {  // on_mps_phase_end, sim.hpp:682-689
-    if (++g.mps_level < 3) {
-      start_mps_window(c, gi);
-    } else {
-      log_rec(c, kLogMpsEnd, gi, -1, 0, 0, 0, 0);
-      finish_profiling(c, gi);
-    }
-  } else if (kind == kEvReconfigDone) {
-    apply_assignment(c, gi);
-  } else if (kind == kEvCkptDone) {
-    begin_mps_windows(c, gi);
-  }
-}
-
-// One warp per seed.
-#ifndef MISO_SIM_MIN_BLOCKS
-#define MISO_SIM_MIN_BLOCKS 8
-#endif
-__global__ void __launch_bounds__(128, MISO_SIM_MIN_BLOCKS) simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
-  const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  if (warp >= b.n_seeds) return;
-  const int lane = lane_id();
-  const int tr = b.task_trace ? b.task_trace[warp] : warp;  // task -> trace
-  const int J0 = b.job_offsets[tr];
-  const int JT = b.job_offsets[tr + 1] - J0;  // trace jobs
-  // capacity: every job's instance_count (sim.hpp:242); clones occupy [JT, J)
-  int extra = 0;
-  if (b.instances)
-    for (int i = lane_id(); i < JT; i += 32) extra += b.instances[J0 + i] > 1 ? b.instances[J0 + i] - 1 : 0;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) extra += __shfl_xor_sync(0xffffffffu, extra, off);
-  const int J = JT + extra;
-  const int G = prm.cluster_size;
-  unsigned char* ws = b.workspace + size_t(warp) * b.ws_stride;
-  Ctx c;
-  c.jobs = reinterpret_cast<DJob*>(ws);  // stride kSimJobBytes == sizeof rounded (asserted)
-  c.gpus = reinterpret_cast<DGpu*>(ws + sim_ws_gpus_off(b.max_jobs));
-  c.slots = reinterpret_cast<Slot*>(ws + sim_ws_slots_off(b.max_jobs, G));
-  c.queue = reinterpret_cast<int32_t*>(ws + sim_ws_queue_off(b.max_jobs, G));
-  c.rate_eff = reinterpret_cast<double*>(ws + sim_ws_scratch_off(b.max_jobs, G));
-  c.stp_prefix = reinterpret_cast<double*>(ws + sim_ws_prefix_off(b.max_jobs, G));
-  c.jst = ws + sim_ws_jst_off(b.max_jobs, G);
-  c.freemask = reinterpret_cast<uint32_t*>(ws + sim_ws_freemask_off(b.max_jobs, G));
-  c.efftruth = reinterpret_cast<double*>(ws + sim_ws_efftruth_off(b.max_jobs, G));
-  c.arr_us = reinterpret_cast<int64_t*>(ws + sim_ws_arrival_off(b.max_jobs, G));
-  c.W = (G + 31) / 32;
-  c.stp_cmin = INT32_MAX;
-  c.stp_lo = 0;
-  c.n_arrived = 0;
-  c.lmin_t = kNoEvent;
-  c.lmin_pk = ~0ull;
-  c.lmin_idx = -1;
-  c.lmin_valid = false;
-  c.chunk = (J + G + 31) / 32;
-  c.own_lo = lane * c.chunk;
-  c.log = b.log ? b.log + size_t(warp) * b.log_cap : nullptr;
-  c.log_cap = b.log_cap;
-  c.log_n = 0;
-  c.stp_series = b.stp_series ? b.stp_series + size_t(warp) * 2 * b.stp_cap : nullptr;
-  c.stp_cap = b.stp_cap;
-  c.J = J;
-  c.J_used = JT;
-  c.cap_gen = 0;
-  c.fail_gen = 0;
-  c.fail_job = -1;
-  c.G = G;
-  c.qhead = c.qtail = 0;
-  c.now = 0;
-  c.seq = 0;
-  c.nonce = 0;
-  c.stp_cur = 0;
-  c.stp_integral = 0;
-  c.stp_last = 0;
-  c.stp_points = 0;
-  c.stp_dirty = false;
-  c.repartitions = c.migrations = c.mps_sessions = c.done_count = 0;
-  c.first_progress = -1;
-  c.last_completion = -1;
-  c.status = 0;
-  c.processed = 0;
-#if MISO_SIM_PRUNE
-  c.prune = b.prune_bound != nullptr && prm.policy == MISO_B200_POLICY_OPTSTA && J == JT;
-  c.lb_fin = c.lb_narr = c.lb_arrsum = c.lb_unstarted = 0;
-  c.lb_p = c.lb_v = 0.0;
-#endif
-  c.p = &prm;
-  c.spare_lut = b.spare_lut;
-  c.rng_seed = b.rng_seed[warp];  // per task
-  c.w = w;
-
-  // ---- init_jobs / init_gpus (sim.hpp:240-276), lanes in parallel ----
-  for (int i = lane; i < JT; i += 32) {
-    DJob& j = c.jobs[i];
-    const int64_t a = us_from_s(b.arrival_s[J0 + i]);
-    j.remaining = b.base_s[J0 + i];
-    j.base = j.remaining;
-    j.consumed = 0;
-    j.rate = 0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      j.truth[k] = b.speeds5[(size_t(J0) + i) * 5 + k];
-      j.est[k] = 0;
-      j.acc[k] = 0;
-    }
-    j.arrival_us = a;
-    j.last_update_us = a;
-    j.first_progress_us = -1;
-    j.completion_us = -1;
-    j.epoch = 0;
-    j.gpu = -1;
-    j.phase = kQueued;
-    j.slice = 4;
-    j.mem = b.mem_gb[J0 + i];
-    j.qos = b.qos_kind[J0 + i];
-    const int qg = j.qos >= 0 ? kind_gpc(j.qos) : 0;
-    int mk = -1;  // min_slice_for (topology.hpp:68-72)
-    for (int k = 4; k >= 0; --k)
-      if (kind_mem_gb(k) >= j.mem && kind_gpc(k) >= qg) mk = k;
-    j.min_kind = static_cast<uint8_t>(mk < 0 ? 0xFF : mk);
-    j.flags = 0;
-    j.slot = -1;
-    j.inst = b.instances ? b.instances[J0 + i] : 1;
-    j.clone_k = 0;
-    j.parent = -1;
-    c.jst[i] = kQueued | (4 << 3);
-#pragma unroll
-    for (int k = 0; k < 5; ++k) c.efftruth[size_t(k) * J + i] = effective_speed(j.truth[k], k, j.mem, j.qos);
-    c.arr_us[i] = a;
-#if MISO_SIM_PRUNE
-    if (c.prune) c.lb_unstarted += runtime_floor_us(j);  // lane partial, reduced below
-#endif
-    Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
-    s.t = a;
-    s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
-    c.slots[i] = s;
-  }
-  for (int gi = lane; gi < G; gi += 32) {
-    DGpu& g = c.gpus[gi];
-    g.objective = 0;
-    g.plan_obj = 0;
-    g.epoch = 0;
-    g.mode = kGpuIdle;
-    g.mps_level = 0;
-    g.nroster = 0;
-    g.plan_n = 0;
-    g.plan_valid = 0;
-    for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k] = g.kind_cnt[k] = 0;
-    g.spare = 4;
-    g.nslots = 0;
-    for (int k = 0; k < 5; ++k) g.fcnt[k] = 0;
-    if (prm.policy == MISO_B200_POLICY_OPTSTA) {  // init_gpus, sim.hpp:266-276
-      const uint8_t* sc = b.static_counts + size_t(warp) * 5;
-      for (int k = 0; k < 5; ++k) g.fcnt[k] = sc[k];
-      for (int k = 4; k >= 0; --k)
-        for (int r = 0; r < sc[k]; ++r) {
-          g.slot_kind[g.nslots] = static_cast<uint8_t>(k);
-          g.slot_job[g.nslots] = -1;
-          ++g.nslots;
-        }
-      for (int k = 0; k < 5; ++k) g.part[k] = sc[k];
-      g.mode = kGpuMig;
-    }
-    c.slots[J + gi].t = kNoEvent;
-  }
-  for (int i = JT + lane; i < J; i += 32) {  // clone slots: no event, not arrived
-    c.slots[i].t = kNoEvent;
-    c.jst[i] = kQueued | (4 << 3);
-  }
-  for (int i = lane; i < J; i += 32) c.rate_eff[i] = 0.0;
-  for (int wi = lane; wi < 5 * c.W; wi += 32) {  // optsta: every GPU starts with all slots free
-    const int k = wi / c.W, w = wi % c.W;
-    const uint8_t* sc = b.static_counts ? b.static_counts + size_t(warp) * 5 : nullptr;
-    uint32_t v = 0;
-    if (prm.policy == MISO_B200_POLICY_OPTSTA && sc[k] > 0) {
-      const int nb = G - (w << 5);
-      v = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
-    }
-    c.freemask[wi] = v;
-  }
-  __syncwarp();
-#if MISO_SIM_PRUNE
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) c.lb_unstarted += __shfl_xor_sync(0xffffffffu, c.lb_unstarted, off);
-#endif
-  c.seq = static_cast<uint64_t>(JT);  // one arrival event per trace job (sim.hpp:219)
-  bool bad_job = false;
-  for (int i = lane; i < JT; i += 32) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
-  bad_job = __any_sync(0xffffffffu, bad_job);
-
-  // ---- event loop (sim.hpp:221-233) ----
-  if (bad_job && (prm.policy == MISO_B200_POLICY_MISO || prm.policy == MISO_B200_POLICY_ORACLE))
-    c.status = MISO_B200_SIM_INVARIANT;
-  while (c.status == 0) {
-    Slot ev;
-    const int slot = next_event(c, &ev);
-    if (slot < 0) break;
-    if (++c.processed > prm.max_events) {
-      c.status = MISO_B200_SIM_EVENT_BUDGET;
-      break;
-    }
-    clear_slot(c, slot);
-    __syncwarp();
-    c.stp_integral += c.stp_cur * s_from_us(ev.t - c.stp_last);
-    c.stp_last = ev.t;
-    c.now = ev.t;
-    dispatch(c, slot, static_cast<uint32_t>(ev.pk & 7));
-    drain_queue(c);
-    refresh_stp(c);
-    __syncwarp();
-#if MISO_SIM_PRUNE
-    if (c.prune && (c.processed & 31) == 0) {
-      // chosen-only search: stop once this run's JCT sum provably exceeds a completed
-      // candidate's (then its avg_jct_s > that candidate's, so it cannot be the first minimum)
-      const int64_t thr = *reinterpret_cast<volatile const int64_t*>(b.prune_bound + tr);
-      // exact integer part + the started jobs' remaining-work floor (FP sums: 1 s of margin,
-      // far above their rounding error)
-      const int64_t lbi = c.lb_fin + c.lb_narr * c.now - c.lb_arrsum + c.lb_unstarted;
-      const double lb = static_cast<double>(lbi) + (c.lb_p - c.lb_v * s_from_us(c.now)) * 1e6 - 1e6;
-      if (thr != INT64_MAX && lb > static_cast<double>(thr) * (1.0 + 1e-9) + 2.0 * JT) {
-        c.status = MISO_B200_SIM_PRUNED;
-        break;
-      }
-    }
-#endif
-  }
-#if MISO_SIM_PRUNE
-  if (c.prune && c.status == 0 && c.done_count == JT && lane == 0)
-    atomicMin(reinterpret_cast<long long*>(b.prune_bound + tr), static_cast<long long>(c.lb_fin));
-#endif
-
-  // ---- finalize (sim.hpp:902-949) ----
-  const int JU = c.J_used;  // jobs_.size(): trace jobs + spawned clones (sim.hpp:903-913)
-  if (b.job_out) {  // per-job report inputs (sim.hpp:916-929), lanes in parallel
-    int64_t* o = b.job_out + size_t(warp) * size_t(b.max_jobs) * kJobOutFields;
-    for (int i = lane; i < JU; i += 32) {
-      const DJob& j = c.jobs[i];
-      int64_t* r = o + size_t(kJobOutFields) * i;
-      r[0] = (j.flags & kDone) ? j.completion_us : -1;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) r[1 + k] = j.acc[k];
-      r[6] = j.parent;
-      r[7] = j.clone_k;
-    }
-  }
-  SimMetrics m{};  // value-initialised: the padding bytes are deterministic too
-  m.status = c.status;
-  m.job_count = JU;
-  m.completed_count = c.done_count;
-  m.completed = c.done_count == JU;
-  m.repartitions = c.repartitions;
-  m.migrations = c.migrations;
-  m.mps_sessions = c.mps_sessions;
-  m.events = static_cast<int64_t>(c.processed);
-  m.log_records = c.log_n;
-  m.stp_points = c.stp_points;
-  // sim.hpp:914-928: sums in job order over completed jobs. 32 jobs are loaded per step (one
-  // memory round trip instead of one per job) and summed sequentially through shuffles --
-  // the same additions in the same order.
-  double totals[5] = {0, 0, 0, 0, 0};
-  double jct_sum = 0;
-  for (int base = 0; base < JU; base += 32) {
-    const int i = base + lane;
-    double v = 0, a[5] = {0, 0, 0, 0, 0};
-    bool done = false;
-    if (i < JU) {
-      const DJob& j = c.jobs[i];
-      done = (j.flags & kDone) != 0;
-      if (b.job_jct_us && !b.task_trace && i < JT)
-        b.job_jct_us[J0 + i] = done ? j.completion_us - j.arrival_us : -1;
-      if (done) {
-        v = s_from_us(j.completion_us - j.arrival_us);
-#pragma unroll
-        for (int k = 0; k < 5; ++k) a[k] = s_from_us(j.acc[k]);
-      }
-    }
-    const unsigned dm = __ballot_sync(0xffffffffu, done);
-    const int cnt = JU - base < 32 ? JU - base : 32;
-    for (int t = 0; t < cnt; ++t) {
-      const double vt = __shfl_sync(0xffffffffu, v, t);
-      double at[5];
-#pragma unroll
-      for (int k = 0; k < 5; ++k) at[k] = __shfl_sync(0xffffffffu, a[k], t);
-      if ((dm >> t) & 1u) {
-        jct_sum += vt;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) totals[k] += at[k];
-      }
-    }
-  }
-  m.queue_frac = m.mps_frac = m.checkpoint_frac = m.run_frac = m.idle_frac = 0;
-  if (jct_sum > 0) {
-    m.queue_frac = totals[0] / jct_sum;
-    m.mps_frac = totals[1] / jct_sum;
-    m.checkpoint_frac = totals[2] / jct_sum;
-    m.run_frac = totals[3] / jct_sum;
-    m.idle_frac = totals[4] / jct_sum;
-  }
-  const double inf = __longlong_as_double(0x7FF0000000000000ll);
-  m.avg_jct_s = inf;
-  m.makespan_s = inf;
-  m.stp_time_avg = 0;
-  if (m.completed) {
-    m.avg_jct_s = jct_sum / static_cast<double>(JU);
-    m.makespan_s = s_from_us(c.last_completion - c.first_progress);
-    if (c.last_completion > c.first_progress)
-      m.stp_time_avg = c.stp_integral / s_from_us(c.last_completion - c.first_progress);
-  }
-  m.jct_sum_s = jct_sum;
-  if (lane == 0) b.metrics[warp] = m;
-}
-
-}  // namespace MISO_SIM_NS
-
-#if MISO_SIM_PRUNE
-// The pruned best-static search's kernel (this file built with MISO_SIM_PRUNE=1): a separate
-// instantiation, so the bound bookkeeping costs the other simulations nothing.
-cudaError_t launch_simulate_prune(const SimBatch& b, const SimParams& p, const ModelW& w,
-                                  cudaStream_t stream) {
-  const int threads = 128;
-  const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
-  sim_prune::simulate_kernel<<<blocks, threads, 0, stream>>>(b, p, w);
-  return cudaGetLastError();
-}
-#else
-cudaError_t launch_simulate_prune(const SimBatch& b, const SimParams& p, const ModelW& w,
-                                  cudaStream_t stream);
 
 size_t sim_workspace_stride(int max_jobs, int cluster_size) {
   return sim_ws_total(max_jobs, cluster_size);
 }
 
-size_t sim_sizeof_job() { return sizeof(sim::DJob); }
-size_t sim_sizeof_gpu() { return sizeof(sim::DGpu); }
+size_t sim_sizeof_job() { return sizeof(simk::DJob); }
+size_t sim_sizeof_gpu() { return sizeof(simk::DGpu); }
+
+namespace {
+__global__ void __launch_bounds__(256) sim_draws_kernel(const uint64_t* __restrict__ rng_seed,
+                                                        int n_tasks, int k, double* __restrict__ out) {
+  const size_t total = size_t(n_tasks) * size_t(k) * 14;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(i & 1), col = static_cast<int>((i >> 1) % 7);
+    const size_t rest = i / 14;
+    const uint64_t nonce = rest % size_t(k) + 1;
+    const size_t task = rest / size_t(k);
+    out[i] = pack_draw(column_draw(rng_seed[task], nonce, col, e));
+  }
+}
+}  // namespace
+
+cudaError_t launch_sim_draws(const uint64_t* rng_seed, int n_tasks, int k, double* out,
+                             cudaStream_t stream) {
+  if (n_tasks <= 0 || k <= 0) return cudaSuccess;
+  const size_t total = size_t(n_tasks) * size_t(k) * 14;
+  const size_t blocks = std::min<size_t>((total + 255) / 256, size_t(148) * 64);
+  sim_draws_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(rng_seed, n_tasks, k, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double* w2,
                             const double* w1, cudaStream_t stream) {
@@ -1486,21 +47,15 @@ cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double*
     w.w2[i] = w2[i];
     w.w1[i] = w1[i];
   }
-  if (b.prune_bound) return launch_simulate_prune(b, p, w, stream);
-  const int threads = 128;
-  const int blocks = (b.n_seeds * 32 + threads - 1) / threads;
-  // MISO_SIM_SMEM_PAD (tuning only): dynamic shared memory reserved per block to cap how many
-  // simulations share an SM's L1/L2 working set.
-  static int pad = -1;
-  if (pad < 0) {
-    const char* e = getenv("MISO_SIM_SMEM_PAD");
-    pad = e ? atoi(e) : 0;
-    if (pad > 0)
-      cudaFuncSetAttribute(sim::simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+  switch (p.policy) {
+    case MISO_B200_POLICY_NOPART: return launch_sim<MISO_B200_POLICY_NOPART, false>(b, p, w, stream);
+    case MISO_B200_POLICY_OPTSTA:
+      return b.prune_bound ? launch_sim<MISO_B200_POLICY_OPTSTA, true>(b, p, w, stream)
+                           : launch_sim<MISO_B200_POLICY_OPTSTA, false>(b, p, w, stream);
+    case MISO_B200_POLICY_ORACLE: return launch_sim<MISO_B200_POLICY_ORACLE, false>(b, p, w, stream);
+    case MISO_B200_POLICY_MISO: return launch_sim<MISO_B200_POLICY_MISO, false>(b, p, w, stream);
+    default: return cudaErrorInvalidValue;
   }
-  sim::simulate_kernel<<<blocks, threads, pad, stream>>>(b, p, w);
-  return cudaGetLastError();
 }
-#endif
 
 }  // namespace miso_b200

@@ -34,7 +34,7 @@ struct SimParams {
 };
 
 struct SimBatch {
-  int n_seeds, max_jobs;
+  int n_seeds, n_traces, max_jobs;
   const int32_t* job_offsets;   // per trace
   const int32_t* task_trace;    // per task (nullable: task i = trace i)
   const uint8_t* static_counts; // per task, optsta static partition
@@ -56,6 +56,10 @@ struct SimBatch {
   double* stp_series;
   int64_t stp_cap;
   int64_t* prune_bound;  // per trace (nullable): chosen-only best-static search, see capi
+  // the noisy predictor's draws, precomputed per task for call nonces 1..draws_k (nullable):
+  // [task][nonce - 1][column 0..6][entry 4g, 3g], pack_draw encoded (predict.cuh)
+  const double* draws;
+  int draws_k;
 };
 
 // Per-seed workspace layout: [jobs][gpus][slots][queue][progress mask][rate scratch]
@@ -95,10 +99,19 @@ __host__ __device__ inline size_t sim_ws_total(int J, int G) {
   return sim_ws_arrival_off(J, G) + sim_al(size_t(J) * 8);
 }
 
+struct ModelW;  // predict.cuh
+
 size_t sim_workspace_stride(int max_jobs, int cluster_size);
+// one kernel per policy (sim_pol_*.cu); PRUNE = the chosen-only best-static search's runs
+template <int POL, bool PRUNE>
+cudaError_t launch_sim(const SimBatch& b, const SimParams& p, const ModelW& w, cudaStream_t s);
 size_t sim_sizeof_job();
 size_t sim_sizeof_gpu();
 cudaError_t launch_simulate(const SimBatch& b, const SimParams& p, const double* w2,
                             const double* w1, cudaStream_t stream);
+// The noisy predictor's draws of every task for call nonces 1..k (SimBatch::draws), one thread
+// per draw: the throughput-bound half of finish_profiling, taken out of the event loop.
+cudaError_t launch_sim_draws(const uint64_t* rng_seed, int n_tasks, int k, double* out,
+                             cudaStream_t stream);
 
 }  // namespace miso_b200

@@ -26,7 +26,8 @@ class SimOptionsC(C.Structure):
         ("checkpoint_restart_s", C.c_double), ("mps_window_s", C.c_double),
         ("interference", C.c_double), ("predictor_noisy", C.c_int), ("target_mae", C.c_double),
         ("check_invariants", C.c_int), ("reprofile_drift_threshold", C.c_double),
-        ("max_events", C.c_uint64),
+        ("max_events", C.c_uint64), ("small_slice_model_fitted", C.c_int),
+        ("small_slice_w2", C.c_double * 4), ("small_slice_w1", C.c_double * 4),
     ]
 
 
@@ -34,7 +35,7 @@ class SimMetricsC(C.Structure):
     _fields_ = [
         ("status", C.c_int), ("completed", C.c_int), ("job_count", C.c_int),
         ("completed_count", C.c_int), ("repartitions", C.c_int), ("migrations", C.c_int),
-        ("mps_sessions", C.c_int), ("pad", C.c_int), ("avg_jct_s", C.c_double),
+        ("mps_sessions", C.c_int), ("detail", C.c_int), ("avg_jct_s", C.c_double),
         ("makespan_s", C.c_double), ("stp_time_avg", C.c_double), ("jct_sum_s", C.c_double),
         ("queue_frac", C.c_double), ("mps_frac", C.c_double), ("checkpoint_frac", C.c_double),
         ("run_frac", C.c_double), ("idle_frac", C.c_double), ("events", C.c_int64),
@@ -44,9 +45,9 @@ class SimMetricsC(C.Structure):
 
 LOG_DTYPE = np.dtype([("t", "<i8"), ("kind", "u1"), ("x", "u1"), ("gpu", "<u2"), ("job", "<i4"),
                       ("a", "<u4"), ("b", "<u4"), ("v", "<f8")])
-METRIC_FIELDS = [f for f, _ in SimMetricsC._fields_ if f != "pad"]
+METRIC_FIELDS = [f for f, _ in SimMetricsC._fields_ if f != "detail"]
 METRICS_DTYPE = np.dtype([(f, "<i4") for f in ("status", "completed", "job_count", "completed_count",
-                                               "repartitions", "migrations", "mps_sessions", "pad")]
+                                               "repartitions", "migrations", "mps_sessions", "detail")]
                          + [(f, "<f8") for f in ("avg_jct_s", "makespan_s", "stp_time_avg",
                                                  "jct_sum_s", "queue_frac", "mps_frac",
                                                  "checkpoint_frac", "run_frac", "idle_frac")]
@@ -57,14 +58,37 @@ assert LOG_DTYPE.itemsize == 32
 lib.miso_b200_generate_trace.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_int,
                                          C.c_double, C.c_double, C.c_double, C.c_double,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
-lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
+_I = C.c_int
+lib.miso_b200_simulate_batch.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), _I, _I, _I] + \
     [C.c_void_p] * 12 + [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]
-lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
+lib.miso_b200_simulate_batch_ex.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), _I, _I, _I] + \
     [C.c_void_p] * 14 + [C.c_int64, C.c_void_p, C.c_int64, C.c_uint, C.c_void_p]
-if hasattr(lib, "miso_b200_simulate_batch_pruned"):  # (absent only in older tuning builds)
-    lib.miso_b200_simulate_batch_pruned.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), C.c_int] + \
-        [C.c_void_p] * 11 + [C.c_uint, C.c_void_p]
-SIM_PRUNED = 5  # MISO_B200_SIM_PRUNED
+lib.miso_b200_simulate_batch_pruned.argtypes = [C.c_void_p, C.POINTER(SimOptionsC), _I, _I, _I] + \
+    [C.c_void_p] * 11 + [C.c_uint, C.c_void_p]
+SIM_PRUNED = 5     # MISO_B200_SIM_PRUNED
+SIM_BAD_INPUT = 6  # MISO_B200_SIM_BAD_INPUT
+
+
+def bad_input_message(detail: int, job_ids=None) -> str:
+    """MISO_B200_SIM_BAD_INPUT's metrics.detail as the reference's invalid_argument text
+    (validate_profile, profiles.hpp:67-87; init_jobs, sim.hpp:246-254)."""
+    code, job = detail & 0xFF, detail >> 8
+    jid = job_ids[job] if job_ids is not None and job < len(job_ids) else f"j{job}"
+    pre = f"job '{jid}': "
+    if 3 <= code < 8:
+        return pre + f"speed on {KIND_NAMES[code - 3]} outside (0,1]"
+    return {1: pre + "base duration must be positive",
+            2: pre + "memory demand must be in (0, 40] GB",
+            8: pre + "speed on 7g must be exactly 1",
+            9: pre + "speed table not monotone in gpc count",
+            10: pre + "instance count must be >= 1",
+            11: "first arrival must be at t=0",
+            12: "arrival times must be non-decreasing",
+            13: "trace has no jobs",
+            14: "task_trace entry out of range",
+            15: "static partition is not a feasible partition",
+            16: "trace jobs exceed the workspace capacity (max_jobs)"}.get(
+                code, f"invalid simulation input (detail {detail})")
 
 
 @dataclass
@@ -81,13 +105,20 @@ class SimOptions:
     check_invariants: bool = True
     reprofile_drift_threshold: float = 0.0
     max_events: int = 100_000_000
+    # SimOptions::small_slice_model (sim.hpp:88): (w2, w1) weights over (f7, f4, f3, 1) of a
+    # fitted LinearMap; None = the shared default model (sim.hpp:894-896)
+    small_slice_model: Optional[tuple] = None
 
     def to_c(self) -> SimOptionsC:
+        fitted = self.small_slice_model is not None
+        w2, w1 = self.small_slice_model if fitted else ((0.0,) * 4, (0.0,) * 4)
         return SimOptionsC(POLICIES[self.policy], self.cluster_size, self.mig_reconfig_s,
                            self.checkpoint_restart_s, self.mps_window_s, self.interference,
                            1 if self.predictor == "noisy" else 0, self.target_mae,
                            1 if self.check_invariants else 0, self.reprofile_drift_threshold,
-                           self.max_events)
+                           self.max_events, 1 if fitted else 0,
+                           (C.c_double * 4)(*[float(x) for x in w2]),
+                           (C.c_double * 4)(*[float(x) for x in w1]))
 
 
 @dataclass
@@ -188,6 +219,13 @@ def _csr(traces):
     """(offsets, arrival, duration, speeds5, mem, qos, instances or None) of a trace list."""
     if isinstance(traces, (TraceBatch, DeviceTraceBatch)) and traces.csr is not None:
         return traces.csr
+    for t in traces:  # the uint8 casts below must not wrap: out-of-range values are rejected here
+        mem = np.asarray(t.mem_gb)
+        bad = np.nonzero((mem < 1) | (mem > 40))[0]
+        if len(bad):
+            raise ValueError(f"job 'j{int(bad[0])}': memory demand must be in (0, 40] GB")
+        if t.instances is not None and (np.asarray(t.instances) > 255).any():
+            raise ValueError("instance_count above 255")
     offs = np.zeros(len(traces) + 1, np.int32)
     offs[1:] = np.cumsum([t.n for t in traces])
     cat = lambda f, dt: np.concatenate([np.asarray(f(t), dt).reshape(-1) for t in traces])  # noqa: E731
@@ -262,7 +300,7 @@ class SimResult:
 
     def report(self, i: int) -> dict:
         m = self.metrics[i]
-        return {f: m[f].item() for f in METRICS_DTYPE.names if f != "pad"}
+        return {f: m[f].item() for f in METRICS_DTYPE.names if f != "detail"}
 
 
 def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
@@ -296,6 +334,21 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     seeds = np.asarray(rng_seeds, np.uint64)
     if opts.policy == "optsta" and static_partitions is None:
         raise ValueError("optsta requires a static partition")  # sim.hpp:208-209
+    if want_jct and task_trace is not None:
+        raise ValueError("want_jct returns per-trace-job JCTs: not with task_trace")
+    # workspace capacity: the largest trace's jobs plus every multi-instance clone
+    if isinstance(traces, DeviceTraceBatch):
+        n_traces, max_jobs = traces.n, traces.job_count
+    else:
+        offs_h = np.asarray(offs, np.int64)
+        n_traces = len(offs_h) - 1
+        per = np.diff(offs_h)
+        if inst is not None:
+            ex = np.maximum(np.asarray(inst, np.int64) - 1, 0)
+            cs = np.concatenate([[0], np.cumsum(ex)])
+            per = per + cs[offs_h[1:]] - cs[offs_h[:-1]]
+        max_jobs = int(per.max()) if len(per) else 1
+    max_jobs = max(1, max_jobs)
     with torch.cuda.stream(st_obj):
         T = lambda x: x.to(dev) if isinstance(x, torch.Tensor) else \
             torch.from_numpy(np.ascontiguousarray(x)).to(dev, non_blocking=False)  # noqa: E731
@@ -314,12 +367,14 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         if prune_bound is not None:
             if inst is not None or want_jct or log_cap or stp_cap:
                 raise ValueError("pruned runs take single-instance traces and return metrics only")
-            _check(lib.miso_b200_simulate_batch_pruned(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+            _check(lib.miso_b200_simulate_batch_pruned(ctx._h, C.byref(o), S, n_traces, max_jobs,
+                                                       p(d_tt), p(d_sc), p(d_offs),
                                                        p(d_arr), p(d_dur), p(d_sp), p(d_mem), p(d_qos),
                                                        p(d_seed), p(d_met), prune_bound.data_ptr(),
                                                        1 if jct_only else 0, st_obj.cuda_stream))
         else:
-            _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, p(d_tt), p(d_sc), p(d_offs),
+            _check(lib.miso_b200_simulate_batch_ex(ctx._h, C.byref(o), S, n_traces, max_jobs,
+                                                   p(d_tt), p(d_sc), p(d_offs),
                                                    p(d_arr), p(d_dur),
                                                    p(d_sp), p(d_mem), p(d_qos), p(d_inst), p(d_seed), p(d_met),
                                                    p(d_jct), None, p(d_log), log_cap, p(d_stp), stp_cap,
@@ -330,6 +385,9 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
         st_obj.synchronize()
         _ = keep  # inputs stay referenced until the stream has finished with them
         met = d_met.cpu().numpy().view(METRICS_DTYPE)
+        bad = np.nonzero(met["status"] == SIM_BAD_INPUT)[0]
+        if len(bad):  # the reference's std::invalid_argument (first failing task)
+            raise ValueError(bad_input_message(int(met["detail"][bad[0]])))
         res = SimResult(met, traces=[] if isinstance(traces, DeviceTraceBatch) else list(traces))
         if want_jct:
             j = d_jct.cpu().numpy()

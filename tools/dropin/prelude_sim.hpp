@@ -1,8 +1,9 @@
 // Force-included (-include) before a reference simulator/experiment test file to run it against
 // the B200 library: every reference header is compiled first (their real definitions, including
-// the reference's own run_experiment / optsta_search, which keep calling the CPU engine), then
-// later mentions of run_simulation, best_static_partition and run_experiment_in_memory in the
-// test file resolve to the B200 binding (include/miso_b200_sim.hpp, miso_b200_experiment.hpp).
+// the reference's own run_experiment / optsta_search), then later mentions of run_simulation,
+// best_static_partition, run_experiment_in_memory, run_experiment and optsta_search in the
+// test file resolve to the B200 binding (include/miso_b200_sim.hpp, miso_b200_experiment.hpp),
+// so no test reaches the reference's CPU engine.
 #pragma once
 #include "miso/common.hpp"
 #include "miso/topology.hpp"
@@ -29,7 +30,15 @@ inline StaticSearchResult b200_best_static_partition_dropin(const JobTrace& t, i
 inline ExperimentResult b200_run_experiment_in_memory_dropin(const ExperimentConfig& c) {
   return b200::run_experiment_in_memory(c);
 }
+inline ExperimentResult b200_run_experiment_dropin(const ExperimentConfig& c) {
+  return b200::run_experiment(c);
+}
+inline StaticSearchResult b200_optsta_search_dropin(const ExperimentConfig& c) {
+  return b200::optsta_search(c);
+}
 }  // namespace miso
 #define run_simulation b200_run_simulation_dropin
 #define best_static_partition b200_best_static_partition_dropin
 #define run_experiment_in_memory b200_run_experiment_in_memory_dropin
+#define run_experiment b200_run_experiment_dropin
+#define optsta_search b200_optsta_search_dropin

@@ -54,6 +54,75 @@ int main() {
       }
     }
   }
+  // A caller-fitted small-slice model (SimOptions::small_slice_model, sim.hpp:88, 894-896): a
+  // model fitted on another corpus drives the miso/oracle estimates on both engines.
+  const miso::LinearMap custom = miso::fit_small_slice_model(miso::make_training_corpus(400, 0xc0ffee));
+  for (int trial = 0; trial < 4; ++trial) {
+    miso::TraceSpec spec;
+    spec.job_count = 60;
+    spec.lambda_s = 25;
+    spec.seed = 9100 + static_cast<uint64_t>(trial);
+    auto trace = miso::generate_trace(spec);
+    for (miso::Policy p : {miso::Policy::oracle, miso::Policy::miso}) {
+      miso::SimOptions o;
+      o.policy = p;
+      o.cluster_size = 3;
+      o.predictor.mode = miso::PredictorSpec::Mode::noisy;
+      o.predictor.rng_seed = spec.seed;
+      o.small_slice_model = custom;
+      std::ostringstream log_ref, log_dev;
+      o.event_log = &log_ref;
+      auto r = miso::run_simulation(trace, o);
+      o.event_log = &log_dev;
+      auto d = miso::b200::run_simulation(trace, o);
+      ++runs;
+      if (miso::format_report(r) != miso::format_report(d) || log_ref.str() != log_dev.str()) {
+        std::printf("custom model trial %d policy %s: DIFFER\n", trial, miso::policy_label(p));
+        ++bad;
+      }
+    }
+  }
+  // max_events (sim.hpp:224) counts every heap pop, stale ones included: find the reference's
+  // smallest budget that completes (= its pop count) and check both sides of it on the device.
+  for (int trial = 0; trial < 3; ++trial) {
+    miso::TraceSpec spec;
+    spec.job_count = 30;
+    spec.lambda_s = 15;
+    spec.seed = 9300 + static_cast<uint64_t>(trial);
+    auto trace = miso::generate_trace(spec);
+    for (miso::Policy p : {miso::Policy::optsta, miso::Policy::miso}) {
+      miso::SimOptions o;
+      o.policy = p;
+      o.cluster_size = 2;
+      o.predictor.mode = miso::PredictorSpec::Mode::noisy;
+      o.predictor.rng_seed = spec.seed;
+      if (p == miso::Policy::optsta) o.static_partition = miso::default_catalog().entries[8];
+      auto completes = [&](bool device, uint64_t budget) {
+        o.max_events = budget;
+        try {
+          if (device) miso::b200::run_simulation(trace, o);
+          else miso::run_simulation(trace, o);
+          return 1;
+        } catch (const miso::SimInvariantError& e) {
+          return std::string(e.what()) == "event budget exhausted" ? 0 : -1;
+        }
+      };
+      uint64_t lo = 1, hi = 1;
+      while (completes(false, hi) == 0) hi *= 2;
+      while (lo < hi) {  // smallest budget that completes
+        const uint64_t mid = (lo + hi) / 2;
+        if (completes(false, mid) == 1) hi = mid;
+        else lo = mid + 1;
+      }
+      const int at = completes(true, lo), below = completes(true, lo - 1);
+      ++runs;
+      if (at != 1 || below != 0) {
+        std::printf("max_events trial %d policy %s: reference needs %llu pops; device %d at it, %d below\n",
+                    trial, miso::policy_label(p), static_cast<unsigned long long>(lo), at, below);
+        ++bad;
+      }
+    }
+  }
   std::printf("%d runs, %d mismatches\n%s\n", runs, bad, bad ? "SIM PARITY FAILED" : "SIM PARITY OK");
   return bad ? 1 : 0;
 }

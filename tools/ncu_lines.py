@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: tools/ncu_lines.py REPORT.ncu-rep CUBIN_SUBSTR KERNEL_SUBSTR [top]
+usage: tools/ncu_lines.py REPORT.ncu-rep CUBIN_SUBSTR KERNEL_SUBSTR [top] [column]
+(column: the source page's sample column, default "Warp Stall Sampling (All Samples)"; e.g.
+stall_no_inst, stall_long_sb, stall_wait)
 Uses `ncu --page source --print-source sass` (samples per SASS instruction) and
 `nvdisasm -g` of the matching cubin extracted from the built library (line table).
 """
@@ -21,12 +23,13 @@ LIB = ROOT / "paper_2207_11428_b200" / "_lib" / "libmiso_b200.so"
 def main():
     rep, cub_sub, kern_sub = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+    col = sys.argv[5] if len(sys.argv) > 5 else "Warp Stall Sampling (All Samples)"
     sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                           capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(sass)))
     h = rows[1]
     data = rows[2:]
-    iall = h.index("Warp Stall Sampling (All Samples)")
+    iall = h.index(col)
     iex = h.index("Instructions Executed")
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", str(LIB)], cwd=d, capture_output=True)
