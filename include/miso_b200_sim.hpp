@@ -430,6 +430,11 @@ inline std::vector<StaticSearchResult> best_static_partition_batch(
 // once, its two likeliest winners (most GPCs, then slice count nearest 3) run first, and every
 // other candidate stops once its JCT sum provably exceeds a completed candidate's
 // (miso_b200_simulate_batch_pruned). Traces with multi-instance jobs take the full search.
+// Error-behaviour divergence (by design): a candidate stopped early never reaches a later
+// SimInvariantError or event-budget exhaustion, so where the reference's best_static_partition
+// (sim.hpp:1031-1066) would throw from a losing candidate, this returns the chosen entry.
+// Callers that need the reference's throw-on-any-candidate behaviour use
+// best_static_partition (full search), which reports every candidate's status.
 inline std::vector<PartitionConfig> best_static_chosen_batch(
     const std::vector<const JobTrace*>& traces, int cluster_size, const OverheadSpec& overheads,
     const PartitionCatalog& catalog = default_catalog()) {

@@ -106,6 +106,28 @@ def _is_torch_cuda(x) -> bool:
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
 
 
+def _check_device_args(speeds, offsets, cand, obj, n: int) -> None:
+    """The device-pointer optimize call dereferences every tensor on speeds' device: reject
+    host tensors, other devices, strided views, wrong dtypes and short buffers up front
+    (the reference raises invalid_argument for malformed input, optimizer.hpp:65-66)."""
+    import torch
+    if speeds.dtype != torch.float64:
+        raise ValueError("speeds must be float64")
+    if offsets.dtype not in (torch.int32, torch.uint32):
+        raise ValueError("offsets must be int32/uint32")
+    if cand.dtype != torch.uint8 or obj.dtype != torch.float64:
+        raise ValueError("cand must be uint8 and obj float64")
+    for name, t in (("speeds", speeds), ("offsets", offsets), ("cand", cand), ("obj", obj)):
+        if not _is_torch_cuda(t) or t.device != speeds.device:
+            raise ValueError(f"{name} must be a CUDA tensor on {speeds.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    if cand.numel() < n or obj.numel() < n:
+        raise ValueError(f"cand/obj hold fewer than {n} instances")
+    if speeds.numel() % 5:
+        raise ValueError("speeds must hold 5 kind speeds per job")
+
+
 class Context:
     """One context per device (miso_b200_create)."""
 
@@ -162,8 +184,8 @@ class Context:
                 cand = torch.empty(n, dtype=torch.uint8, device=speeds.device)
             if obj is None:
                 obj = torch.empty(n, dtype=torch.float64, device=speeds.device)
-            assert speeds.dtype == torch.float64 and offsets.dtype in (torch.int32, torch.uint32)
-            s = stream if stream is not None else torch.cuda.current_stream(speeds.device).cuda_stream
+            _check_device_args(speeds, offsets, cand, obj, n)
+            s =stream if stream is not None else torch.cuda.current_stream(speeds.device).cuda_stream
             _check(lib.miso_b200_optimize_batch(self._h, speeds.data_ptr(), offsets.data_ptr(), n,
                                                 cand.data_ptr(), obj.data_ptr(), s))
             return cand, obj
