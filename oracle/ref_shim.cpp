@@ -435,6 +435,23 @@ int ref_load_trace(const char* text, int* job_count, char* msg, size_t cap) {
   }
 }
 
+// parse_profile_record (profiles.hpp:564-568) of `line` at `lineno`, then
+// format_profile_record (:493-495) of the result: 0 and the record text in out, or the
+// ParseError line (-1 when it is 0) / -2 for std::invalid_argument, and what() in out.
+int ref_profile_record(const char* line, int lineno, char* out, size_t cap) {
+  try {
+    const std::string t = miso::format_profile_record(miso::parse_profile_record(line, lineno));
+    std::snprintf(out, cap, "%s", t.c_str());
+    return 0;
+  } catch (const miso::ParseError& e) {
+    std::snprintf(out, cap, "%s", e.what());
+    return e.line() > 0 ? e.line() : -1;
+  } catch (const std::invalid_argument& e) {
+    std::snprintf(out, cap, "%s", e.what());
+    return -2;
+  }
+}
+
 // Raw std::mt19937_64 draws of DetRng(seed) (common.hpp:85-119), for fixture generators.
 void ref_rng_raw(uint64_t seed, size_t n, uint64_t* out) {
   miso::DetRng rng(seed);

@@ -8,6 +8,7 @@ the C++ binding uses the reference's own reader.
 """
 from __future__ import annotations
 
+import ctypes
 import io
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, TextIO, Union
@@ -99,10 +100,13 @@ def synthetic_mps_rates(speeds5: np.ndarray) -> np.ndarray:
     return out
 
 
-def _validate_profile(job_id, duration, mem, speeds, mps, line):
-    """validate_profile (profiles.hpp:67-87), ParseError form (line > 0)."""
+def _validate_profile(job_id, duration, mem, speeds, mps, line, instance_count=1):
+    """validate_profile (profiles.hpp:67-87): ParseError when line > 0, else ValueError (the
+    reference's std::invalid_argument)."""
     def fail(msg):
-        raise ParseError(f"job '{job_id}': {msg}", line)
+        if line > 0:
+            raise ParseError(f"job '{job_id}': {msg}", line)
+        raise ValueError(f"job '{job_id}': {msg}")
     if not job_id:
         fail("empty job id")
     if "," in job_id:
@@ -122,27 +126,110 @@ def _validate_profile(job_id, duration, mem, speeds, mps, line):
     for r in mps:
         if not (r > 0.0 and r <= 1.0):
             fail("mps rate outside (0,1]")
+    if instance_count < 1:
+        fail("instance count must be >= 1")
+
+
+_libc = ctypes.CDLL(None, use_errno=True)
+_libc.strtod.restype = ctypes.c_double
+_libc.strtod.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p)]
+_libc.strtol.restype = ctypes.c_long
+_libc.strtol.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p), ctypes.c_int]
+_ERANGE = 34
+
+
+def _c_convert(fn, tok: str, *base):
+    """(value, characters consumed, ERANGE?) of libc strtod/strtol -- what std::stod/stoi call
+    (hex floats, nan(...), leading whitespace and underflow/overflow as the reference sees them)."""
+    raw = tok.encode()
+    if b"\0" in raw:
+        raw = raw[:raw.index(b"\0")]  # std::stod sees the C string
+    buf = ctypes.create_string_buffer(raw)
+    end = ctypes.c_char_p()
+    ctypes.set_errno(0)
+    v = fn(buf, ctypes.byref(end), *base)
+    err = ctypes.get_errno()
+    used = ctypes.cast(end, ctypes.c_void_p).value - ctypes.addressof(buf)
+    return v, len(raw[:used].decode(errors="replace")), err == _ERANGE
 
 
 def _parse_double(tok: str, what: str, line: int) -> float:
-    """std::stod with the whole token consumed (common.hpp parse_double)."""
-    s = tok.lstrip(" \t\n\v\f\r")
-    if s != s.rstrip() or "_" in s or not s:
+    """detail::parse_double (profiles.hpp:512-522): std::stod with the whole token consumed."""
+    v, used, erange = _c_convert(_libc.strtod, tok)
+    if used == 0 or erange or used != len(tok):
         raise ParseError(f"bad {what} '{tok}'", line)
-    try:
-        return float(s)
-    except ValueError:
-        raise ParseError(f"bad {what} '{tok}'", line) from None
+    return v
 
 
 def _parse_int(tok: str, what: str, line: int) -> int:
-    s = tok.lstrip(" \t\n\v\f\r")
-    if not s or s != s.strip() or "_" in s:
+    """detail::parse_int (profiles.hpp:524-534): std::stoi (strtol, then the int range)."""
+    v, used, erange = _c_convert(_libc.strtol, tok, 10)
+    if used == 0 or erange or not (-2**31 <= v < 2**31) or used != len(tok):
         raise ParseError(f"bad {what} '{tok}'", line)
-    try:
-        return int(s, 10)
-    except ValueError:
-        raise ParseError(f"bad {what} '{tok}'", line) from None
+    return v
+
+
+@dataclass
+class ProfileRecord:
+    """JobProfile (profiles.hpp:47-56) as a profile record carries it."""
+    job_id: str
+    base_duration_s: float
+    mem_demand_gb: int
+    qos_kind: int               # -1 = none, else kind index 0..4 (1g..7g)
+    speeds5: np.ndarray         # kind order 1g..7g
+    mps_rates: np.ndarray       # rates at MPS levels 100/50/14
+
+
+def split_csv(line: str) -> List[str]:
+    """detail::split_csv (profiles.hpp:497-510): split on ',', drop every '\\r'."""
+    return [t.replace("\r", "") for t in line.split(",")]
+
+
+def format_profile_body(p: ProfileRecord) -> str:
+    """format_profile_body (profiles.hpp:484-491): base, mem, qos gpc (0 = none), f7..f1,
+    mps100/50/14."""
+    qg = GPC[int(p.qos_kind)] if p.qos_kind is not None and int(p.qos_kind) >= 0 else 0
+    sp = np.asarray(p.speeds5, np.float64).reshape(5)
+    out = [fmt_exact(float(p.base_duration_s)), str(int(p.mem_demand_gb)), str(qg)]
+    out += [fmt_exact(float(sp[k])) for k in range(4, -1, -1)]
+    out += [fmt_exact(float(r)) for r in np.asarray(p.mps_rates, np.float64).reshape(3)]
+    return ",".join(out)
+
+
+def format_profile_record(p: ProfileRecord) -> str:
+    """format_profile_record (profiles.hpp:493-495)."""
+    return p.job_id + "," + format_profile_body(p)
+
+
+def parse_profile_body(job_id: str, tokens: Sequence[str], offset: int,
+                       line: int) -> ProfileRecord:
+    """parse_profile_body (profiles.hpp:539-562): the 11 fields after tokens[offset - 1],
+    checked in the reference's order, then validate_profile."""
+    if len(tokens) != offset + 11:
+        raise ParseError(f"expected {offset + 11} fields, got {len(tokens)}", line)
+    i = offset
+    d = _parse_double(tokens[i], "duration", line)
+    m = _parse_int(tokens[i + 1], "memory demand", line)
+    qg = _parse_int(tokens[i + 2], "qos gpc", line)
+    qk = -1
+    if qg != 0:
+        if qg not in GPC:
+            raise ParseError(f"qos gpc {qg} is not a slice size", line)
+        qk = GPC.index(qg)
+    s5 = [0.0] * 5
+    for j, k in enumerate(range(4, -1, -1)):
+        s5[k] = _parse_double(tokens[i + 3 + j], "speed", line)
+    r3 = [_parse_double(tokens[i + 8 + r], "mps rate", line) for r in range(3)]
+    _validate_profile(job_id, d, m, s5, r3, line)
+    return ProfileRecord(job_id, d, m, qk, np.asarray(s5), np.asarray(r3))
+
+
+def parse_profile_record(line_text: str, line: int = 0) -> ProfileRecord:
+    """parse_profile_record (profiles.hpp:564-568)."""
+    tok = split_csv(line_text)
+    if not tok or not tok[0]:
+        raise ParseError("missing job id", line)
+    return parse_profile_body(tok[0], tok, 1, line)
 
 
 def save_trace(trace: Trace, spec: TraceSpec, out: Union[str, TextIO],
@@ -232,23 +319,12 @@ def loads(text: str) -> TraceFile:
         line = lines[idx]
         if not line:
             continue
-        tok = [t.replace("\r", "") for t in line.split(",")]
+        tok = split_csv(line)
         if len(tok) != 13:
             raise ParseError(f"expected 13 fields, got {len(tok)}", ln)
         a = _parse_double(tok[1], "arrival", ln)
-        d = _parse_double(tok[2], "duration", ln)
-        m = _parse_int(tok[3], "memory demand", ln)
-        qg = _parse_int(tok[4], "qos gpc", ln)
-        qk = -1
-        if qg != 0:
-            if qg not in GPC:
-                raise ParseError(f"qos gpc {qg} is not a slice size", ln)
-            qk = GPC.index(qg)
-        s5 = [0.0] * 5
-        for j, k in enumerate(range(4, -1, -1)):
-            s5[k] = _parse_double(tok[5 + j], "speed", ln)
-        r3 = [_parse_double(tok[10 + r], "mps rate", ln) for r in range(3)]
-        _validate_profile(tok[0], d, m, s5, r3, ln)
+        pr = parse_profile_body(tok[0], tok, 2, ln)
+        d, m, qk, s5, r3 = pr.base_duration_s, pr.mem_demand_gb, pr.qos_kind, pr.speeds5, pr.mps_rates
         if tok[0] in seen:
             raise ParseError(f"duplicate job id '{tok[0]}'", ln)
         seen.add(tok[0])
@@ -261,7 +337,7 @@ def loads(text: str) -> TraceFile:
             raise ParseError("duration exceeds max_duration_s cap", ln)
         prev = a
         ids.append(tok[0]); arr.append(a); dur.append(d); mem.append(m); qos.append(qk)
-        sp.append(s5); mps.append(r3)
+        sp.append(list(s5)); mps.append(list(r3))
     if len(ids) != spec.job_count:
         raise ParseError(f"spec says {spec.job_count} jobs, file has {len(ids)}", ln)
     q = np.asarray(qos, np.int8)

@@ -195,6 +195,16 @@ class Ref:
         r = f(text.encode(), C.byref(jc), msg, 512)
         return r, jc.value, msg.value.decode()
 
+    def profile_record(self, line: str, lineno: int = 0):
+        """The reference's parse_profile_record -> format_profile_record on `line`:
+        (0, record text) or (ParseError line / -1 when 0 / -2 invalid_argument, what())."""
+        f = self.lib.ref_profile_record
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_size_t]
+        out = C.create_string_buffer(1024)
+        r = f(line.encode(), lineno, out, 1024)
+        return r, out.value.decode()
+
     def c1_time(self, reps: int, seed=7, job_count=3, interference=0.8, target_mae=0.017):
         """Seconds for `reps` config-1 decisions on this thread (ref_c1_time) and the sum of
         their objectives (nonce 1..reps)."""

@@ -73,3 +73,51 @@ def test_load_trace_errors_match_reference(ref):
         assert ei.value.line == r_line
         n += 1
     assert n >= 15
+
+
+def _profile_lines(ref):
+    """Valid records (every line of a reference trace, minus its arrival field) and mutations
+    that trip each of parse_profile_body's and validate_profile's checks."""
+    text = ref.trace_text(5, 12, 10.0).split("\n")
+    rows = [ln.split(",") for ln in text[3:] if ln]
+    good = [",".join([r[0]] + r[2:]) for r in rows]
+    yield from good
+    base = good[3].split(",")
+    for i, bad in [(1, "x"), (1, "0"), (1, "-2"), (1, " 3"), (1, "3 "), (1, "nan"), (1, "inf"),
+                   (2, "0"), (2, "41"), (2, "7.5"), (2, "+5"), (2, "0x10"), (3, "5"), (3, "-1"),
+                   (3, "2"), (4, "1.0000001"), (4, "0.5"), (5, "1.5"), (6, "0"), (7, "-0.1"),
+                   (8, "1e-320"), (9, "0"), (10, "2"), (11, "nan"), (0, ""), (0, "a\rb"),
+                   (5, "1e999"), (5, "0x1p-1"), (2, "99999999999"), (1, "nan(1)"), (2, " 5"),
+                   (1, "1e-310"), (7, "0x1.8p-1"), (1, "INFINITY"), (2, "-0"), (3, "+4")]:
+        r = list(base)
+        r[i] = bad
+        yield ",".join(r)
+    yield ",".join(base[:11])
+    yield ",".join(base + ["1"])
+    yield ",".join(base) + "\r"
+    yield ""
+
+
+@pytest.mark.parametrize("lineno", [0, 7])
+def test_profile_records_match_reference(ref, lineno):
+    """parse_profile_record / format_profile_record (profiles.hpp:484-568) against the
+    reference's: the same text back for every accepted line, the same ParseError line and
+    message (or std::invalid_argument from validate_profile when lineno is 0) otherwise."""
+    from paper_2207_11428_b200 import tracefile as tf
+    n_ok = n_err = 0
+    for line in _profile_lines(ref):
+        r, want = ref.profile_record(line, lineno)
+        if r == 0:
+            assert tf.format_profile_record(tf.parse_profile_record(line, lineno)) == want, line
+            n_ok += 1
+            continue
+        exc = ValueError if r == -2 else tf.ParseError
+        with pytest.raises(exc) as ei:
+            tf.parse_profile_record(line, lineno)
+        if r != -2:
+            assert isinstance(ei.value, tf.ParseError) and ei.value.line == (r if r > 0 else 0)
+        else:
+            assert not isinstance(ei.value, tf.ParseError)
+        assert str(ei.value) == want, (line, want)
+        n_err += 1
+    assert n_ok >= 12 and n_err >= 25
