@@ -599,8 +599,22 @@ def sec_c1(args, ctx):
         py_lat.append(time.perf_counter() - t0)
     first, _ = ctx.decide(jobs, nonce=1, rng_seed=7)
     exe = ROOT / "paper_2207_11428_b200" / "_lib" / "c1_latency"
-    cpp = json.loads(subprocess.run([str(exe), str(K)], check=True, capture_output=True,
+    # the scalar optimize_partition drop-in on 2000 acceptance-distribution mixes (DetRng
+    # 0xacce91, acceptance_test.cpp:72-85), one instance per call from C++
+    import tempfile
+    ol = oracle_lib()
+    have_ref = ol.have_ref()
+    n_opt = 2000
+    o_sp, o_off = (ol.Ref() if have_ref else ol.Oracle()).gen_mixes(0xACCE91, n_opt)
+    tmpd = tempfile.mkdtemp(prefix="miso_c1_")
+    mixf, outf = os.path.join(tmpd, "mixes.bin"), os.path.join(tmpd, "out.bin")
+    with open(mixf, "wb") as f:
+        f.write(np.uint64(n_opt).tobytes() + o_off.astype(np.uint32).tobytes() + o_sp.tobytes())
+    cpp = json.loads(subprocess.run([str(exe), str(K), mixf, outf], check=True, capture_output=True,
                                     text=True).stdout)
+    raw = open(outf, "rb").read()
+    g_ent = np.frombuffer(raw[:4 * n_opt], np.int32)
+    g_obj = np.frombuffer(raw[4 * n_opt:], np.float64)
     res = {"metric": "config-1 decision latency (MPS profile -> predictor -> best MIG partition, 3 jobs)",
            "value": cpp["consecutive_us"], "unit": "us/decision", "higher_is_better": False,
            "p99_us": cpp["consecutive_p99_us"],
@@ -616,9 +630,22 @@ def sec_c1(args, ctx):
            "roofline": {"bound": "latency (PCIe round trip of one request; see DESIGN.md 4(a))"},
            "e2e": {"value": cpp["consecutive_us"], "unit": "us/decision",
                    "h2d_bytes_per_step": 320, "d2h_bytes_per_step": 8 * (4 + 5 * 3)}}
-    if "optimize_us" in cpp:
-        res["optimize_partition_us"] = cpp["optimize_us"]
-    ol = oracle_lib()
+    opt = {"value": cpp["optimize_us"], "p99_us": cpp["optimize_p99_us"], "unit": "us/call",
+           "calls": cpp["optimize_calls"],
+           "api": "miso_b200_optimize from C++ (one instance per call, host pointers; search-only request to the resident server)",
+           "data": "acceptance_test.cpp:72-85 mixes, DetRng(0xacce91), m ~ U{1..7}"}
+    if have_ref and not args.no_cpu_baseline:
+        r = ol.Ref()
+        r.optimize_batch(o_sp, o_off, threads=1)  # warm
+        t0 = time.perf_counter()
+        w_ent, _, w_obj = r.optimize_batch(o_sp, o_off, threads=1)
+        opt["cpu_baseline"] = {"value": (time.perf_counter() - t0) / n_opt * 1e6, "unit": "us/call",
+                               "cores": 1, "kind": "reference",
+                               "sample": f"the same {n_opt} mixes, optimize_partition per instance, 1 thread"}
+        ok = bool(np.array_equal(g_ent, w_ent.astype(np.int32)) and bits_equal(g_obj, w_obj))
+        opt["parity"] = {"checked_against": "oracle/_ref optimize_partition", "instances": n_opt,
+                         "entry_and_objective_bits_equal": ok, "ok": ok}
+    res["optimize_partition"] = opt
     if ol.have_ref() and not args.no_cpu_baseline:
         sec, ref_acc = ol.Ref().c1_time(K)
         res["cpu_baseline"] = {"value": sec / K * 1e6, "unit": "us/decision", "cores": 1,

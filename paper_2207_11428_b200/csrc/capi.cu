@@ -348,17 +348,32 @@ int miso_b200_optimize_batch_host(miso_b200_ctx* ctx, const double* speeds,
   return MISO_B200_OK;
 }
 
+static int run_decide_request(miso_b200_ctx* ctx, const DecideOneArgs& a, int pub_m);
+
 int miso_b200_optimize(miso_b200_ctx* ctx, const double* speeds, int m, int* entry,
                        uint8_t* place, double* obj) {
   if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
   if (m < 1 || m > 7)
     return fail(MISO_B200_E_INVALID, "optimize_partition needs 1..7 jobs, got " + std::to_string(m));
   if (!speeds) return fail(MISO_B200_E_INVALID, "null speeds");
-  uint32_t offs[2] = {0, static_cast<uint32_t>(m)};
-  uint8_t c = 0;
-  double o = 0;
-  int rc = miso_b200_optimize_batch_host(ctx, speeds, offs, 1, &c, &o);
-  if (rc) return rc;
+  DeviceGuard g(ctx->device);
+  // One instance is a latency problem: it goes to the resident decision server as a
+  // search-only request (one PCIe round trip), not through the batch pipeline.
+  DecideOneArgs a;
+  std::memset(&a, 0, sizeof(a));
+  double* sp = &a.truth[0][0];
+  const int stride = m == 1 ? 5 : 4;  // only the m = 1 entry "7g" reads a 7g speed
+  for (int j = 0; j < m; ++j)
+    for (int k = 0; k < stride; ++k) sp[j * stride + k] = speeds[5 * j + k];
+  a.en0 = ctx->en0;
+  a.en1 = ctx->en1;
+  a.seq = ++ctx->decide_seq;
+  a.m = m;
+  a.noisy = kSearchOnly;
+  if (int rc = run_decide_request(ctx, a, 0)) return rc;
+  const DecideOneOut* h = static_cast<const DecideOneOut*>(ctx->h_stage);
+  const uint8_t c = static_cast<uint8_t>(h->cand);
+  const double o = h->obj;
   if (c == MISO_B200_CAND_INFEASIBLE) return 0;
   int e = -1, mm = 0;
   uint8_t p[7];
@@ -420,38 +435,16 @@ int miso_b200_decide_batch(miso_b200_ctx* ctx, const double* truth3, const uint8
   return MISO_B200_OK;
 }
 
-int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
-                     const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
-                     double target_mae, int* entry, uint8_t* place, double* obj, double* est5) {
-  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
-  if (m < 1 || m > 7)
-    return fail(MISO_B200_E_INVALID, "optimize_partition needs 1..7 jobs, got " + std::to_string(m));
-  if (int rc = check_predictor(mode, target_mae)) return rc;
-  DeviceGuard g(ctx->device);
-  // Latency path: the roster goes by value in the launch, results come back through mapped
-  // pinned memory, completion is a sequence number the kernel stores last (decide_one_kernel).
+// One single-roster request (args filled in, a.seq assigned) through the resident server or
+// one decide_one_kernel launch; returns once the result record in ctx->h_stage answers it.
+// pub_m: the est rows the device publishes with the header (0 for search-only requests).
+static int run_decide_request(miso_b200_ctx* ctx, const DecideOneArgs& a, int pub_m) {
   if (!ctx->h_stage) {
     CUDA_TRY(cudaHostAlloc(&ctx->h_stage, sizeof(DecideOneOut), cudaHostAllocMapped));
     CUDA_TRY(cudaHostGetDevicePointer(&ctx->d_stage, ctx->h_stage, 0));
     std::memset(ctx->h_stage, 0, sizeof(DecideOneOut));
   }
   if (!ctx->streams[0]) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->streams[0], cudaStreamNonBlocking));
-  DecideOneArgs a;
-  std::memset(&a, 0, sizeof(a));
-  for (int c = 0; c < m; ++c) {
-    for (int k = 0; k < 3; ++k) a.truth[c][k] = truth3[3 * c + k];
-    a.mem[c] = mem_gb[c];
-    a.qos[c] = qos_kind[c];
-  }
-  default_model(a.w2, a.w1);
-  a.target_mae = target_mae;
-  a.nonce = nonce;
-  a.rng_seed = rng_seed;
-  a.en0 = ctx->en0;
-  a.en1 = ctx->en1;
-  a.seq = ++ctx->decide_seq;
-  a.m = m;
-  a.noisy = mode;
   DecideOneOut* h = static_cast<DecideOneOut*>(ctx->h_stage);
   // The result record is accepted once it names this request and its check word matches
   // (decide_publish: the device stores it without a fence).
@@ -459,7 +452,7 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
   auto answered = [&]() {
     if (hw[kOutSeq] != a.seq) return false;
     uint64_t sum = 0;
-    for (int i = 0; i < kOutEst + 5 * m; ++i)
+    for (int i = 0; i < kOutEst + 5 * pub_m; ++i)
       if (i != kOutCheck) sum += mbx_mix(hw[i], uint64_t(i));
     return sum == hw[kOutCheck];
   };
@@ -516,6 +509,37 @@ int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* me
     }
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  return MISO_B200_OK;
+}
+
+int miso_b200_decide(miso_b200_ctx* ctx, const double* truth3, const uint8_t* mem_gb,
+                     const int8_t* qos_kind, int m, uint64_t nonce, uint64_t rng_seed, int mode,
+                     double target_mae, int* entry, uint8_t* place, double* obj, double* est5) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (m < 1 || m > 7)
+    return fail(MISO_B200_E_INVALID, "optimize_partition needs 1..7 jobs, got " + std::to_string(m));
+  if (int rc = check_predictor(mode, target_mae)) return rc;
+  DeviceGuard g(ctx->device);
+  // Latency path: the roster goes by value in the launch, results come back through mapped
+  // pinned memory, completion is a sequence number the kernel stores last (decide_one_kernel).
+  DecideOneArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int c = 0; c < m; ++c) {
+    for (int k = 0; k < 3; ++k) a.truth[c][k] = truth3[3 * c + k];
+    a.mem[c] = mem_gb[c];
+    a.qos[c] = qos_kind[c];
+  }
+  default_model(a.w2, a.w1);
+  a.target_mae = target_mae;
+  a.nonce = nonce;
+  a.rng_seed = rng_seed;
+  a.en0 = ctx->en0;
+  a.en1 = ctx->en1;
+  a.seq = ++ctx->decide_seq;
+  a.m = m;
+  a.noisy = mode;
+  if (int rc = run_decide_request(ctx, a, m)) return rc;
+  const DecideOneOut* h = static_cast<const DecideOneOut*>(ctx->h_stage);
   if (est5) std::memcpy(est5, h->est, sizeof(double) * 5 * m);
   if (h->cand == MISO_B200_CAND_INFEASIBLE) return 0;
   int e = -1, mm = 0;

@@ -24,6 +24,9 @@ cudaError_t launch_decide(const double* truth3, const uint8_t* mem_gb, const int
 // pinned memory with no fences: each side covers its words with a check word (the sum of
 // mbx_mix over the words), and the reader accepts a record only when the check matches, so a
 // record read while it is being written (torn) is simply read again.
+// noisy == kSearchOnly: an optimize_partition request (miso_b200_optimize). The job speeds
+// replace truth/w2/w1/target_mae: 4 per job (1g..4g) packed from truth[0][0], or 5 for m = 1.
+constexpr int kSearchOnly = 2;
 struct DecideOneArgs {
   double truth[7][3];  // (f7, f4, f3) per job
   double w2[4], w1[4];
@@ -47,6 +50,8 @@ struct DecideMailbox {
   uint64_t check;      // sum of mbx_mix over the kArgWords words of args
   uint64_t stop;       // nonzero: the server exits
 };
+static_assert(__builtin_offsetof(DecideOneArgs, target_mae) == 29 * 8,
+              "search-only requests pack up to 29 speeds over truth/w2/w1");
 constexpr int kArgWords = static_cast<int>(sizeof(DecideOneArgs) / 8);
 constexpr int kArgSeqWord = static_cast<int>(__builtin_offsetof(DecideOneArgs, seq) / 8);
 constexpr int kOutWords = static_cast<int>(sizeof(DecideOneOut) / 8);

@@ -206,6 +206,25 @@ __device__ __forceinline__ void decide_one_body(const DecideOneArgs& a, DecideOn
   __shared__ double s_pert[7][2];
   const int lane = threadIdx.x;
   const int m = a.m;
+  if (a.noisy == kSearchOnly) {  // optimize_partition alone: the speeds come packed in the args
+    const double* sp = &a.truth[0][0];
+    const int stride = m == 1 ? 5 : 4;  // 7g is used by the m = 1 entry "7g" only
+    if (lane < 7) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        o.est[lane * 5 + k] = lane < m && (k < 4 || m == 1) ? sp[lane * stride + k] : 0.0;
+    }
+    __syncwarp();
+    double ob;
+    const uint8_t c = warp_search(o.est, m, a.en0, a.en1, place, &ob);
+    if (lane == 0) {
+      o.cand = c;
+      o.obj = ob;
+      o.seq = a.seq;
+    }
+    __syncwarp();
+    return;
+  }
   const long long c0 = clock64();
   // perturbed 4g / 3g entries (profiles.hpp:234-244), one per lane
   if (lane < 2 * m) {
@@ -278,7 +297,7 @@ __device__ __forceinline__ void decide_publish(const DecideOneOut& o, DecideOneO
 __global__ void __launch_bounds__(32) decide_one_kernel(DecideOneArgs a, DecideOneOut* out) {
   __shared__ DecideOneOut s_o;
   decide_one_body(a, s_o, kCandPlaceD);
-  decide_publish(s_o, out, a.m);
+  decide_publish(s_o, out, a.noisy == kSearchOnly ? 0 : a.m);  // search-only: header alone
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -462,6 +481,14 @@ __global__ void __launch_bounds__(64) decide_server_kernel(const DecideMailbox* 
       __syncwarp();
       const uint64_t ts1 = stamps ? global_ns() : 0;
       const long long c1 = clock64();
+      if (s_a.noisy == kSearchOnly) {  // optimize_partition request: no predictor, no draw-ahead
+        decide_one_body(s_a, s_o, s_place);
+        decide_publish(s_o, out, 0);
+        last = seq;
+        __syncwarp();
+        t_last = global_ns();
+        return false;
+      }
       NoiseDraw mine = pre;
       bool hit = false;
       if (s_a.noisy) {

@@ -62,6 +62,47 @@ def test_literal_cases_dropin(ctx, golden):
     assert r.partition_name == "3g+3g" and abs(r.objective - 1.35) < 1e-12
 
 
+@pytest.mark.parametrize("server", [True, False])
+@pytest.mark.parametrize("name", ["opt_accept_acce91", "opt_ties_71e5"])
+def test_scalar_optimize_golden(ctx, golden, oracle, name, server):
+    """miso_b200_optimize (the scalar optimize_partition drop-in: one search-only request per
+    call to the resident decision server, or one decide_one_kernel launch per call with the
+    server disabled) instance by instance against the golden decisions, then against the oracle
+    on instances with NaN / inf / -0 / subnormal / > 1 speeds in every slot."""
+    import paper_2207_11428_b200 as m
+    g = np.load(golden / f"{name}.npz")
+    off = g["offsets"].astype(np.int64)
+    sp = g["speeds"].reshape(-1, 5)
+    m.lib.miso_b200_decide_server(ctx._h, 2000 if server else 0)
+    try:
+        n = min(len(off) - 1, 600)
+        for i in range(n):
+            jobs = [(f"j{j}", sp[off[i] + j]) for j in range(off[i + 1] - off[i])]
+            r = ctx.optimize_partition(jobs)
+            if g["entry"][i] < 0:
+                assert r is None, i
+                continue
+            assert r.entry == g["entry"][i], i
+            assert [a.slice for a in r.assignments] == list(g["place"][off[i]:off[i + 1]]), i
+            assert bits(r.objective) == bits(g["obj"][i]), i
+        rng = np.random.default_rng(5)
+        specials = np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, 5e-324, 1.5, 1e300, -1.0])
+        for t in range(300):
+            mm = int(rng.integers(1, 8))
+            s5 = rng.uniform(0.05, 1.0, (mm, 5))
+            hit = rng.random((mm, 5)) < 0.15
+            s5[hit] = rng.choice(specials, int(hit.sum()))
+            e, p, o = oracle.optimize_batch(s5.reshape(-1), np.array([0, mm], np.uint32))
+            r = ctx.optimize_partition([(f"j{j}", s5[j]) for j in range(mm)])
+            if e[0] < 0:
+                assert r is None, t
+                continue
+            assert r.entry == e[0] and [a.slice for a in r.assignments] == list(p[:mm]), t
+            assert bits(r.objective) == bits(o[0]), t
+    finally:
+        m.lib.miso_b200_decide_server(ctx._h, 2000)
+
+
 def test_job_count_out_of_range(ctx):
     with pytest.raises(ValueError):
         ctx.optimize_partition([])
