@@ -73,6 +73,23 @@ int miso_b200_candidate(const miso_b200_ctx* ctx, int cand, int* entry, int* m, 
 int miso_b200_optimize_batch(miso_b200_ctx* ctx, const double* speeds, const uint32_t* offsets,
                              uint64_t n, uint8_t* cand, double* obj, void* stream);
 
+/* One batch for miso_b200_optimize_batches: the arguments of miso_b200_optimize_batch. */
+typedef struct miso_b200_batch {
+  const double* speeds;
+  const uint32_t* offsets;
+  uint64_t n;
+  uint8_t* cand;
+  double* obj;
+} miso_b200_batch;
+
+/* miso_b200_optimize_batch over n_batches independent batches (DEVICE pointers, each with the
+ * contract above) in one stream-ordered call: up to 32 batches share one persistent-kernel
+ * launch, so a queue of batches pays the launch's fixed cost (grid start, first-tile latency,
+ * CTA tail) once instead of per batch. Outputs are the same bytes as one call per batch. The
+ * descriptor array is read during the call (host memory; it may be reused on return). */
+int miso_b200_optimize_batches(miso_b200_ctx* ctx, const miso_b200_batch* batches,
+                               int n_batches, void* stream);
+
 /* Same contract with HOST pointers: chunked H2D -> search -> D2H pipeline over two streams.
  * Synchronous. Offsets are validated chunk by chunk as the pipeline advances: on
  * MISO_B200_E_MALFORMED, results of instances before the offending chunk may have been written. */

@@ -13,6 +13,7 @@ from ._native import (  # noqa: F401
     NUM_CANDIDATES,
     Assignment,
     AssignmentVector,
+    BatchList,
     Context,
     MisoError,
     default_model,
@@ -26,7 +27,7 @@ from .sim import (DeviceTraceBatch, SimOptions, Trace, TraceBatch, best_static_p
 from . import tracefile  # noqa: F401,E402
 
 __all__ = [
-    "Context", "Assignment", "AssignmentVector", "MisoError", "DEFAULT_CATALOG",
+    "Context", "BatchList", "Assignment", "AssignmentVector", "MisoError", "DEFAULT_CATALOG",
     "partition_name", "CAND_INFEASIBLE", "CAND_BAD_M", "NUM_CANDIDATES", "KIND_NAMES",
     "SimOptions", "Trace", "TraceBatch", "DeviceTraceBatch", "generate_trace", "generate_traces",
     "generate_traces_device", "simulate_batch", "best_static_partition", "render_log", "tracefile",

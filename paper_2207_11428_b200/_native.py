@@ -54,6 +54,7 @@ def _load():
     L.miso_b200_candidate.argtypes = [vp, i32, C.POINTER(i32), C.POINTER(i32), vp]
     L.miso_b200_optimize_batch.argtypes = [vp, vp, vp, u64, vp, vp, vp]
     L.miso_b200_optimize_batch_host.argtypes = [vp, vp, vp, u64, vp, vp]
+    L.miso_b200_optimize_batches.argtypes = [vp, vp, i32, vp]
     L.miso_b200_optimize.argtypes = [vp, vp, i32, C.POINTER(i32), vp, vp]
     L.miso_b200_default_model.argtypes = [vp, vp]
     L.miso_b200_predict_batch.argtypes = [vp, vp, u64, i32, u64, u64, i32, C.c_double, vp, vp,
@@ -100,6 +101,31 @@ class AssignmentVector:
     @property
     def partition_name(self) -> str:
         return partition_name(self.partition)
+
+
+class _BatchC(C.Structure):
+    """miso_b200_batch (include/miso_b200.h)."""
+    _fields_ = [("speeds", C.c_void_p), ("offsets", C.c_void_p), ("n", C.c_uint64),
+                ("cand", C.c_void_p), ("obj", C.c_void_p)]
+
+
+class BatchList:
+    """The miso_b200_batch descriptors of a list of (speeds, offsets, cand, obj) CUDA tensor
+    tuples, checked once (the tensors must outlive the list)."""
+
+    def __init__(self, batches):
+        self.arr = (_BatchC * max(1, len(batches)))()
+        self.n = len(batches)
+        self.device = None
+        self._keep = list(batches)
+        for i, (sp, off, cand, obj) in enumerate(batches):
+            n = len(off) - 1
+            _check_device_args(sp, off, cand, obj, n)
+            if self.device is None:
+                self.device = sp.device
+            elif sp.device != self.device:
+                raise ValueError("all batches must be on one device")
+            self.arr[i] = _BatchC(sp.data_ptr(), off.data_ptr(), n, cand.data_ptr(), obj.data_ptr())
 
 
 def _is_torch_cuda(x) -> bool:
@@ -198,6 +224,18 @@ class Context:
         _check(lib.miso_b200_optimize_batch_host(self._h, speeds.ctypes.data, offsets.ctypes.data,
                                                  n, cand.ctypes.data, obj.ctypes.data))
         return cand, obj
+
+    def optimize_batches(self, batches, stream=None):
+        """miso_b200_optimize_batches: several independent device batches, each a tuple
+        (speeds, offsets, cand, obj) of CUDA tensors as optimize_batch takes them, in one
+        stream-ordered call (up to 32 batches per persistent launch). `batches` may also be a
+        BatchList prepared once (checked descriptors, reusable across calls)."""
+        import torch
+        bl = batches if isinstance(batches, BatchList) else BatchList(batches)
+        if not bl.n:
+            return
+        s = stream if stream is not None else torch.cuda.current_stream(bl.device).cuda_stream
+        _check(lib.miso_b200_optimize_batches(self._h, C.cast(bl.arr, C.c_void_p), bl.n, s))
 
     def decode(self, cand: np.ndarray, offsets: np.ndarray):
         """Per-instance active-catalog entry (-1 nullopt, -2 bad m) and packed placement[sum m]."""

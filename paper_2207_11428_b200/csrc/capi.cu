@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -298,6 +299,26 @@ int miso_b200_optimize_batch(miso_b200_ctx* ctx, const double* speeds, const uin
   DeviceGuard g(ctx->device);
   CUDA_TRY(launch_optimize(speeds, offsets, n, cand, obj, ctx->en0, ctx->en1,
                            static_cast<cudaStream_t>(stream)));
+  return MISO_B200_OK;
+}
+
+static_assert(sizeof(miso_b200_batch) == sizeof(SearchBatch) &&
+                  offsetof(miso_b200_batch, obj) == offsetof(SearchBatch, obj),
+              "miso_b200_batch mirrors SearchBatch");
+
+int miso_b200_optimize_batches(miso_b200_ctx* ctx, const miso_b200_batch* batches,
+                               int n_batches, void* stream) {
+  if (!ctx) return fail(MISO_B200_E_INVALID, "null context");
+  if (n_batches < 0 || (n_batches > 0 && !batches)) return fail(MISO_B200_E_INVALID, "bad batch list");
+  for (int i = 0; i < n_batches; ++i) {
+    const miso_b200_batch& b = batches[i];
+    if (b.n && (!b.speeds || !b.offsets || !b.cand || !b.obj))
+      return fail(MISO_B200_E_INVALID, "null buffer in batch " + std::to_string(i));
+  }
+  if (n_batches == 0) return MISO_B200_OK;
+  DeviceGuard g(ctx->device);
+  CUDA_TRY(launch_optimize_batches(reinterpret_cast<const SearchBatch*>(batches), n_batches,
+                                   ctx->en0, ctx->en1, static_cast<cudaStream_t>(stream)));
   return MISO_B200_OK;
 }
 

@@ -6,6 +6,18 @@
 
 namespace miso_b200 {
 
+// One batch of independent instances for the search (device pointers).
+struct SearchBatch {
+  const double* speeds;
+  const uint32_t* offsets;
+  uint64_t n;
+  uint8_t* cand;
+  double* obj;
+};
+constexpr int kMaxPipeBatches = 32;  // batches per persistent-pipeline launch
+// Several batches in one persistent launch (queued batches share the launch's fixed cost).
+cudaError_t launch_optimize_batches(const SearchBatch* batches, int nb, uint64_t en0,
+                                    uint64_t en1, cudaStream_t stream);
 cudaError_t launch_optimize(const double* speeds, const uint32_t* offsets, uint64_t n,
                             uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
                             cudaStream_t stream);

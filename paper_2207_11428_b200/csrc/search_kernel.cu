@@ -171,13 +171,30 @@ struct PipeLayout {
   static constexpr size_t kBytes = kStageBytes * kS + 128;
 };
 
+// The batches of one launch (kernel parameter space, read with dynamic indices through
+// __grid_constant__): batch b owns global tiles tile0[b] .. tile0[b+1]-1 of kT instances each.
+struct PipeBatches {
+  const double* speeds[kMaxPipeBatches];
+  const uint32_t* offsets[kMaxPipeBatches];
+  uint8_t* cand[kMaxPipeBatches];
+  double* obj[kMaxPipeBatches];
+  uint64_t n[kMaxPipeBatches];
+  uint64_t tile0[kMaxPipeBatches + 1];
+  int nb;
+};
+
+// Advances a batch cursor to the batch that owns global tile `tile` (tiles only grow per thread).
+__device__ __forceinline__ int batch_of(const PipeBatches& B, uint64_t tile, int b) {
+  while (B.tile0[b + 1] <= tile) ++b;
+  return b;
+}
+
 // kPos: nibble m = position of job count m's bucket in the sorted tile (identity = ascending
 // m). Warps straddle bucket boundaries and run both paths, so an order that puts cheap m next
 // to expensive m shortens the slowest warp of a tile.
 template <int kT, int kS, int kCap, int kG, bool kAll, uint32_t kPos = 0x76543210u>
 __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
-    const double* __restrict__ speeds, const uint32_t* __restrict__ offsets, uint64_t n,
-    uint8_t* __restrict__ cand_out, double* __restrict__ obj_out, uint64_t en0, uint64_t en1) {
+    const __grid_constant__ PipeBatches B, uint64_t en0, uint64_t en1) {
   static_assert(kS % kG == 0, "each consumer group owns every kG-th stage");
   using L = PipeLayout<kT, kS, kCap>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -188,7 +205,7 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
   __shared__ uint8_t s_cand[kG][2][kT];
 
   const int tid = threadIdx.x;
-  const uint64_t ntiles = (n + kT - 1) / kT;
+  const uint64_t ntiles = B.tile0[B.nb];
   if (tid == 0) TRACE(4095);
   if (tid == 0) {
     for (int s = 0; s < kS; ++s) {
@@ -211,28 +228,40 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
   if (tid >= kT * kG) {
     // ------------------------------ producer warp ------------------------------
     const int lane = tid & 31;
+    // lane b: the end of batch b's speed rows (a TMA rounded up to 16 bytes stays inside it)
+    const uintptr_t my_end =
+        lane < B.nb ? reinterpret_cast<uintptr_t>(B.speeds[lane] +
+                                                  size_t(__ldg(B.offsets[lane] + B.n[lane])) * 5)
+                    : 0;
     uint32_t pre0 = 0, pre1 = 0;
-    const uintptr_t speeds_end =
-        reinterpret_cast<uintptr_t>(speeds + size_t(__ldg(offsets + n)) * 5);
+    int pre_b = 0, cur = 0;  // lane's prefetched tile batch / its batch cursor
     int k = 0;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
       if ((k & 31) == 0) {
         const uint64_t tl = tile + uint64_t(lane) * gridDim.x;
         if (tl < ntiles) {
-          const uint64_t t0l = tl * kT;
-          const uint64_t cl = n - t0l < uint64_t(kT) ? n - t0l : uint64_t(kT);
-          pre0 = __ldg(offsets + t0l);
-          pre1 = __ldg(offsets + t0l + cl);
+          cur = batch_of(B, tl, cur);
+          const uint64_t nl = B.n[cur];
+          const uint64_t t0l = (tl - B.tile0[cur]) * kT;
+          const uint64_t cl = nl - t0l < uint64_t(kT) ? nl - t0l : uint64_t(kT);
+          pre0 = __ldg(B.offsets[cur] + t0l);
+          pre1 = __ldg(B.offsets[cur] + t0l + cl);
+          pre_b = cur;
         }
       }
       const uint32_t o0 = __shfl_sync(0xffffffffu, pre0, k & 31);
       const uint32_t oend = __shfl_sync(0xffffffffu, pre1, k & 31);
+      const int b = __shfl_sync(0xffffffffu, pre_b, k & 31);
+      const uintptr_t speeds_end = __shfl_sync(0xffffffffu, my_end, b);
       const int st = k % kS;
       const uint32_t ph = (k / kS) & 1;
       if (lane == 0) {
         if (k >= kS) mbar_wait(&empty_bar[st], ph ^ 1);
         TRACE(k * 16 + 3);
-        const uint64_t t0 = tile * kT;
+        const double* speeds = B.speeds[b];
+        const uint32_t* offsets = B.offsets[b];
+        const uint64_t n = B.n[b];
+        const uint64_t t0 = (tile - B.tile0[b]) * kT;
         const uint32_t cnt = static_cast<uint32_t>(n - t0 < uint64_t(kT) ? n - t0 : uint64_t(kT));
         unsigned char* base = stage_base(st);
         uint32_t* so = reinterpret_cast<uint32_t*>(base);
@@ -281,8 +310,11 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
   const int ct = tid % kT;  // thread within group
   const int lane = tid & 31;
   int k = 0;  // this group's tile count; it owns CTA tile numbers kk = g, g+kG, ...
+  int b = 0;  // batch cursor
   uint64_t prev_t0 = 0;
   int prev_cnt = 0;
+  uint8_t* prev_cand = nullptr;
+  double* prev_obj = nullptr;
   for (uint64_t tile = blockIdx.x + uint64_t(g) * gridDim.x; tile < ntiles;
        tile += uint64_t(kG) * gridDim.x) {
     const int kk = k * kG + g;
@@ -290,11 +322,14 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     const int st = kk % kS;
     const uint32_t ph = (kk / kS) & 1;
     const int p = k & 1;
+    b = batch_of(B, tile, b);
+    const double* speeds = B.speeds[b];
+    const uint64_t n = B.n[b];
     mbar_wait(&full_bar[st], ph);
     if (ct == 0) TRACE(kk * 16 + 6);
     const unsigned char* base = stage_base(st);
     const uint32_t* so = reinterpret_cast<const uint32_t*>(base);
-    const uint64_t t0 = tile * kT;
+    const uint64_t t0 = (tile - B.tile0[b]) * kT;
     const int cnt = static_cast<int>(n - t0 < uint64_t(kT) ? n - t0 : uint64_t(kT));
     const uint32_t j0 = so[0], oend = so[cnt];
     const uint32_t njobs = oend - j0;
@@ -311,19 +346,19 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     named_bar_sync(1 + g, kT);
     // Everyone finished the previous tile: flush its decisions (coalesced) from buffer p^1.
     if (ct < prev_cnt) {
-      cand_out[prev_t0 + ct] = s_cand[g][p ^ 1][ct];
-      obj_out[prev_t0 + ct] = s_obj[g][p ^ 1][ct];
+      prev_cand[prev_t0 + ct] = s_cand[g][p ^ 1][ct];
+      prev_obj[prev_t0 + ct] = s_obj[g][p ^ 1][ct];
     }
     if (ct == 0) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) s_cnt[g][p ^ 1][q] = 0;
     }
     if (ct < cnt) {
-      int b = 0;
+      int bb = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        b += ((kPos >> (4 * q)) & 15) < ((kPos >> (4 * my_m)) & 15) ? s_cnt[g][p][q] : 0;
-      s_order[g][b + my_rank] = static_cast<uint16_t>(ct);
+        bb += ((kPos >> (4 * q)) & 15) < ((kPos >> (4 * my_m)) & 15) ? s_cnt[g][p][q] : 0;
+      s_order[g][bb + my_rank] = static_cast<uint16_t>(ct);
     }
     named_bar_sync(1 + g, kT);
     if (ct < cnt) {
@@ -344,18 +379,19 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
     if (ct == 0) TRACE(kk * 16 + 7);
     prev_t0 = t0;
     prev_cnt = cnt;
+    prev_cand = B.cand[b];
+    prev_obj = B.obj[b];
   }
   named_bar_sync(1 + g, kT);
   if (ct < prev_cnt) {
     const int p = k & 1;
-    cand_out[prev_t0 + ct] = s_cand[g][p][ct];
-    obj_out[prev_t0 + ct] = s_obj[g][p][ct];
+    prev_cand[prev_t0 + ct] = s_cand[g][p][ct];
+    prev_obj[prev_t0 + ct] = s_obj[g][p][ct];
   }
 }
 
 template <int kT, int kS, int kCap, int kG, bool kAll, uint32_t kPos = 0x76543210u>
-cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint64_t n,
-                            uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
+cudaError_t launch_pipe_cfg(const SearchBatch* batches, int nb, uint64_t en0, uint64_t en1,
                             cudaStream_t stream) {
   using L = PipeLayout<kT, kS, kCap>;
   auto kern = optimize_pipe_kernel<kT, kS, kCap, kG, kAll, kPos>;
@@ -370,7 +406,27 @@ cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint6
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT * kG + 32, L::kBytes);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const uint64_t tiles = (n + kT - 1) / kT;
+  PipeBatches B;
+  B.nb = nb;
+  B.tile0[0] = 0;
+  for (int i = 0; i < nb; ++i) {
+    B.speeds[i] = batches[i].speeds;
+    B.offsets[i] = batches[i].offsets;
+    B.cand[i] = batches[i].cand;
+    B.obj[i] = batches[i].obj;
+    B.n[i] = batches[i].n;
+    B.tile0[i + 1] = B.tile0[i] + (batches[i].n + kT - 1) / kT;
+  }
+  for (int i = nb; i < kMaxPipeBatches; ++i) {
+    B.speeds[i] = nullptr;
+    B.offsets[i] = nullptr;
+    B.cand[i] = nullptr;
+    B.obj[i] = nullptr;
+    B.n[i] = 0;
+    B.tile0[i + 1] = B.tile0[nb];
+  }
+  const uint64_t tiles = B.tile0[nb];
+  if (tiles == 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>(tiles < uint64_t(grid_cap) ? tiles : uint64_t(grid_cap));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -382,7 +438,7 @@ cudaError_t launch_pipe_cfg(const double* speeds, const uint32_t* offsets, uint6
   attr[0].val.programmaticStreamSerializationAllowed = use_pdl() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, speeds, offsets, n, cand, obj, en0, en1);
+  return cudaLaunchKernelEx(&cfg, kern, B, en0, en1);
 }
 
 // MISO_B200_PIPE_CFG selects a tile/stage/group configuration (tuning only).
@@ -396,15 +452,15 @@ static int pipe_cfg() {
 }
 
 template <bool kAll>
-cudaError_t launch_pipe(const double* speeds, const uint32_t* offsets, uint64_t n, uint8_t* cand,
-                        double* obj, uint64_t en0, uint64_t en1, cudaStream_t stream) {
+cudaError_t launch_pipe(const SearchBatch* bs, int nb, uint64_t en0, uint64_t en1,
+                        cudaStream_t stream) {
   switch (pipe_cfg()) {
-    case 1: return launch_pipe_cfg<128, 8, 640, 4, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
-    case 2: return launch_pipe_cfg<128, 6, 640, 3, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
-    case 3: return launch_pipe_cfg<256, 4, 1280, 2, kAll>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    case 1: return launch_pipe_cfg<128, 8, 640, 4, kAll>(bs, nb, en0, en1, stream);
+    case 2: return launch_pipe_cfg<128, 6, 640, 3, kAll>(bs, nb, en0, en1, stream);
+    case 3: return launch_pipe_cfg<256, 4, 1280, 2, kAll>(bs, nb, en0, en1, stream);
     // bucket order 3,2,5,7,6,1,4 (bad m last): adjacent buckets pair cheap and expensive
     // searches (max adjacent cost 268 vs 361 for ascending m; costs ~ candidates + loads)
-    default: return launch_pipe_cfg<256, 4, 1280, 2, kAll, 0x34260157u>(speeds, offsets, n, cand, obj, en0, en1, stream);
+    default: return launch_pipe_cfg<256, 4, 1280, 2, kAll, 0x34260157u>(bs, nb, en0, en1, stream);
   }
 }
 
@@ -427,17 +483,43 @@ cudaError_t launch_tile(const double* speeds, const uint32_t* offsets, uint64_t 
 
 constexpr uint64_t kAllEn0 = ~0ull, kAllEn1 = (1ull << (kNumCands - 64)) - 1;
 
+cudaError_t launch_optimize_batches(const SearchBatch* batches, int nb, uint64_t en0,
+                                    uint64_t en1, cudaStream_t stream) {
+  const bool all = en0 == kAllEn0 && en1 == kAllEn1;
+  // 16-byte aligned batches go through the TMA pipeline, up to kMaxPipeBatches per launch;
+  // the rest (or MISO_B200_SIMPLE_SEARCH=1) through the one-shot tile kernel.
+  SearchBatch piped[kMaxPipeBatches];
+  int np = 0;
+  auto flush = [&]() -> cudaError_t {
+    cudaError_t e = np ? (all ? launch_pipe<true>(piped, np, en0, en1, stream)
+                              : launch_pipe<false>(piped, np, en0, en1, stream))
+                       : cudaSuccess;
+    np = 0;
+    return e;
+  };
+  for (int i = 0; i < nb; ++i) {
+    const SearchBatch& bt = batches[i];
+    if (bt.n == 0) continue;
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(bt.speeds) | reinterpret_cast<uintptr_t>(bt.offsets)) & 15) == 0;
+    if (aligned && !force_simple_path()) {
+      piped[np++] = bt;
+      if (np == kMaxPipeBatches)
+        if (cudaError_t e = flush()) return e;
+      continue;
+    }
+    cudaError_t e = all ? launch_tile<true>(bt.speeds, bt.offsets, bt.n, bt.cand, bt.obj, en0, en1, stream)
+                        : launch_tile<false>(bt.speeds, bt.offsets, bt.n, bt.cand, bt.obj, en0, en1, stream);
+    if (e) return e;
+  }
+  return flush();
+}
+
 cudaError_t launch_optimize(const double* speeds, const uint32_t* offsets, uint64_t n,
                             uint8_t* cand, double* obj, uint64_t en0, uint64_t en1,
                             cudaStream_t stream) {
-  if (n == 0) return cudaSuccess;
-  const bool all = en0 == kAllEn0 && en1 == kAllEn1;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(speeds) | reinterpret_cast<uintptr_t>(offsets)) & 15) == 0;
-  if (aligned && !force_simple_path())
-    return all ? launch_pipe<true>(speeds, offsets, n, cand, obj, en0, en1, stream)
-               : launch_pipe<false>(speeds, offsets, n, cand, obj, en0, en1, stream);
-  return all ? launch_tile<true>(speeds, offsets, n, cand, obj, en0, en1, stream)
-             : launch_tile<false>(speeds, offsets, n, cand, obj, en0, en1, stream);
+  const SearchBatch b{speeds, offsets, n, cand, obj};
+  return launch_optimize_batches(&b, 1, en0, en1, stream);
 }
 
 }  // namespace miso_b200

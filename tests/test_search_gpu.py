@@ -281,3 +281,41 @@ def test_spare_slice_table_matches_oracle(ctx, oracle):
             want = oracle.max_spare(list(kinds))
             got = ctx.max_spare_slice(list(kinds))
             assert (got if got is not None else -1) == want, (kinds, got, want)
+
+
+def test_optimize_batches_equal_per_batch_calls(ctx, oracle):
+    """miso_b200_optimize_batches: 40 batches (two launches of <= 32), empty batches, a batch
+    whose speeds are only 8-byte aligned (one-shot tile kernel), sizes that are not multiples
+    of the 256-instance tile, and one batch of 300k instances -- every batch's decisions and
+    objective bits equal a separate optimize_batch call, and a sample equals the oracle."""
+    import torch
+    rng = np.random.default_rng(11)
+    sizes = [int(x) for x in rng.integers(1, 5000, 37)] + [0, 300_000, 0]
+    rng.shuffle(sizes)
+    batches, want = [], []
+    for i, n in enumerate(sizes):
+        sp, off = oracle.gen_mixes(0x5EA + i, max(n, 1))
+        if n == 0:
+            sp, off = sp[:0], off[:1] * 0
+        d_sp = torch.from_numpy(sp).cuda()
+        if i == 5 and n:  # misaligned: an 8-byte offset view of a copy
+            buf = torch.zeros(len(sp) + 1, dtype=torch.float64, device="cuda")
+            buf[1:] = d_sp
+            d_sp = buf[1:]
+        d_off = torch.from_numpy(off.astype(np.int32)).cuda()
+        c, o = ctx.optimize_batch(d_sp, d_off)
+        want.append((c, o))
+        batches.append((d_sp, d_off, torch.full((max(n, 1),), 0xAB, dtype=torch.uint8, device="cuda"),
+                        torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")))
+    ctx.optimize_batches(batches)
+    torch.cuda.synchronize()
+    for i, ((sp, off, c, o), (wc, wo)) in enumerate(zip(batches, want)):
+        n = len(off) - 1
+        assert torch.equal(c[:n], wc[:n]), i
+        assert torch.equal(o[:n].view(torch.int64), wo[:n].view(torch.int64)), i
+        if n == 0:
+            assert int(c[0]) == 0xAB  # nothing written for an empty batch
+    i = next(j for j, n in enumerate(sizes) if n > 100 and j != 5)
+    sp, off = oracle.gen_mixes(0x5EA + i, sizes[i])
+    e, p, obj = oracle.optimize_batch(sp, off)
+    check_against(ctx, sp, off, e, p, obj, batches[i][2].cpu().numpy(), batches[i][3].cpu().numpy())
