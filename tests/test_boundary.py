@@ -5,6 +5,7 @@ import ctypes as C
 import re
 import subprocess
 import sys
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -98,3 +99,35 @@ def test_default_model_host_fit_matches_reference(golden):
     w2, w1 = m.default_model()
     assert np.array_equal(w2.view(np.uint64), g["w2"].view(np.uint64))
     assert np.array_equal(w1.view(np.uint64), g["w1"].view(np.uint64))
+
+
+def test_dropin_sim_binaries_never_reach_the_reference_engine(tmp_path):
+    """The reference's sim / experiment / acceptance test files, compiled with -fno-inline
+    against the B200 binding (tools/dropin), carry no symbol of the reference's CPU engine
+    (SimEngine members, run_simulation, best_static_partition, run_experiment[_in_memory],
+    optsta_search, run_trial_unit): every simulation they run goes to the device. Positive
+    control: the same flags on a file that calls the reference's run_simulation do emit them."""
+    import re
+    import shutil
+    import subprocess
+    bins = ROOT / "tools" / "dropin" / "_bin"
+    if not (bins / "sim_test_b200").exists() or not shutil.which("nm"):
+        pytest.skip("drop-in binaries not built")
+    pat = re.compile(r" miso::(SimEngine::|(run_simulation|best_static_partition|"
+                     r"run_experiment_in_memory|run_experiment|optsta_search|run_trial_unit)\()")
+    for name in ("sim", "experiment", "acceptance"):
+        syms = subprocess.run(["nm", "-C", str(bins / f"{name}_test_b200")], capture_output=True,
+                              text=True, check=True).stdout
+        hits = [ln for ln in syms.splitlines() if pat.search(ln)]
+        assert not hits, (name, hits[:5])
+        assert "miso::b200::" in syms, name
+    ref = Path("/root/reference/proj/include")
+    if ref.is_dir() and shutil.which("g++"):
+        src = tmp_path / "ctl.cpp"
+        src.write_text('#include "miso/sim.hpp"\nmiso::MetricsReport f(const miso::JobTrace& t) '
+                       '{ miso::SimOptions o; return miso::run_simulation(t, o); }\n')
+        obj = tmp_path / "ctl.o"
+        subprocess.run(["g++", "-std=c++20", "-O2", "-fno-inline", f"-I{ref}", "-c", str(src),
+                        "-o", str(obj)], check=True)
+        syms = subprocess.run(["nm", "-C", str(obj)], capture_output=True, text=True).stdout
+        assert pat.search(syms), "positive control: the reference engine's symbols must show"
