@@ -98,4 +98,6 @@ for rep in range(2):
     for mode in (False, True):
         batch(mode)
         out[f"{'pruned' if mode else 'full'}_{rep}"] = batch(mode)
+    batch_probes_full()
+    out[f"probes_full_{rep}"] = batch_probes_full()
 print(json.dumps(out))
