@@ -913,6 +913,26 @@ def sec_c5(args, D, ctx, runner, steps=10):
         ok = bool(np.array_equal(g_e, e.astype(np.int32)) and
                   bits_equal(obj[n - per_chunk: n - per_chunk + k].cpu().numpy(), o))
         par_search = {"instances": k, "chunk": chunks - 1, "ok": ok}
+    # every chunk, sampled: 2 x 1000 instances (its start and its middle) of each of this rank's
+    # chunks against the reference (one thread), decisions, placements and objective bits
+    samp_n = samp_bad = 0
+    if not args.no_cpu_baseline and oracle_lib().have_ref():
+        ref = oracle_lib().Ref()
+        for i in range(c_hi - c_lo):
+            for j0 in (0, per_chunk // 2):
+                a = i * per_chunk + j0
+                b = min(a + 1000, n)
+                o = offs[a:b + 1]
+                r0 = int(o[0])
+                o_loc = (o - r0).cpu().numpy().astype(np.uint32)
+                spd = sp[r0 * 5:(r0 + int(o_loc[-1])) * 5].cpu().numpy()
+                e, p, ob = ref.optimize_batch(spd, o_loc, threads=1)
+                g_e, g_p = ctx.decode(cand[a:b].cpu().numpy(), o_loc)
+                feas = np.repeat(e >= 0, np.diff(o_loc.astype(np.int64)))
+                ok = (np.array_equal(g_e, e.astype(np.int32)) and bits_equal(obj[a:b].cpu().numpy(), ob)
+                      and np.array_equal(g_p[feas], p[:len(feas)][feas]))
+                samp_n += b - a
+                samp_bad += 0 if ok else 1
     del sp, offs, cand, obj
     torch.cuda.empty_cache()
     # ---- trials: every seed of this rank's shard in one launch per policy ----
@@ -943,7 +963,7 @@ def sec_c5(args, D, ctx, runner, steps=10):
     # parity results live on the last rank: bring them to rank 0
     flags = D.reduce([0.0 if par_search is None else (1.0 if par_search["ok"] else -1.0),
                       0.0 if par_trials is None else (1.0 if par_trials["ok"] else -1.0),
-                      cpu_search, cpu_trials], "sum")
+                      cpu_search, cpu_trials, float(samp_n), float(samp_bad)], "sum")
     if D.rank != 0:
         return None
     r = allrows.reshape(S, 3)
@@ -970,9 +990,11 @@ def sec_c5(args, D, ctx, runner, steps=10):
     }
     if flags[0] != 0 or flags[1] != 0:
         res["parity"] = {"search_sample_of_last_chunk_ok": None if flags[0] == 0 else bool(flags[0] > 0),
+                         "every_chunk_sampled": {"instances": int(flags[4]), "chunks": chunks,
+                                                 "failed_samples": int(flags[5]), "ok": flags[5] == 0},
                          "last_16_trials_ok": None if flags[1] == 0 else bool(flags[1] > 0),
-                         "checked_against": "oracle/_ref (optimize_partition on 50k mixes of the last chunk; run_trial_unit-equivalent trials of the last 16 seeds)",
-                         "ok": bool(flags[0] >= 0 and flags[1] >= 0)}
+                         "checked_against": "oracle/_ref (optimize_partition on 50k mixes of the last chunk and on 2 x 1000 mixes of every chunk; run_trial_unit-equivalent trials of the last 16 seeds)",
+                         "ok": bool(flags[0] >= 0 and flags[1] >= 0 and flags[5] == 0)}
         threads = oracle_lib().host_threads()
         res["cpu_baseline"] = {"value": flags[2], "unit": "instances/s", "cores": threads,
                                "kind": "reference",
