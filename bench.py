@@ -951,7 +951,10 @@ def sec_c5(args, D, ctx, runner, steps=10):
     gen_s = time.perf_counter() - t0
     # the pruned static search wins at ~1k seeds per GPU (config 4), the full one at 8k
     pruned = (s_hi - s_lo) <= 2048
-    runner(traces[: min(len(traces), 64)], pruned=pruned)  # warm the three contexts' workspaces
+    # warm-up at full size: the contexts' workspaces grow to this shard's task counts here
+    # (cudaMalloc of up to tens of GB for the static search's candidate runs), not in the
+    # timed call
+    runner(traces, pruned=pruned)
     D.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
