@@ -183,6 +183,14 @@ struct PipeBatches {
   int nb;
 };
 
+#ifndef MISO_SEARCH_ALL_ARRIVE
+#define MISO_SEARCH_ALL_ARRIVE 0
+#endif
+// Arrivals that release a stage: one per consumer warp (lane 0 after __syncwarp), or one per
+// consumer thread with MISO_SEARCH_ALL_ARRIVE (the form compute-sanitizer racecheck can follow).
+template <int kT>
+constexpr uint32_t kEmptyArrivals = MISO_SEARCH_ALL_ARRIVE ? kT : kT / 32;
+
 // Advances a batch cursor to the batch that owns global tile `tile` (tiles only grow per thread).
 __device__ __forceinline__ int batch_of(const PipeBatches& B, uint64_t tile, int b) {
   while (B.tile0[b + 1] <= tile) ++b;
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
   if (tid == 0) {
     for (int s = 0; s < kS; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kT / 32);
+      mbar_init(&empty_bar[s], kEmptyArrivals<kT>);
     }
     fence_mbar_init();
   }
@@ -375,7 +383,11 @@ __global__ void __launch_bounds__(kT * kG + 32, 1) optimize_pipe_kernel(
       s_obj[g][p][l] = obj;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[st]);
+#if MISO_SEARCH_ALL_ARRIVE
+    mbar_arrive(&empty_bar[st]);  // every consumer thread releases its own reads
+#else
+    if (lane == 0) mbar_arrive(&empty_bar[st]);  // the warp's reads, ordered by __syncwarp
+#endif
     if (ct == 0) TRACE(kk * 16 + 7);
     prev_t0 = t0;
     prev_cnt = cnt;

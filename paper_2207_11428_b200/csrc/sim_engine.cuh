@@ -161,6 +161,18 @@ __shared__ double g_sim_rows[35];
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Single-writer update of a warp-uniform Ctx field (shared memory): every lane evaluates the
+// new value from the same state, the warp barrier orders all of those reads before lane 0's
+// store, and the second barrier orders the store before any later read. Plain stores of a
+// value that does not depend on the field itself stay all-lane (identical values).
+#define CTX_SET(field, value)             \
+  do {                                    \
+    const auto ctx_v_ = (value);          \
+    __syncwarp();                         \
+    if (lane_id() == 0) (field) = ctx_v_; \
+    __syncwarp();                         \
+  } while (0)
+
 __device__ __forceinline__ double s_from_us(int64_t us) { return static_cast<double>(us) * 1e-6; }
 __device__ __forceinline__ int64_t us_from_s(double s) {  // llround: half away from zero
   return static_cast<int64_t>(llround(s * 1e6));
@@ -209,7 +221,7 @@ struct Engine {
 
   static __device__ __forceinline__ void fail(int code) {
     Ctx& c = g_sim_ctx;
-    if (c.status == 0) c.status = code;
+    CTX_SET(c.status, c.status == 0 ? code : c.status);
   }
 
   // ---- event log (optional) -------------------------------------------------------------
@@ -235,7 +247,7 @@ struct Engine {
       c.log[c.log_n] = r;
     }
     __syncwarp();
-    ++c.log_n;
+    CTX_SET(c.log_n, c.log_n + 1);
   }
 
 
@@ -246,7 +258,7 @@ struct Engine {
     Slot s;
     s.t = t;
     s.pk = (static_cast<uint64_t>(prio) << 62) | (c.seq << 3) | kind;
-    ++c.seq;
+    CTX_SET(c.seq, c.seq + 1);
     c.slots[slot] = s;
     if (static_cast<unsigned>(slot - (lane_id() * c.chunk)) < static_cast<unsigned>(c.chunk)) {  // owner lane
       // keeps its minimum current
@@ -353,8 +365,8 @@ struct Engine {
     advance_job(j);
     if constexpr (PRUNE) {
     if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // retire the old-rate term
-      c.lb_p -= j.lbp;
-      c.lb_v -= j.rate / max_speed(j);
+      CTX_SET(c.lb_p, c.lb_p - (j.lbp));
+      CTX_SET(c.lb_v, c.lb_v - (j.rate / max_speed(j)));
     }
     }
     j.phase = phase;
@@ -364,22 +376,22 @@ struct Engine {
     if (progressing(phase)) {
       j.flags |= kRunState;
       if (j.first_progress_us < 0) j.first_progress_us = c.now;
-      if (c.first_progress < 0) c.first_progress = c.now;
+      if (c.first_progress < 0) CTX_SET(c.first_progress, c.now);
     }
     // the STP window's sums only need redoing from ji if the job's term actually changed
     const double re = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
     if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
       c.rate_eff[ji] = re;
       c.stp_dirty = true;
-      if (ji < c.stp_cmin) c.stp_cmin = ji;
+      CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
     }
     sync_jst(ji, j);
     if constexpr (PRUNE) {
     if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // remaining / mx, from now
       const double mx = max_speed(j);
       j.lbp = (j.remaining + j.rate * s_from_us(c.now)) / mx;
-      c.lb_p += j.lbp;
-      c.lb_v += j.rate / mx;
+      CTX_SET(c.lb_p, c.lb_p + (j.lbp));
+      CTX_SET(c.lb_v, c.lb_v + (j.rate / mx));
     }
     }
   }
@@ -438,7 +450,7 @@ struct Engine {
         c.stp_series[2 * c.stp_points + 1] = s;
       }
       __syncwarp();
-      ++c.stp_points;
+      CTX_SET(c.stp_points, c.stp_points + 1);
     }
   }
 
@@ -459,7 +471,7 @@ struct Engine {
     }
     c.queue[pos] = ji;
     __syncwarp();
-    ++c.qtail;
+    CTX_SET(c.qtail, c.qtail + 1);
   }
 
   // ---- GPU roster helpers -----------------------------------------------------------------
@@ -495,7 +507,7 @@ struct Engine {
     Ctx& c = g_sim_ctx;
     DJob& j = c.jobs[ji];
     if constexpr (PRUNE) {
-    if (c.prune && j.first_progress_us < 0) c.lb_unstarted -= runtime_floor_us(j);
+    if (c.prune && j.first_progress_us < 0) CTX_SET(c.lb_unstarted, c.lb_unstarted - runtime_floor_us(j));
     }
     const double r = c.efftruth[size_t(s) * c.J + ji];  // == true_rate(j, s)
     if (c.prm.check_invariants && !(r > 0)) fail(MISO_B200_SIM_INFEASIBLE_SLICE);
@@ -555,7 +567,7 @@ struct Engine {
       c.J_used = ci + 1;
       sync_jst(ci, j);
       if (ci + 1 > c.n_arrived) {
-        if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;
+        CTX_SET(c.stp_cmin, c.n_arrived < c.stp_cmin ? c.n_arrived : c.stp_cmin);
         c.n_arrived = ci + 1;
       }
       log_rec(kLogSpawn, -1, ci, 0, static_cast<uint32_t>(pi), 0, 0);
@@ -635,7 +647,7 @@ struct Engine {
       finish_profiling(gi);
       return;
     }
-    ++c.mps_sessions;
+    CTX_SET(c.mps_sessions, c.mps_sessions + 1);
     bool need_ckpt = false;
     if (c.prm.ckpt_us > 0)
       for (int i = 0; i < g.nroster; ++i)
@@ -665,7 +677,8 @@ struct Engine {
         cache_estimates(ji, c.jobs[ji].truth);
       }
     } else {
-      const uint64_t nonce = ++c.nonce;
+      const uint64_t nonce = c.nonce + 1;
+      CTX_SET(c.nonce, nonce);
       double e[5] = {0, 0, 0, 0, 0};
       const int ln = lane_id();
       if (ln < n) {
@@ -774,7 +787,7 @@ struct Engine {
       return;
     }
     if (!force && !(obj > g.objective + 1e-12)) return;
-    ++c.repartitions;
+    CTX_SET(c.repartitions, c.repartitions + 1);
     g.plan_obj = obj;
     g.plan_n = static_cast<uint8_t>(m);
 #pragma unroll
@@ -830,7 +843,7 @@ struct Engine {
       }
     }
     if (best < 0) return -1;
-    ++c.qhead;  // pop_queue: the placed job is always the queue head
+    CTX_SET(c.qhead, c.qhead + 1);  // pop_queue: the placed job is always the queue head
     DGpu& g = c.gpus[best];
     roster_push(g, ji);
     c.jobs[ji].gpu = static_cast<int16_t>(best);
@@ -854,7 +867,7 @@ struct Engine {
 
   static __device__ __forceinline__ void free_slot(int gi, int i) {
     Ctx& c = g_sim_ctx;
-    ++c.cap_gen;
+    CTX_SET(c.cap_gen, c.cap_gen + 1);
     DGpu& g = c.gpus[gi];
     const int k = g.slot_kind[i];
     g.slot_job[i] = -1;
@@ -895,7 +908,7 @@ struct Engine {
     DGpu& g = c.gpus[bg];
     int bi = 0;
     while (!(g.slot_kind[bi] == bk && g.slot_job[bi] == -1)) ++bi;
-    ++c.qhead;
+    CTX_SET(c.qhead, c.qhead + 1);
     occupy_slot(bg, bi, ji);
     roster_push(g, ji);
     DJob& jm = c.jobs[ji];
@@ -927,7 +940,7 @@ struct Engine {
     int b = best >= 0 ? best : INT32_MAX;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, off));
-    ++c.qhead;
+    CTX_SET(c.qhead, c.qhead + 1);
     DGpu& g = c.gpus[b];
     g.mode = kGpuMig;
     roster_push(g, ji);
@@ -1109,7 +1122,7 @@ struct Engine {
       m.slot = static_cast<int8_t>(si);
       m.slice = static_cast<uint8_t>(kind);
       sync_jst(best, m);
-      ++c.migrations;
+      CTX_SET(c.migrations, c.migrations + 1);
       log_rec(kLogMigrate, gi, best, static_cast<uint8_t>(kind), static_cast<uint32_t>(si), 0, 0);
       if (c.prm.ckpt_us > 0) {
         set_phase(best, kCkpt, 0.0);
@@ -1126,8 +1139,8 @@ struct Engine {
     DJob& j = c.jobs[ji];
     if constexpr (PRUNE) {
     if (c.prune) {  // the job's remaining-work term leaves with it
-      c.lb_p -= j.lbp;
-      c.lb_v -= j.rate / max_speed(j);
+      CTX_SET(c.lb_p, c.lb_p - (j.lbp));
+      CTX_SET(c.lb_v, c.lb_v - (j.rate / max_speed(j)));
     }
     }
     advance_job(j);
@@ -1141,12 +1154,14 @@ struct Engine {
     clear_slot(ji);
     c.rate_eff[ji] = 0.0;
     c.stp_dirty = true;
-    if (ji < c.stp_cmin) c.stp_cmin = ji;
+    CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
     sync_jst(ji, j);
-    while (c.stp_lo < c.n_arrived && (c.jst[c.stp_lo] & 64)) ++c.stp_lo;  // done bit, dense
+    int stp_lo = c.stp_lo;
+    while (stp_lo < c.n_arrived && (c.jst[stp_lo] & 64)) ++stp_lo;
+    CTX_SET(c.stp_lo, stp_lo);  // done bit, dense
     j.completion_us = c.now;
-    ++c.done_count;
-    if (c.now > c.last_completion) c.last_completion = c.now;
+    CTX_SET(c.done_count, c.done_count + 1);
+    CTX_SET(c.last_completion, c.now > c.last_completion ? c.now : c.last_completion);
     if (c.prm.check_invariants) {
       int64_t total = 0;
 #pragma unroll
@@ -1156,9 +1171,9 @@ struct Engine {
     const int64_t jct = c.now - j.arrival_us;
     if constexpr (PRUNE) {
     if (c.prune) {
-      c.lb_fin += jct;
-      --c.lb_narr;
-      c.lb_arrsum -= j.arrival_us;
+      CTX_SET(c.lb_fin, c.lb_fin + (jct));
+      CTX_SET(c.lb_narr, c.lb_narr - 1);
+      CTX_SET(c.lb_arrsum, c.lb_arrsum - (j.arrival_us));
     }
     }
     log_rec(kLogComplete, -1, ji, 0, static_cast<uint32_t>(jct & 0xFFFFFFFF),
@@ -1168,7 +1183,7 @@ struct Engine {
     roster_erase(g, ji);
     if constexpr (POL == MISO_B200_POLICY_NOPART) {
       g.mode = kGpuIdle;
-      ++c.cap_gen;
+      CTX_SET(c.cap_gen, c.cap_gen + 1);
     } else if constexpr (POL == MISO_B200_POLICY_OPTSTA) {
       free_slot(gi, j.slot);
       process_freed_slots(gi, j.slot);
@@ -1184,14 +1199,14 @@ struct Engine {
       const int ji = slot;
       if (kind == kEvArrival) {
         if (ji + 1 > c.n_arrived) {
-          if (c.n_arrived < c.stp_cmin) c.stp_cmin = c.n_arrived;  // new window entries need sums
+          CTX_SET(c.stp_cmin, c.n_arrived < c.stp_cmin ? c.n_arrived : c.stp_cmin);  // new window entries need sums
           c.n_arrived = ji + 1;
         }
         log_rec(kLogArrival, -1, ji, 0, 0, 0, 0);
     if constexpr (PRUNE) {
         if (c.prune) {
-          ++c.lb_narr;
-          c.lb_arrsum += c.now;  // == arrival_us
+          CTX_SET(c.lb_narr, c.lb_narr + 1);
+          CTX_SET(c.lb_arrsum, c.lb_arrsum + (c.now));  // == arrival_us
         }
     }
         enqueue(ji);
@@ -1473,13 +1488,14 @@ struct Engine {
       Slot ev;
       const int slot = next_event(&ev);
       if (slot < 0) break;
-      if (++c.processed > prm.max_events) {
+      CTX_SET(c.processed, c.processed + 1);
+      if (c.processed > prm.max_events) {
         c.status = MISO_B200_SIM_EVENT_BUDGET;
         break;
       }
       clear_slot(slot);
       __syncwarp();
-      c.stp_integral += c.stp_cur * s_from_us(ev.t - c.stp_last);
+      CTX_SET(c.stp_integral, c.stp_integral + (c.stp_cur * s_from_us(ev.t - c.stp_last)));
       c.stp_last = ev.t;
       c.now = ev.t;
       dispatch(slot, static_cast<uint32_t>(ev.pk & 7));
@@ -1504,7 +1520,7 @@ struct Engine {
     }
     // every pushed event is popped by the reference exactly once (live or stale), so its
     // max_events budget (sim.hpp:224, stale pops included) is exceeded iff the pushes exceed it
-    if (c.status == 0 && c.seq > prm.max_events) c.status = MISO_B200_SIM_EVENT_BUDGET;
+    CTX_SET(c.status, (c.status == 0 && c.seq > prm.max_events) ? MISO_B200_SIM_EVENT_BUDGET : c.status);
     if constexpr (PRUNE) {
     if (c.prune && c.status == 0 && c.done_count == JT && lane == 0)
       atomicMin(reinterpret_cast<long long*>(b.prune_bound + tr), static_cast<long long>(c.lb_fin));

@@ -1,6 +1,9 @@
 // sim_launch.cuh -- the simulator kernel and its launcher, included only by the per-policy TUs
 // (sim_pol_*.cu), each of which explicitly instantiates its policy.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
+
 #include "sim_engine.cuh"
 
 // Resident one-warp blocks per SM: the dynamic policies (miso, oracle) carry the predictor and
@@ -22,8 +25,45 @@ simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
   simk::Engine<POL, PRUNE>::run(b, prm, w);
 }
 
+// The engine uses ~2.5 KB of shared memory per block and lives on L1 hits (job records, event
+// slots, dense per-job arrays): the unified L1/shared array is split so that shared memory
+// holds exactly the resident blocks' records and the rest is L1.
+// MISO_B200_SIM_CARVEOUT=<percent shared> overrides it (-1 = the driver's default choice).
+inline int sim_carveout_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("MISO_B200_SIM_CARVEOUT");
+    v = e ? atoi(e) : -3;  // -3: computed per kernel
+  }
+  return v;
+}
+
 template <int POL, bool PRUNE>
 cudaError_t launch_sim(const SimBatch& b, const SimParams& p, const ModelW& w, cudaStream_t s) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    attr_set = true;
+    auto kern = simulate_kernel<POL, PRUNE>;
+    int pct = sim_carveout_env();
+    if (pct == -3) {
+      cudaFuncAttributes fa{};
+      int dev = 0, smem_sm = 0, blocks = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+      if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && smem_sm > 0 &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32, 0) == cudaSuccess) {
+        const size_t need = size_t(blocks) * (fa.sharedSizeBytes + 1024);  // + per-block reserve
+        pct = static_cast<int>(std::min<size_t>(100, (need * 100 + smem_sm - 1) / smem_sm));
+      } else {
+        pct = -1;
+      }
+    }
+    if (pct >= 0) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      if (e != cudaSuccess) return e;
+    }
+  }
   simulate_kernel<POL, PRUNE><<<b.n_seeds, 32, 0, s>>>(b, p, w);  // one warp (block) per task
   return cudaGetLastError();
 }

@@ -319,3 +319,27 @@ def test_optimize_batches_equal_per_batch_calls(ctx, oracle):
     sp, off = oracle.gen_mixes(0x5EA + i, sizes[i])
     e, p, obj = oracle.optimize_batch(sp, off)
     check_against(ctx, sp, off, e, p, obj, batches[i][2].cpu().numpy(), batches[i][3].cpu().numpy())
+
+
+def test_optimize_batches_catalog_subset(oracle):
+    """The queued entry on a context with a catalog subset (the kernel's masked-candidate
+    instantiation): each batch equals its own optimize_batch call."""
+    import torch
+    import paper_2207_11428_b200 as m
+    c = m.Context(0)
+    try:
+        full = c.catalog()
+        c.set_catalog(full[::3])
+        batches, want = [], []
+        for i, n in enumerate([3000, 1, 257, 4096]):
+            sp, off = oracle.gen_mixes(0x5B + i, n)
+            d_sp, d_off = torch.from_numpy(sp).cuda(), torch.from_numpy(off.astype(np.int32)).cuda()
+            want.append(c.optimize_batch(d_sp, d_off))
+            batches.append((d_sp, d_off, torch.empty(n, dtype=torch.uint8, device="cuda"),
+                            torch.empty(n, dtype=torch.float64, device="cuda")))
+        c.optimize_batches(m.BatchList(batches))
+        torch.cuda.synchronize()
+        for (_, _, cc, oo), (wc, wo) in zip(batches, want):
+            assert torch.equal(cc, wc) and torch.equal(oo.view(torch.int64), wo.view(torch.int64))
+    finally:
+        c.close()
