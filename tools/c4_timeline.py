@@ -55,7 +55,7 @@ def batch(chosen_only, chunks=1):
     return {"nopart": [f(a0), f(a1)], "miso": [f(c0), f(c1)], "static": [f(b0), f(b1)], "rerun": [f(b1), f(b2)]}
 
 
-def batch_probes_full():
+def batch_probes_full(rest_waits=False):
     """Probes in full mode (their metrics are the optsta result when one of them is chosen)
     beside the other candidates (JCT-only, pruned against the probes' bound) on a 4th stream."""
     t0 = ev(torch.cuda.current_stream())
@@ -75,6 +75,8 @@ def batch_probes_full():
     p_pr = miso.simulate_batch(ctx_b, traces, opts, task_trace=ti[probe].astype(np.int32),
                                static_partitions=cat[ee[probe]], stream=s_b, defer=True, prune_bound=bound)
     b1 = ev(s_b)
+    if rest_waits:  # the pruned rest starts once every trace's bound is set by its probes
+        s_d.wait_stream(s_b)
     d0 = ev(s_d)
     p_rest = miso.simulate_batch(ctx_d, traces, opts, task_trace=ti[~probe].astype(np.int32),
                                  static_partitions=cat[ee[~probe]], jct_only=True, stream=s_d, defer=True,
@@ -94,6 +96,20 @@ def batch_probes_full():
 
 
 out = {}
+if len(sys.argv) > 1 and sys.argv[1] == "probes":  # probes (full metrics) first, then the rest
+    for rep in range(2):
+        for w in (False, True):
+            batch_probes_full(w)
+            out[f"probes_full{'_then_rest' if w else ''}_{rep}"] = batch_probes_full(w)
+    print(json.dumps(out))
+    sys.exit(0)
+if len(sys.argv) > 1 and sys.argv[1] == "chunks":  # the static search split into sequential launches
+    for rep in range(2):
+        for ch in (1, 2, 4, 8):
+            batch(True, ch)
+            out[f"pruned_chunks{ch}_{rep}"] = batch(True, ch)
+    print(json.dumps(out))
+    sys.exit(0)
 for rep in range(2):
     for mode in (False, True):
         batch(mode)
