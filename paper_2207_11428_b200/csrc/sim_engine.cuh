@@ -137,7 +137,7 @@ struct Ctx {  // warp-uniform engine state: one record per block, in shared memo
   // for every job that has not started (see runtime_floor_us)
   bool prune;
   int64_t lb_fin, lb_narr, lb_arrsum, lb_unstarted;
-  // started, unfinished jobs: sum of remaining_work / max_speed in seconds, kept as
+  // started, unfinished jobs: sum of remaining_work / prune_mx in seconds, kept as
   // lb_p - lb_v * now_s with per-job terms (remaining + rate * t_update) / mx and rate / mx
   double lb_p, lb_v;
   // options
@@ -173,6 +173,14 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
     __syncwarp();                         \
   } while (0)
 
+// The pruned search's bound terms (Ctx::lb_*) are lane 0's alone: only lane 0 updates them and
+// only lane 0 evaluates the stop test (broadcast by a shuffle), so their updates need no warp
+// barriers.
+#define LB_SET(field, value)                    \
+  do {                                          \
+    if (lane_id() == 0) (field) = (value);      \
+  } while (0)
+
 __device__ __forceinline__ double s_from_us(int64_t us) { return static_cast<double>(us) * 1e-6; }
 __device__ __forceinline__ int64_t us_from_s(double s) {  // llround: half away from zero
   return static_cast<int64_t>(llround(s * 1e6));
@@ -184,19 +192,18 @@ __device__ __forceinline__ uint32_t pack_part(const uint8_t* p) {
   return p[0] | (p[1] << 4) | (p[2] << 8) | (p[3] << 12) | (p[4] << 16);
 }
 
-// Pruned best-static search (SimBatch::prune_bound). A job can never run faster than
-// max_speed (every rate is an effective true speed, <= truth[k]), so from any moment it needs
-// at least remaining / max_speed more seconds (migrations only add checkpoint pauses), and a
-// job that has not started needs at least base / max_speed (completions are scheduled
-// llround(remaining / rate * 1e6) us ahead: rounded down with margin).
-__device__ __forceinline__ double max_speed(const DJob& j) {  // >= any rate the job can get
-  double mx = 1.0;
-#pragma unroll
-  for (int k = 0; k < 5; ++k) mx = j.truth[k] > mx ? j.truth[k] : mx;
-  return mx;
-}
+// Pruned best-static search (SimBatch::prune_bound). Under optsta a job only ever runs in a slot
+// of the static partition, at that slot kind's effective true speed (start_running), so it can
+// never run faster than prune_mx = the largest effective true speed over the partition's kinds
+// (set once at init, kept in the job's est[0]: the estimates are unused under optsta, and pruned
+// runs have no clones). From any moment it therefore needs at least remaining / prune_mx more
+// seconds (migrations only add checkpoint pauses), and a job that has not started needs at least
+// base / prune_mx (completions are scheduled llround(remaining / rate * 1e6) us ahead: rounded
+// down with margin). A job no kind of the partition can run never completes (the run ends
+// incomplete); its floor uses 1.0, which is still a valid bound.
+__device__ __forceinline__ double prune_mx(const DJob& j) { return j.est[0]; }
 __device__ __forceinline__ int64_t runtime_floor_us(const DJob& j) {
-  const double us = j.base / max_speed(j) * 1e6 * (1.0 - 1e-12) - 2.0;
+  const double us = j.base / prune_mx(j) * 1e6 * (1.0 - 1e-12) - 2.0;
   return us > 0.0 ? static_cast<int64_t>(us) : 0;
 }
 
@@ -365,8 +372,8 @@ struct Engine {
     advance_job(j);
     if constexpr (PRUNE) {
     if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // retire the old-rate term
-      CTX_SET(c.lb_p, c.lb_p - (j.lbp));
-      CTX_SET(c.lb_v, c.lb_v - (j.rate / max_speed(j)));
+      LB_SET(c.lb_p, c.lb_p - (j.lbp));
+      LB_SET(c.lb_v, c.lb_v - (j.rate / prune_mx(j)));
     }
     }
     j.phase = phase;
@@ -388,10 +395,10 @@ struct Engine {
     sync_jst(ji, j);
     if constexpr (PRUNE) {
     if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // remaining / mx, from now
-      const double mx = max_speed(j);
+      const double mx = prune_mx(j);
       j.lbp = (j.remaining + j.rate * s_from_us(c.now)) / mx;
-      CTX_SET(c.lb_p, c.lb_p + (j.lbp));
-      CTX_SET(c.lb_v, c.lb_v + (j.rate / mx));
+      LB_SET(c.lb_p, c.lb_p + (j.lbp));
+      LB_SET(c.lb_v, c.lb_v + (j.rate / mx));
     }
     }
   }
@@ -507,7 +514,7 @@ struct Engine {
     Ctx& c = g_sim_ctx;
     DJob& j = c.jobs[ji];
     if constexpr (PRUNE) {
-    if (c.prune && j.first_progress_us < 0) CTX_SET(c.lb_unstarted, c.lb_unstarted - runtime_floor_us(j));
+    if (c.prune && j.first_progress_us < 0) LB_SET(c.lb_unstarted, c.lb_unstarted - runtime_floor_us(j));
     }
     const double r = c.efftruth[size_t(s) * c.J + ji];  // == true_rate(j, s)
     if (c.prm.check_invariants && !(r > 0)) fail(MISO_B200_SIM_INFEASIBLE_SLICE);
@@ -885,18 +892,37 @@ struct Engine {
   static __device__ bool admit_optsta(int ji) {
     Ctx& c = g_sim_ctx;
     if (ji == c.fail_job && c.fail_gen == c.cap_gen) return false;  // nothing freed since
+    const int lane = lane_id();
+    // the job's feasible kinds (true_rate > 0), one lane per kind: one load round trip
+    const bool fk = lane < 5 && c.efftruth[size_t(lane < 5 ? lane : 0) * c.J + ji] > 0;
+    const unsigned feas = __ballot_sync(0xffffffffu, fk);
     int bg = -1, bk = -1;
-    for (int k = 4; k >= 0 && bg < 0; --k) {
-      if (!(c.efftruth[size_t(k) * c.J + ji] > 0)) continue;  // == true_rate(j, k)
-      for (int w0 = 0; w0 < c.W && bg < 0; w0 += 32) {
-        const int wi = w0 + lane_id();
-        const uint32_t word = wi < c.W ? c.freemask[k * c.W + wi] : 0u;
-        const unsigned nz = __ballot_sync(0xffffffffu, word != 0);
-        if (nz) {
-          const int l = __ffs(nz) - 1;
-          const uint32_t wv = __shfl_sync(0xffffffffu, word, l);
-          bg = ((w0 + l) << 5) + __ffs(wv) - 1;
-          bk = k;
+    if (5 * c.W <= 32) {  // every kind's free-GPU words in one load (lane = k * W + word)
+      const uint32_t word = lane < 5 * c.W ? c.freemask[lane] : 0u;
+      const unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+      const unsigned grp = (1u << c.W) - 1u;
+      for (int k = 4; k >= 0; --k) {
+        const unsigned g = (nz >> (k * c.W)) & grp;
+        if (!((feas >> k) & 1u) || !g) continue;
+        const int l = k * c.W + __ffs(g) - 1;
+        const uint32_t wv = __shfl_sync(0xffffffffu, word, l);
+        bg = ((l - k * c.W) << 5) + __ffs(wv) - 1;
+        bk = k;
+        break;
+      }
+    } else {
+      for (int k = 4; k >= 0 && bg < 0; --k) {
+        if (!((feas >> k) & 1u)) continue;
+        for (int w0 = 0; w0 < c.W && bg < 0; w0 += 32) {
+          const int wi = w0 + lane;
+          const uint32_t word = wi < c.W ? c.freemask[k * c.W + wi] : 0u;
+          const unsigned nz = __ballot_sync(0xffffffffu, word != 0);
+          if (nz) {
+            const int l = __ffs(nz) - 1;
+            const uint32_t wv = __shfl_sync(0xffffffffu, word, l);
+            bg = ((w0 + l) << 5) + __ffs(wv) - 1;
+            bk = k;
+          }
         }
       }
     }
@@ -906,8 +932,10 @@ struct Engine {
       return false;
     }
     DGpu& g = c.gpus[bg];
-    int bi = 0;
-    while (!(g.slot_kind[bi] == bk && g.slot_job[bi] == -1)) ++bi;
+    // the GPU's first free slot of kind bk, one lane per slot
+    const bool fs = lane < g.nslots && g.slot_kind[lane < 7 ? lane : 0] == bk &&
+                    g.slot_job[lane < 7 ? lane : 0] == -1;
+    const int bi = __ffs(__ballot_sync(0xffffffffu, fs)) - 1;
     CTX_SET(c.qhead, c.qhead + 1);
     occupy_slot(bg, bi, ji);
     roster_push(g, ji);
@@ -1139,8 +1167,8 @@ struct Engine {
     DJob& j = c.jobs[ji];
     if constexpr (PRUNE) {
     if (c.prune) {  // the job's remaining-work term leaves with it
-      CTX_SET(c.lb_p, c.lb_p - (j.lbp));
-      CTX_SET(c.lb_v, c.lb_v - (j.rate / max_speed(j)));
+      LB_SET(c.lb_p, c.lb_p - (j.lbp));
+      LB_SET(c.lb_v, c.lb_v - (j.rate / prune_mx(j)));
     }
     }
     advance_job(j);
@@ -1171,9 +1199,9 @@ struct Engine {
     const int64_t jct = c.now - j.arrival_us;
     if constexpr (PRUNE) {
     if (c.prune) {
-      CTX_SET(c.lb_fin, c.lb_fin + (jct));
-      CTX_SET(c.lb_narr, c.lb_narr - 1);
-      CTX_SET(c.lb_arrsum, c.lb_arrsum - (j.arrival_us));
+      LB_SET(c.lb_fin, c.lb_fin + (jct));
+      LB_SET(c.lb_narr, c.lb_narr - 1);
+      LB_SET(c.lb_arrsum, c.lb_arrsum - (j.arrival_us));
     }
     }
     log_rec(kLogComplete, -1, ji, 0, static_cast<uint32_t>(jct & 0xFFFFFFFF),
@@ -1205,8 +1233,8 @@ struct Engine {
         log_rec(kLogArrival, -1, ji, 0, 0, 0, 0);
     if constexpr (PRUNE) {
         if (c.prune) {
-          CTX_SET(c.lb_narr, c.lb_narr + 1);
-          CTX_SET(c.lb_arrsum, c.lb_arrsum + (c.now));  // == arrival_us
+          LB_SET(c.lb_narr, c.lb_narr + 1);
+          LB_SET(c.lb_arrsum, c.lb_arrsum + (c.now));  // == arrival_us
         }
     }
         enqueue(ji);
@@ -1420,7 +1448,17 @@ struct Engine {
       for (int k = 0; k < 5; ++k) c.efftruth[size_t(k) * J + i] = effective_speed(j.truth[k], k, j.mem, j.qos);
       c.arr_us[i] = a;
       if constexpr (PRUNE)
-        if (c.prune) lb_unstarted += runtime_floor_us(j);
+        if (c.prune) {
+          const uint8_t* sc = b.static_counts + size_t(warp) * 5;
+          double mx = 0.0;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            const double r = c.efftruth[size_t(k) * J + i];
+            if (sc[k] > 0 && r > mx) mx = r;
+          }
+          j.est[0] = mx > 0.0 ? mx : 1.0;
+          lb_unstarted += runtime_floor_us(j);
+        }
       Slot s;  // arrival events pushed in job order: seq = j (sim.hpp:219)
       s.t = a;
       s.pk = (1ull << 62) | (static_cast<uint64_t>(i) << 3) | kEvArrival;
@@ -1484,12 +1522,13 @@ struct Engine {
     // ---- event loop (sim.hpp:221-233) ----
     if (bad_job && (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE))
       c.status = MISO_B200_SIM_INVARIANT;  // "fits no slice kind" (sim.hpp:381)
+    uint64_t processed = 0;  // warp-uniform, in a register (stored to Ctx after the loop)
     while (c.status == 0) {
       Slot ev;
       const int slot = next_event(&ev);
       if (slot < 0) break;
-      CTX_SET(c.processed, c.processed + 1);
-      if (c.processed > prm.max_events) {
+      ++processed;
+      if (processed > prm.max_events) {
         c.status = MISO_B200_SIM_EVENT_BUDGET;
         break;
       }
@@ -1503,21 +1542,26 @@ struct Engine {
       refresh_stp();
       __syncwarp();
     if constexpr (PRUNE) {
-      if (c.prune && (c.processed & 31) == 0) {
+      if (c.prune && (processed & 31) == 0) {
         // chosen-only search: stop once this run's JCT sum provably exceeds a completed
         // candidate's (then its avg_jct_s > that candidate's, so it cannot be the first minimum)
-        const int64_t thr = *reinterpret_cast<volatile const int64_t*>(b.prune_bound + tr);
-        // exact integer part + the started jobs' remaining-work floor (FP sums: 1 s of margin,
-        // far above their rounding error)
-        const int64_t lbi = c.lb_fin + c.lb_narr * c.now - c.lb_arrsum + c.lb_unstarted;
-        const double lb = static_cast<double>(lbi) + (c.lb_p - c.lb_v * s_from_us(c.now)) * 1e6 - 1e6;
-        if (thr != INT64_MAX && lb > static_cast<double>(thr) * (1.0 + 1e-9) + 2.0 * JT) {
+        bool stop = false;
+        if (lane == 0) {
+          const int64_t thr = *reinterpret_cast<volatile const int64_t*>(b.prune_bound + tr);
+          // exact integer part + the started jobs' remaining-work floor (FP sums: 1 s of margin,
+          // far above their rounding error)
+          const int64_t lbi = c.lb_fin + c.lb_narr * c.now - c.lb_arrsum + c.lb_unstarted;
+          const double lb = static_cast<double>(lbi) + (c.lb_p - c.lb_v * s_from_us(c.now)) * 1e6 - 1e6;
+          stop = thr != INT64_MAX && lb > static_cast<double>(thr) * (1.0 + 1e-9) + 2.0 * JT;
+        }
+        if (__shfl_sync(0xffffffffu, stop, 0)) {
           c.status = MISO_B200_SIM_PRUNED;
           break;
         }
       }
     }
     }
+    c.processed = processed;
     // every pushed event is popped by the reference exactly once (live or stale), so its
     // max_events budget (sim.hpp:224, stale pops included) is exceeded iff the pushes exceed it
     CTX_SET(c.status, (c.status == 0 && c.seq > prm.max_events) ? MISO_B200_SIM_EVENT_BUDGET : c.status);

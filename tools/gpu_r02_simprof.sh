@@ -1,0 +1,6 @@
+# Simulator source-level captures: miso (1024 config-4 seeds) and the best-static candidates.
+set -x
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simulate_kernel -c 1 -o gpurun_out/sim_miso -f python tools/sim_one_policy.py miso 1024 > gpurun_out/ncu_sim.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:simulate_kernel -c 1 -o gpurun_out/sim_static -f python tools/sim_static_once.py 256 1 >> gpurun_out/ncu_sim.log 2>&1
+timeout 600 python tools/c4_phases.py > gpurun_out/c4_phases.txt 2>&1
