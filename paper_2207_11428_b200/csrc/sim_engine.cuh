@@ -104,6 +104,7 @@ struct Ctx {  // warp-uniform engine state: one record per block, in shared memo
   double* stp_prefix;   // [J] cached sequential partial sums of rate_eff over the window
   int stp_cmin;         // smallest job index whose rate_eff changed since the last refresh
   int stp_lo, n_arrived; // jobs < stp_lo are done; jobs >= n_arrived have not arrived
+  int stp_hi;            // rate_eff is 0.0 at every index >= stp_hi (<= n_arrived; never shrinks)
   int chunk;            // event slots per lane: lane l owns [l*chunk, (l+1)*chunk)
   uint8_t* jst;         // [J] SoA job state for warp scans: phase | slice << 3 | done << 6
   uint32_t* freemask;   // optsta: [5][W] bit g set iff GPU g has a free slot of that kind
@@ -389,6 +390,11 @@ struct Engine {
     const double re = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
     if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
       c.rate_eff[ji] = re;
+      if (re != 0.0 && ji >= c.stp_hi) {  // the summed range grows: its new blocks need sums
+        const int h = c.stp_hi;
+        CTX_SET(c.stp_cmin, h < c.stp_cmin ? h : c.stp_cmin);
+        CTX_SET(c.stp_hi, ji + 1);
+      }
       c.stp_dirty = true;
       CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
     }
@@ -415,9 +421,11 @@ struct Engine {
   }
 
   // sim.hpp:353-361: s = sum over jobs in index order of rate (progressing, not done). Only
-  // jobs in [stp_lo, n_arrived) can progress; rate_eff holds 0.0 for the others, and s + 0.0 == s
-  // for the non-negative partial sums, so the sequential FP64 sum over that window is
-  // bit-identical to the reference's loop over all jobs. Partial sums are cached per index and
+  // jobs in [stp_lo, stp_hi) can have a nonzero term (below stp_lo every job is done; at and
+  // above stp_hi none has progressed yet -- under FCFS admission the queued tail of the arrived
+  // jobs); rate_eff holds 0.0 for the others, and s + 0.0 == s for the non-negative partial
+  // sums, so the sequential FP64 sum over that window is bit-identical to the reference's loop
+  // over all jobs. Partial sums are cached per index and
   // the chain restarts at the smallest index changed since the previous refresh.
   static __device__ void refresh_stp() {
     Ctx& c = g_sim_ctx;
@@ -425,7 +433,7 @@ struct Engine {
     c.stp_dirty = false;
     const double* r = c.rate_eff;
     double* P = c.stp_prefix;  // P[q]: the sum through index 8q + 7, cached at block ends
-    const int lo = c.stp_lo, hi = c.n_arrived;
+    const int lo = c.stp_lo, hi = c.stp_hi;
     int i0 = c.stp_cmin > lo ? c.stp_cmin : lo;
     if (i0 > hi) i0 = hi;  // changes at not-yet-arrived indices: the window's sum is unchanged
     c.stp_cmin = INT32_MAX;
@@ -573,10 +581,7 @@ struct Engine {
       __syncwarp();
       c.J_used = ci + 1;
       sync_jst(ci, j);
-      if (ci + 1 > c.n_arrived) {
-        CTX_SET(c.stp_cmin, c.n_arrived < c.stp_cmin ? c.n_arrived : c.stp_cmin);
-        c.n_arrived = ci + 1;
-      }
+      if (ci + 1 > c.n_arrived) c.n_arrived = ci + 1;
       log_rec(kLogSpawn, -1, ci, 0, static_cast<uint32_t>(pi), 0, 0);
       enqueue(ci);
     }
@@ -1103,7 +1108,7 @@ struct Engine {
       double bgain = 0.0;
       int64_t barr = 0;
       const double* eff_k = c.efftruth + size_t(kind) * c.J;
-      for (int mi = c.stp_lo + lane_id(); mi < c.n_arrived; mi += 32) {
+      for (int mi = c.stp_lo + lane_id(); mi < c.stp_hi; mi += 32) {  // running jobs lie below stp_hi
         // dense arrays only (coalesced): state byte, effective true speed on `kind`, the
         // running rate (rate_eff == rate for a running job), arrival time
         const uint8_t st = c.jst[mi];
@@ -1226,10 +1231,7 @@ struct Engine {
     if (slot < c.J) {
       const int ji = slot;
       if (kind == kEvArrival) {
-        if (ji + 1 > c.n_arrived) {
-          CTX_SET(c.stp_cmin, c.n_arrived < c.stp_cmin ? c.n_arrived : c.stp_cmin);  // new window entries need sums
-          c.n_arrived = ji + 1;
-        }
+        if (ji + 1 > c.n_arrived) c.n_arrived = ji + 1;
         log_rec(kLogArrival, -1, ji, 0, 0, 0, 0);
     if constexpr (PRUNE) {
         if (c.prune) {
@@ -1366,6 +1368,7 @@ struct Engine {
     c.stp_cmin = INT32_MAX;
     c.stp_lo = 0;
     c.n_arrived = 0;
+    c.stp_hi = 0;
     c.lmin_t[lane] = kNoEvent;
     c.lmin_pk[lane] = ~0ull;
     c.lmin_idx[lane] = -1;
