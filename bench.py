@@ -949,8 +949,12 @@ def sec_c5(args, D, ctx, runner, steps=10):
     traces = miso.generate_traces_device(runner.ctx[0], seeds, 1000, lambda_s=10.0)
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
-    # the pruned static search wins at ~1k seeds per GPU (config 4), the full one at 8k
-    pruned = (s_hi - s_lo) <= 2048
+    # the chosen-only pruned static search (with the per-partition speed ceiling in its bound)
+    # beats the full search at 1k and at 8k seeds per GPU (profiles/r02_c5_prune_ab.txt)
+    pruned = True
+    env = os.environ.get("MISO_C4_PRUNED_STATIC")
+    if env is not None:
+        pruned = env == "1"
     # warm-up at full size: the contexts' workspaces grow to this shard's task counts here
     # (cudaMalloc of up to tens of GB for the static search's candidate runs), not in the
     # timed call
