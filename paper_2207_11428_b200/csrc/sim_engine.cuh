@@ -111,6 +111,7 @@ struct Ctx {  // warp-uniform engine state: one record per block, in shared memo
   double* efftruth;     // [5][J]: effective_speed(truth[k], k, mem, qos) per job (static)
   int64_t* arr_us;      // [J]: arrival_us per job (dense copy for coalesced scans)
   int W;                // words per freemask row
+  uint8_t* gplace;      // miso/oracle: [G] placement view of each GPU (sync_place)
   LogRec* log;
   int64_t log_cap, log_n;
   int J, G;             // J: job capacity (trace jobs + every possible clone)
@@ -491,6 +492,20 @@ struct Engine {
 
   // ---- GPU roster helpers -----------------------------------------------------------------
 
+  // miso/oracle: place_dynamic's view of GPU g, one byte per GPU so the placement scan reads a
+  // few dense sectors instead of one per GPU record: 0x0F if the GPU takes no job (mode other
+  // than idle/MIG, or 7 jobs), else (allow + 1) << 4 | nroster, where allow is the largest
+  // min-kind it accepts (any when empty, its spare slice otherwise; a spare of -1 accepts none).
+  static __device__ __forceinline__ void sync_place(const DGpu& g) {
+    if constexpr (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE) {
+      Ctx& c = g_sim_ctx;
+      uint8_t v = 0x0F;
+      if ((g.mode == kGpuIdle || g.mode == kGpuMig) && g.nroster < 7)
+        v = static_cast<uint8_t>(((g.nroster == 0 ? 5 : g.spare + 1) << 4) | g.nroster);
+      c.gplace[&g - c.gpus] = v;
+    }
+  }
+
   static __device__ void roster_push(DGpu& g, int ji) {
     Ctx& c = g_sim_ctx;
     g.roster[g.nroster] = ji;
@@ -498,6 +513,7 @@ struct Engine {
     ++g.nroster;
     ++g.kind_cnt[c.jobs[ji].min_kind];
     g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
+    sync_place(g);
   }
 
   static __device__ void roster_erase(DGpu& g, int ji) {
@@ -513,6 +529,7 @@ struct Engine {
     --g.nroster;
     --g.kind_cnt[c.jobs[ji].min_kind];
     g.spare = g.nroster >= 7 ? -1 : c.spare_lut[lut_index(g.kind_cnt)];
+    sync_place(g);
   }
 
   // ---- forward declarations of the mutually recursive steps ---------------------------------
@@ -652,6 +669,7 @@ struct Engine {
     Ctx& c = g_sim_ctx;
     DGpu& g = c.gpus[gi];
     g.mode = kGpuMps;
+    sync_place(g);
 #pragma unroll
     for (int k = 0; k < 5; ++k) g.part[k] = 0;
     g.objective = 0;
@@ -733,6 +751,7 @@ struct Engine {
     for (int k = 0; k < 5; ++k) g.part[k] = g.plan_part[k];
     g.objective = g.plan_obj;
     g.mode = kGpuMig;
+    sync_place(g);
     int cnt = 0;
 #pragma unroll
     for (int k = 0; k < 5; ++k) cnt += g.plan_part[k];
@@ -768,6 +787,7 @@ struct Engine {
       return;
     }
     g.mode = kGpuReconfig;
+    sync_place(g);
     for (int i = 0; i < g.nroster; ++i) {
       const int ji = g.roster[i];
       const DJob& j = c.jobs[ji];
@@ -836,13 +856,11 @@ struct Engine {
     const int need = c.jobs[ji].min_kind;
     int best = -1, best_cnt = 8;
     for (int gi = lane_id(); gi < c.G; gi += 32) {
-      const DGpu& g = c.gpus[gi];
-      if (g.mode != kGpuIdle && g.mode != kGpuMig) continue;
-      if (g.nroster >= 7) continue;
-      if (g.nroster > 0 && (g.spare < 0 || g.spare < need)) continue;
-      if (g.nroster < best_cnt) {
+      const int v = c.gplace[gi];  // (allow + 1) << 4 | nroster, see sync_place
+      if ((v >> 4) <= need) continue;
+      if ((v & 15) < best_cnt) {
         best = gi;
-        best_cnt = g.nroster;
+        best_cnt = v & 15;
       }
     }
 #pragma unroll
@@ -1031,6 +1049,7 @@ struct Engine {
         ++g.epoch;
         clear_slot(c.J + gi);
         g.mode = kGpuIdle;
+        sync_place(g);
         return;
       }
       const int lv = g.mps_level == 0 ? 100 : (g.mps_level == 1 ? 50 : 14);
@@ -1060,6 +1079,7 @@ struct Engine {
     else --g.part[j.slice];
     if (g.nroster == 0) {
       g.mode = kGpuIdle;
+      sync_place(g);
 #pragma unroll
       for (int k = 0; k < 5; ++k) g.part[k] = 0;
       g.objective = 0;
@@ -1364,6 +1384,7 @@ struct Engine {
     c.freemask = reinterpret_cast<uint32_t*>(ws + sim_ws_freemask_off(b.max_jobs, G));
     c.efftruth = reinterpret_cast<double*>(ws + sim_ws_efftruth_off(b.max_jobs, G));
     c.arr_us = reinterpret_cast<int64_t*>(ws + sim_ws_arrival_off(b.max_jobs, G));
+    c.gplace = ws + sim_ws_gplace_off(b.max_jobs, G);
     c.W = (G + 31) / 32;
     c.stp_cmin = INT32_MAX;
     c.stp_lo = 0;
@@ -1494,6 +1515,7 @@ struct Engine {
         g.mode = kGpuMig;
       }
       c.slots[J + gi].t = kNoEvent;
+      c.gplace[gi] = 0x50;  // idle, no jobs: takes any job (sync_place)
     }
     for (int i = JT + lane; i < J; i += 32) {  // clone slots: no event, not arrived
       c.slots[i].t = kNoEvent;

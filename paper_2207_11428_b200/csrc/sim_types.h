@@ -95,8 +95,12 @@ __host__ __device__ inline size_t sim_ws_efftruth_off(int J, int G) {
 __host__ __device__ inline size_t sim_ws_arrival_off(int J, int G) {
   return sim_ws_efftruth_off(J, G) + sim_al(size_t(5) * J * 8);
 }
-__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+// miso/oracle placement view: one byte per GPU
+__host__ __device__ inline size_t sim_ws_gplace_off(int J, int G) {
   return sim_ws_arrival_off(J, G) + sim_al(size_t(J) * 8);
+}
+__host__ __device__ inline size_t sim_ws_total(int J, int G) {
+  return sim_ws_gplace_off(J, G) + sim_al(size_t(G));
 }
 
 struct ModelW;  // predict.cuh
