@@ -111,6 +111,7 @@ struct Ctx {  // warp-uniform engine state: one record per block, in shared memo
   double* efftruth;     // [5][J]: effective_speed(truth[k], k, mem, qos) per job (static)
   int64_t* arr_us;      // [J]: arrival_us per job (dense copy for coalesced scans)
   int W;                // words per freemask row
+  int part_min_gpc;     // optsta: the GPC count of the static partition's smallest slice kind
   uint8_t* gplace;      // miso/oracle: [G] placement view of each GPU (sync_place)
   LogRec* log;
   int64_t log_cap, log_n;
@@ -518,8 +519,9 @@ struct Engine {
 
   static __device__ void roster_erase(DGpu& g, int ji) {
     Ctx& c = g_sim_ctx;
-    int i = 0;
-    while (i < g.nroster && g.roster[i] != ji) ++i;
+    const int ln = lane_id();  // the job's roster position, one lane per entry
+    const unsigned hit = __ballot_sync(0xffffffffu, ln < g.nroster && g.roster[ln < 7 ? ln : 0] == ji);
+    const int i = hit ? __ffs(hit) - 1 : g.nroster;
     for (int k = i; k + 1 < g.nroster; ++k) {
       const int v = g.roster[k + 1];
       __syncwarp();
@@ -1128,21 +1130,30 @@ struct Engine {
       double bgain = 0.0;
       int64_t barr = 0;
       const double* eff_k = c.efftruth + size_t(kind) * c.J;
-      for (int mi = c.stp_lo + lane_id(); mi < c.stp_hi; mi += 32) {  // running jobs lie below stp_hi
-        // dense arrays only (coalesced): state byte, effective true speed on `kind`, the
-        // running rate (rate_eff == rate for a running job), arrival time
-        const uint8_t st = c.jst[mi];
-        if ((st & 64) || (st & 7) != kRunning) continue;
-        if (kind_gpc((st >> 3) & 7) >= kg) continue;
-        const double ns = eff_k[mi];
-        if (!(ns > 0)) continue;
-        const double gain = ns - c.rate_eff[mi];
-        if (gain <= 0) continue;
-        const int64_t arr = c.arr_us[mi];
-        if (best < 0 || gain > bgain || (gain == bgain && (arr < barr || (arr == barr && mi < best)))) {
-          best = mi;
-          bgain = gain;
-          barr = arr;
+      // (no job can run on a smaller kind than the partition's smallest: nothing to scan)
+      const int lo = c.stp_lo, hi = kg > c.part_min_gpc ? c.stp_hi : lo;  // running jobs lie below stp_hi
+      // dense arrays only (coalesced): state bytes four at a time (one 4-byte load per lane
+      // covers 128 jobs per warp), then for the survivors the effective true speed on `kind`,
+      // the running rate (rate_eff == rate for a running job) and the arrival time. The
+      // comparison is a total order, so the visiting order does not matter.
+      for (int b = (lo & ~3) + 4 * lane_id(); b < hi; b += 128) {
+        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(c.jst + b);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int mi = b + q;
+          const uint32_t st = (w4 >> (8 * q)) & 255u;
+          if (mi < lo || mi >= hi || (st & 64) || (st & 7) != kRunning) continue;
+          if (kind_gpc((st >> 3) & 7) >= kg) continue;
+          const double ns = eff_k[mi];
+          if (!(ns > 0)) continue;
+          const double gain = ns - c.rate_eff[mi];
+          if (gain <= 0) continue;
+          const int64_t arr = c.arr_us[mi];
+          if (best < 0 || gain > bgain || (gain == bgain && (arr < barr || (arr == barr && mi < best)))) {
+            best = mi;
+            bgain = gain;
+            barr = arr;
+          }
         }
       }
 #pragma unroll
@@ -1386,6 +1397,12 @@ struct Engine {
     c.arr_us = reinterpret_cast<int64_t*>(ws + sim_ws_arrival_off(b.max_jobs, G));
     c.gplace = ws + sim_ws_gplace_off(b.max_jobs, G);
     c.W = (G + 31) / 32;
+    c.part_min_gpc = 99;
+    if (POL == MISO_B200_POLICY_OPTSTA) {
+      const uint8_t* sc = b.static_counts + size_t(warp) * 5;
+      for (int k = 4; k >= 0; --k)
+        if (sc[k] > 0) c.part_min_gpc = kind_gpc(k);
+    }
     c.stp_cmin = INT32_MAX;
     c.stp_lo = 0;
     c.n_arrived = 0;
