@@ -824,6 +824,13 @@ def sec_c4(args, D, runner, seeds_per_rank=1024, steps=3):
                       "frac_note": "issue floor / achieved: the fraction of cycles a simulation warp issues",
                       "ncu_capture": {"issue_active": ncu_val(l0, "smsp__issue_active.avg.pct_of_peak_sustained_active") / 100,
                                       "source": "profiles/sim_kernel_ncu.json"}})
+    # the step's own floor: its longest dependent chain is one miso seed's event sequence, so the
+    # step cannot end before the miso launch alone would (the other sets run beside it)
+    bound["critical_path"] = {"miso_alone_ms": ms_miso, "step_ms": dt * 1e3,
+                              "frac": ms_miso / (dt * 1e3),
+                              "note": "miso simulations alone (CUDA events) / the trial step: the "
+                                      "step's distance from its critical-path floor (the miso "
+                                      "warps slow down beside the other sets' warps)"}
     res["roofline"] = bound
     if D.rank == 0 and not args.no_cpu_baseline and oracle_lib().have_ref():
         k = min(S, max(16, oracle_lib().host_threads()))
