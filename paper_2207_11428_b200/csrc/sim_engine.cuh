@@ -444,9 +444,14 @@ struct Engine {
     // done, contributing +0.0, so a start below lo is exact too)
     int i = i0 & ~7;
     double s = (i > 0 && i - 1 >= lo) ? P[(i >> 3) - 1] : 0.0;
-    for (; i + 8 <= hi; i += 8) {  // 64-byte aligned: four 16-byte loads per block
-      const double2* r2 = reinterpret_cast<const double2*>(r + i);
-      const double2 a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
+    // 64-byte aligned blocks of eight terms, four 16-byte loads each, loaded one block ahead of
+    // the additions (the chain of dependent adds, not the loads, sets the pace); the partial
+    // last block is loaded whole (rate_eff is padded by 32 entries) and added term by term
+    const double2* r2 = reinterpret_cast<const double2*>(r + i);
+    double2 a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
+    for (; i + 8 <= hi; i += 8) {
+      r2 += 4;
+      const double2 b01 = r2[0], b23 = r2[1], b45 = r2[2], b67 = r2[3];
       s = s + a01.x;
       s = s + a01.y;
       s = s + a23.x;
@@ -456,8 +461,15 @@ struct Engine {
       s = s + a67.x;
       s = s + a67.y;
       if (lane_id() == 0) P[i >> 3] = s;
+      a01 = b01;
+      a23 = b23;
+      a45 = b45;
+      a67 = b67;
     }
-    for (; i < hi; ++i) s = s + r[i];
+    const double t[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+      if (i + k < hi) s = s + t[k];
     __syncwarp();
     if (hi <= lo) s = 0.0;
     if (s != c.stp_cur) {
