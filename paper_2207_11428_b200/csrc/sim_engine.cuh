@@ -217,6 +217,35 @@ __device__ __forceinline__ double est_rate(const DJob& j, int k) {
   return effective_speed(j.est[k], k, j.mem, j.qos);
 }
 
+// The lane holding the warp's minimum (t, pk) key (t >= 0; keys of live events are distinct, and
+// among equal keys the lowest lane): 32-bit warp min-reductions over the key's words, most
+// significant first, each stage only among the lanes still tied -- usually two stages (event
+// times rarely tie), instead of a five-round shuffle tree over 128-bit keys.
+__device__ __forceinline__ int warp_argmin_key(int64_t t, uint64_t pk) {
+  const unsigned full = 0xffffffffu;
+  const uint32_t th = static_cast<uint32_t>(static_cast<uint64_t>(t) >> 32);
+  const uint32_t tl = static_cast<uint32_t>(t);
+  const uint32_t m1 = __reduce_min_sync(full, th);
+  unsigned c = __ballot_sync(full, th == m1);
+  if (c & (c - 1)) {
+    const bool in = th == m1;
+    const uint32_t m2 = __reduce_min_sync(full, in ? tl : 0xffffffffu);
+    c = __ballot_sync(full, in && tl == m2);
+    if (c & (c - 1)) {
+      const bool in2 = in && tl == m2;
+      const uint32_t ph = static_cast<uint32_t>(pk >> 32), pl = static_cast<uint32_t>(pk);
+      const uint32_t m3 = __reduce_min_sync(full, in2 ? ph : 0xffffffffu);
+      c = __ballot_sync(full, in2 && ph == m3);
+      if (c & (c - 1)) {
+        const bool in3 = in2 && ph == m3;
+        const uint32_t m4 = __reduce_min_sync(full, in3 ? pl : 0xffffffffu);
+        c = __ballot_sync(full, in3 && pl == m4);
+      }
+    }
+  }
+  return __ffs(c) - 1;
+}
+
 __device__ __forceinline__ int lut_index(const uint8_t* k) {
   return (((k[0] * 7 + k[1]) * 7 + k[2]) * 7 + k[3]) * 7 + k[4];
 }
@@ -296,7 +325,7 @@ struct Engine {
     Ctx& c = g_sim_ctx;
     const int n = c.J + c.G;
     const int lane = lane_id();
-    unsigned inval = __ballot_sync(0xffffffffu, !c.lmin_valid[lane_id()]);
+    unsigned inval = __ballot_sync(0xffffffffu, !c.lmin_valid[lane]);
     while (inval) {
       const int owner = __ffs(inval) - 1;
       inval &= inval - 1;
@@ -314,42 +343,19 @@ struct Engine {
           bi = i;
         }
       }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
-        const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (ot < bt || (ot == bt && ok < bk)) {
-          bt = ot;
-          bk = ok;
-          bi = oi;
-        }
-      }
-      if (lane == owner) {
-        c.lmin_t[lane_id()] = bt;
-        c.lmin_pk[lane_id()] = bk;
-        c.lmin_idx[lane_id()] = bi;
-        c.lmin_valid[lane_id()] = true;
+      if (lane == warp_argmin_key(bt, bk)) {  // the chunk's minimum becomes the owner's
+        c.lmin_t[owner] = bt;
+        c.lmin_pk[owner] = bk;
+        c.lmin_idx[owner] = bi;
+        c.lmin_valid[owner] = true;
       }
     }
     __syncwarp();
-    int64_t bt = c.lmin_t[lane_id()];
-    uint64_t bk = c.lmin_pk[lane_id()];
-    int bi = c.lmin_idx[lane_id()];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int64_t ot = __shfl_xor_sync(0xffffffffu, bt, off);
-      const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (ot < bt || (ot == bt && ok < bk)) {
-        bt = ot;
-        bk = ok;
-        bi = oi;
-      }
-    }
+    const int w = warp_argmin_key(c.lmin_t[lane], c.lmin_pk[lane]);
+    const int64_t bt = c.lmin_t[w];
     out->t = bt;
-    out->pk = bk;
-    return bt == kNoEvent ? -1 : bi;
+    out->pk = c.lmin_pk[w];
+    return bt == kNoEvent ? -1 : c.lmin_idx[w];
   }
 
   // ---- job state ---------------------------------------------------------------------------
@@ -448,24 +454,35 @@ struct Engine {
     // the additions (the chain of dependent adds, not the loads, sets the pace); the partial
     // last block is loaded whole (rate_eff is padded by 32 entries) and added term by term
     const double2* r2 = reinterpret_cast<const double2*>(r + i);
+    const bool lane0 = lane_id() == 0;
     double2 a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
-    for (; i + 8 <= hi; i += 8) {
-      r2 += 4;
-      const double2 b01 = r2[0], b23 = r2[1], b45 = r2[2], b67 = r2[3];
-      s = s + a01.x;
-      s = s + a01.y;
-      s = s + a23.x;
-      s = s + a23.y;
-      s = s + a45.x;
-      s = s + a45.y;
-      s = s + a67.x;
-      s = s + a67.y;
-      if (lane_id() == 0) P[i >> 3] = s;
-      a01 = b01;
-      a23 = b23;
-      a45 = b45;
-      a67 = b67;
+    double2 b01, b23, b45, b67;
+#define MISO_STP_ADD8(x01, x23, x45, x67) \
+    s = s + x01.x;                        \
+    s = s + x01.y;                        \
+    s = s + x23.x;                        \
+    s = s + x23.y;                        \
+    s = s + x45.x;                        \
+    s = s + x45.y;                        \
+    s = s + x67.x;                        \
+    s = s + x67.y
+    for (; i + 16 <= hi; i += 16) {  // two blocks per trip: no register copies between them
+      b01 = r2[4], b23 = r2[5], b45 = r2[6], b67 = r2[7];
+      MISO_STP_ADD8(a01, a23, a45, a67);
+      if (lane0) P[i >> 3] = s;
+      r2 += 8;
+      a01 = r2[0], a23 = r2[1], a45 = r2[2], a67 = r2[3];
+      MISO_STP_ADD8(b01, b23, b45, b67);
+      if (lane0) P[(i >> 3) + 1] = s;
     }
+    if (i + 8 <= hi) {
+      b01 = r2[4], b23 = r2[5], b45 = r2[6], b67 = r2[7];
+      MISO_STP_ADD8(a01, a23, a45, a67);
+      if (lane0) P[i >> 3] = s;
+      i += 8;
+      a01 = b01, a23 = b23, a45 = b45, a67 = b67;
+    }
+#undef MISO_STP_ADD8
     const double t[8] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y, a67.x, a67.y};
 #pragma unroll
     for (int k = 0; k < 7; ++k)
