@@ -217,33 +217,32 @@ __device__ __forceinline__ double est_rate(const DJob& j, int k) {
   return effective_speed(j.est[k], k, j.mem, j.qos);
 }
 
-// The lane holding the warp's minimum (t, pk) key (t >= 0; keys of live events are distinct, and
-// among equal keys the lowest lane): 32-bit warp min-reductions over the key's words, most
-// significant first, each stage only among the lanes still tied -- usually two stages (event
-// times rarely tie), instead of a five-round shuffle tree over 128-bit keys.
-__device__ __forceinline__ int warp_argmin_key(int64_t t, uint64_t pk) {
+// The lane holding the warp's minimum of a key given as N 32-bit words, most significant first
+// (among equal keys the lowest lane): one 32-bit warp min-reduction per word, each stage only
+// among the lanes still tied, stopping as soon as one lane is left -- a few redux.sync steps
+// instead of a five-round shuffle tree over the whole key.
+template <int N>
+__device__ __forceinline__ int warp_argmin_words(const uint32_t (&w)[N]) {
   const unsigned full = 0xffffffffu;
-  const uint32_t th = static_cast<uint32_t>(static_cast<uint64_t>(t) >> 32);
-  const uint32_t tl = static_cast<uint32_t>(t);
-  const uint32_t m1 = __reduce_min_sync(full, th);
-  unsigned c = __ballot_sync(full, th == m1);
-  if (c & (c - 1)) {
-    const bool in = th == m1;
-    const uint32_t m2 = __reduce_min_sync(full, in ? tl : 0xffffffffu);
-    c = __ballot_sync(full, in && tl == m2);
-    if (c & (c - 1)) {
-      const bool in2 = in && tl == m2;
-      const uint32_t ph = static_cast<uint32_t>(pk >> 32), pl = static_cast<uint32_t>(pk);
-      const uint32_t m3 = __reduce_min_sync(full, in2 ? ph : 0xffffffffu);
-      c = __ballot_sync(full, in2 && ph == m3);
-      if (c & (c - 1)) {
-        const bool in3 = in2 && ph == m3;
-        const uint32_t m4 = __reduce_min_sync(full, in3 ? pl : 0xffffffffu);
-        c = __ballot_sync(full, in3 && pl == m4);
-      }
-    }
+  bool in = true;
+  unsigned c = full;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    const uint32_t m = __reduce_min_sync(full, in ? w[k] : 0xffffffffu);
+    in = in && w[k] == m;
+    c = __ballot_sync(full, in);
+    if (!(c & (c - 1))) break;  // warp-uniform
   }
   return __ffs(c) - 1;
+}
+
+// event keys: (t >= 0, pk) -- live events' keys are distinct, and event times rarely tie, so
+// this is usually two stages
+__device__ __forceinline__ int warp_argmin_key(int64_t t, uint64_t pk) {
+  const uint32_t w[4] = {static_cast<uint32_t>(static_cast<uint64_t>(t) >> 32),
+                         static_cast<uint32_t>(t), static_cast<uint32_t>(pk >> 32),
+                         static_cast<uint32_t>(pk)};
+  return warp_argmin_words(w);
 }
 
 __device__ __forceinline__ int lut_index(const uint8_t* k) {
@@ -894,16 +893,12 @@ struct Engine {
         best_cnt = v & 15;
       }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const int ob = __shfl_xor_sync(0xffffffffu, best, off);
-      const int oc = __shfl_xor_sync(0xffffffffu, best_cnt, off);
-      if (ob >= 0 && (best < 0 || oc < best_cnt || (oc == best_cnt && ob < best))) {
-        best = ob;
-        best_cnt = oc;
-      }
+    if (!__ballot_sync(0xffffffffu, best >= 0)) return -1;
+    {  // the least-loaded candidate, ties to the lowest GPU id
+      const uint32_t key[2] = {best >= 0 ? static_cast<uint32_t>(best_cnt) : 0xffffffffu,
+                               static_cast<uint32_t>(best)};
+      best = __shfl_sync(0xffffffffu, best, warp_argmin_words(key));
     }
-    if (best < 0) return -1;
     CTX_SET(c.qhead, c.qhead + 1);  // pop_queue: the placed job is always the queue head
     DGpu& g = c.gpus[best];
     roster_push(g, ji);
@@ -1019,9 +1014,7 @@ struct Engine {
       return false;
     }
     // lowest id among lanes' first idle GPUs
-    int b = best >= 0 ? best : INT32_MAX;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, off));
+    const int b = static_cast<int>(__reduce_min_sync(0xffffffffu, best >= 0 ? static_cast<uint32_t>(best) : 0xffffffffu));
     CTX_SET(c.qhead, c.qhead + 1);
     DGpu& g = c.gpus[b];
     g.mode = kGpuMig;
@@ -1185,19 +1178,18 @@ struct Engine {
           }
         }
       }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const int ob = __shfl_xor_sync(0xffffffffu, best, off);
-        const double og = __shfl_xor_sync(0xffffffffu, bgain, off);
-        const int64_t oa = __shfl_xor_sync(0xffffffffu, barr, off);
-        if (ob >= 0 && (best < 0 || og > bgain ||
-                        (og == bgain && (oa < barr || (oa == barr && ob < best))))) {
-          best = ob;
-          bgain = og;
-          barr = oa;
-        }
+      if (!__ballot_sync(0xffffffffu, best >= 0)) continue;
+      {  // largest gain (> 0: its bits order like the value; complemented for a minimum), then
+         // earliest arrival (>= 0), then lowest index
+        const uint64_t gb = ~static_cast<uint64_t>(__double_as_longlong(bgain));
+        const bool has = best >= 0;
+        const uint32_t key[5] = {has ? static_cast<uint32_t>(gb >> 32) : 0xffffffffu,
+                                 has ? static_cast<uint32_t>(gb) : 0xffffffffu,
+                                 has ? static_cast<uint32_t>(static_cast<uint64_t>(barr) >> 32) : 0xffffffffu,
+                                 has ? static_cast<uint32_t>(barr) : 0xffffffffu,
+                                 has ? static_cast<uint32_t>(best) : 0xffffffffu};
+        best = __shfl_sync(0xffffffffu, best, warp_argmin_words(key));
       }
-      if (best < 0) continue;
       DJob& m = c.jobs[best];
       DGpu& og = c.gpus[m.gpu];
       free_slot(m.gpu, m.slot);
