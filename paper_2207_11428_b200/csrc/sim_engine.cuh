@@ -249,7 +249,9 @@ __device__ __forceinline__ int lut_index(const uint8_t* k) {
   return (((k[0] * 7 + k[1]) * 7 + k[2]) * 7 + k[3]) * 7 + k[4];
 }
 
-template <int POL, bool PRUNE>
+// LOG: the event-log writer is compiled in (the parity runs that request a log); measured runs
+// use the LOG = false instantiation, which carries no log calls at all.
+template <int POL, bool PRUNE, bool LOG>
 struct Engine {
 
   static __device__ __forceinline__ void sync_jst(int ji, const DJob& j) {
@@ -267,7 +269,9 @@ struct Engine {
   // the kernel's instruction footprint for a path that is off in measured runs)
   static __device__ __forceinline__ void log_rec(uint8_t kind, int gpu, int job, uint8_t x,
                                                  uint32_t a, uint32_t b, double v) {
-    if (g_sim_ctx.log) log_write(kind, gpu, job, x, a, b, v);
+    if constexpr (LOG) {
+      if (g_sim_ctx.log) log_write(kind, gpu, job, x, a, b, v);
+    }
   }
   static __device__ __noinline__ void log_write(uint8_t kind, int gpu, int job, uint8_t x,
                                                 uint32_t a, uint32_t b, double v) {
