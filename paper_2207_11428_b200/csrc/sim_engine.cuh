@@ -250,8 +250,10 @@ __device__ __forceinline__ int lut_index(const uint8_t* k) {
 }
 
 // LOG: the event-log writer is compiled in (the parity runs that request a log); measured runs
-// use the LOG = false instantiation, which carries no log calls at all.
-template <int POL, bool PRUNE, bool LOG>
+// use the LOG = false instantiation, which carries no log calls at all. STP: the STP series and
+// integral are tracked (SimParams::track_stp; the best-static search's JCT-only candidate runs
+// use STP = false, which carries no STP bookkeeping).
+template <int POL, bool PRUNE, bool LOG, bool STP>
 struct Engine {
 
   static __device__ __forceinline__ void sync_jst(int ji, const DJob& j) {
@@ -402,12 +404,16 @@ struct Engine {
     if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
       c.rate_eff[ji] = re;
       if (re != 0.0 && ji >= c.stp_hi) {  // the summed range grows: its new blocks need sums
-        const int h = c.stp_hi;
-        CTX_SET(c.stp_cmin, h < c.stp_cmin ? h : c.stp_cmin);
+        if constexpr (STP) {
+          const int h = c.stp_hi;
+          CTX_SET(c.stp_cmin, h < c.stp_cmin ? h : c.stp_cmin);
+        }
         CTX_SET(c.stp_hi, ji + 1);
       }
-      c.stp_dirty = true;
-      CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+      if constexpr (STP) {
+        c.stp_dirty = true;
+        CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+      }
     }
     sync_jst(ji, j);
     if constexpr (PRUNE) {
@@ -440,7 +446,8 @@ struct Engine {
   // the chain restarts at the smallest index changed since the previous refresh.
   static __device__ void refresh_stp() {
     Ctx& c = g_sim_ctx;
-    if (!c.stp_dirty || !c.prm.track_stp) return;
+    if constexpr (!STP) return;
+    if (!c.stp_dirty) return;
     c.stp_dirty = false;
     const double* r = c.rate_eff;
     double* P = c.stp_prefix;  // P[q]: the sum through index 8q + 7, cached at block ends
@@ -588,10 +595,14 @@ struct Engine {
   // arrival as FCFS position and JCT baseline, the parent's estimates, queued in FCFS order
   // (arrival_us, index == entry_seq). The STP window grows to the clone's index; jobs in between
   // that have not arrived yet contribute +0.0 (exact).
-  static __device__ __noinline__ void spawn_instances(int pi) {
+  // (the common single-instance case is decided inline; the spawning itself is out of line)
+  static __device__ __forceinline__ void spawn_instances(int pi) {
+    const DJob& par = g_sim_ctx.jobs[pi];
+    if (!(par.flags & kSpawned) && par.inst > 1) spawn_clones(pi);
+  }
+  static __device__ __noinline__ void spawn_clones(int pi) {
     Ctx& c = g_sim_ctx;
     DJob& par = c.jobs[pi];
-    if ((par.flags & kSpawned) || par.inst <= 1) return;
     par.flags |= kSpawned;
     for (int k = 1; k < par.inst; ++k) {
       const int ci = c.J_used;
@@ -1242,8 +1253,10 @@ struct Engine {
     ++j.epoch;
     clear_slot(ji);
     c.rate_eff[ji] = 0.0;
-    c.stp_dirty = true;
-    CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+    if constexpr (STP) {
+      c.stp_dirty = true;
+      CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+    }
     sync_jst(ji, j);
     int stp_lo = c.stp_lo;
     while (stp_lo < c.n_arrived && (c.jst[stp_lo] & 64)) ++stp_lo;
@@ -1601,8 +1614,10 @@ struct Engine {
       }
       clear_slot(slot);
       __syncwarp();
-      CTX_SET(c.stp_integral, c.stp_integral + (c.stp_cur * s_from_us(ev.t - c.stp_last)));
-      c.stp_last = ev.t;
+      if constexpr (STP) {
+        CTX_SET(c.stp_integral, c.stp_integral + (c.stp_cur * s_from_us(ev.t - c.stp_last)));
+        c.stp_last = ev.t;
+      }
       c.now = ev.t;
       dispatch(slot, static_cast<uint32_t>(ev.pk & 7));
       drain_queue();

@@ -18,11 +18,11 @@
 
 namespace miso_b200 {
 
-template <int POL, bool PRUNE, bool LOG>
+template <int POL, bool PRUNE, bool LOG, bool STP>
 __global__ void __launch_bounds__(32, (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE)
                                           ? MISO_SIM_MIN_BLOCKS_DYN : MISO_SIM_MIN_BLOCKS)
 simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
-  simk::Engine<POL, PRUNE, LOG>::run(b, prm, w);
+  simk::Engine<POL, PRUNE, LOG, STP>::run(b, prm, w);
 }
 
 // The engine uses ~2.5 KB of shared memory per block and lives on L1 hits (job records, event
@@ -38,12 +38,12 @@ inline int sim_carveout_env() {
   return v;
 }
 
-template <int POL, bool PRUNE, bool LOG>
+template <int POL, bool PRUNE, bool LOG, bool STP>
 cudaError_t launch_sim_k(const SimBatch& b, const SimParams& p, const ModelW& w, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     attr_set = true;
-    auto kern = simulate_kernel<POL, PRUNE, LOG>;
+    auto kern = simulate_kernel<POL, PRUNE, LOG, STP>;
     int pct = sim_carveout_env();
     if (pct == -3) {
       cudaFuncAttributes fa{};
@@ -64,19 +64,23 @@ cudaError_t launch_sim_k(const SimBatch& b, const SimParams& p, const ModelW& w,
       if (e != cudaSuccess) return e;
     }
   }
-  simulate_kernel<POL, PRUNE, LOG><<<b.n_seeds, 32, 0, s>>>(b, p, w);  // one warp (block) per task
+  simulate_kernel<POL, PRUNE, LOG, STP><<<b.n_seeds, 32, 0, s>>>(b, p, w);  // one warp (block) per task
   return cudaGetLastError();
 }
 
-// The event-log variant only when a log is requested (pruned runs never take one).
+// The event-log variant only when a log is requested (pruned runs never take one); the STP
+// variant only when the STP is tracked.
 template <int POL, bool PRUNE>
 cudaError_t launch_sim(const SimBatch& b, const SimParams& p, const ModelW& w, cudaStream_t s) {
   if constexpr (!PRUNE) {
-    if (b.log) return launch_sim_k<POL, PRUNE, true>(b, p, w, s);
+    if (b.log)
+      return p.track_stp ? launch_sim_k<POL, PRUNE, true, true>(b, p, w, s)
+                         : launch_sim_k<POL, PRUNE, true, false>(b, p, w, s);
   } else {
     if (b.log) return cudaErrorInvalidValue;
   }
-  return launch_sim_k<POL, PRUNE, false>(b, p, w, s);
+  return p.track_stp ? launch_sim_k<POL, PRUNE, false, true>(b, p, w, s)
+                     : launch_sim_k<POL, PRUNE, false, false>(b, p, w, s);
 }
 
 }  // namespace miso_b200
