@@ -573,6 +573,24 @@ struct Engine {
     sync_place(g);
   }
 
+  // Lane-parallel roster reads (one lane per roster entry, one load round trip instead of a
+  // chain of roster -> job loads per entry): bit i = the predicate for roster entry i.
+  static __device__ __forceinline__ unsigned roster_flag_mask(const DGpu& g, uint8_t flag) {
+    const int ln = lane_id();
+    const bool p = ln < g.nroster && (g_sim_ctx.jobs[g.roster[ln < 7 ? ln : 0]].flags & flag);
+    return __ballot_sync(0xffffffffu, p);
+  }
+  // entry i's job already runs on the planned slice (begin_reconfig / apply_assignment skip it)
+  static __device__ __forceinline__ unsigned roster_on_plan_mask(const DGpu& g) {
+    const int ln = lane_id();
+    bool p = false;
+    if (ln < g.nroster) {
+      const DJob& j = g_sim_ctx.jobs[g.roster[ln]];
+      p = j.phase == kRunning && j.slice == g.plan_slice[ln];
+    }
+    return __ballot_sync(0xffffffffu, p);
+  }
+
   // ---- forward declarations of the mutually recursive steps ---------------------------------
 
   // sim.hpp:480-489
@@ -668,9 +686,9 @@ struct Engine {
     const double eq = 100.0 / static_cast<double>(n);
     if (eq < share) share = eq;  // std::min(level, 100/n)
     const double gpc = clampd(share / 100.0 * 7.0, 1.0, 7.0);
-    for (int i = 0; i < n; ++i) {
-      const int ji = g.roster[i];
-      const DJob& j = c.jobs[ji];
+    double my_rate = 0.0;  // lane i: roster entry i's MPS rate (the loads in parallel)
+    if (lane_id() < n) {
+      const DJob& j = c.jobs[g.roster[lane_id()]];
       double sp;
       if (gpc <= 1.0) {
         sp = j.truth[0];
@@ -683,8 +701,12 @@ struct Engine {
         const double wgt = (gpc - knots[k - 1]) / (knots[k] - knots[k - 1]);
         sp = j.truth[k - 1] + wgt * (j.truth[k] - j.truth[k - 1]);
       }
-      const double rate = clampd(c.prm.interference * sp, kSpeedFloor, 1.0);
-      set_phase(ji, kMps, rate);
+      my_rate = clampd(c.prm.interference * sp, kSpeedFloor, 1.0);
+    }
+    __syncwarp();
+    for (int i = 0; i < n; ++i) {
+      const int ji = g.roster[i];
+      set_phase(ji, kMps, __shfl_sync(0xffffffffu, my_rate, i));
       schedule_completion(ji);
     }
   }
@@ -723,14 +745,12 @@ struct Engine {
       return;
     }
     CTX_SET(c.mps_sessions, c.mps_sessions + 1);
-    bool need_ckpt = false;
-    if (c.prm.ckpt_us > 0)
-      for (int i = 0; i < g.nroster; ++i)
-        if (c.jobs[g.roster[i]].flags & kRunState) need_ckpt = true;
+    const unsigned ran = roster_flag_mask(g, kRunState);
+    const bool need_ckpt = c.prm.ckpt_us > 0 && ran != 0;
     if (need_ckpt) {
       for (int i = 0; i < g.nroster; ++i) {
         const int ji = g.roster[i];
-        set_phase(ji, (c.jobs[ji].flags & kRunState) ? kCkpt : kQueued, 0.0);
+        set_phase(ji, ((ran >> i) & 1u) ? kCkpt : kQueued, 0.0);
       }
       ++g.epoch;
       push_event(c.J + gi, c.now + c.prm.ckpt_us, 2, kEvCkptDone);
@@ -806,11 +826,10 @@ struct Engine {
     log_rec(kLogPartition, gi, -1, static_cast<uint8_t>(g.nroster), pack_part(g.part), 0, 0);
     for (int i = 0; i < g.nroster; ++i)
       log_rec(kLogAssign, gi, g.roster[i], g.plan_slice[i], 0, 0, 0);
+    const unsigned keep = roster_on_plan_mask(g);
     for (int i = 0; i < g.nroster; ++i) {
-      const int ji = g.roster[i];
-      const DJob& j = c.jobs[ji];
-      if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-      start_running(ji, g.plan_slice[i]);
+      if ((keep >> i) & 1u) continue;
+      start_running(g.roster[i], g.plan_slice[i]);
     }
   }
 
@@ -818,13 +837,10 @@ struct Engine {
   static __device__ void begin_reconfig(int gi) {
     Ctx& c = g_sim_ctx;
     DGpu& g = c.gpus[gi];
-    bool any = false, restart = false;
-    for (int i = 0; i < g.nroster; ++i) {
-      const DJob& j = c.jobs[g.roster[i]];
-      if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-      any = true;
-      if (j.flags & kRunState) restart = true;
-    }
+    const unsigned all = (1u << g.nroster) - 1u;
+    const unsigned move = ~roster_on_plan_mask(g) & all;  // entries whose job changes slice
+    const unsigned ran = roster_flag_mask(g, kRunState);
+    const bool any = move != 0, restart = (move & ran) != 0;
     const int64_t pause = c.prm.reconfig_us + (restart ? c.prm.ckpt_us : 0);
     g.plan_valid = 1;
     if (!any || pause == 0) {
@@ -834,10 +850,8 @@ struct Engine {
     g.mode = kGpuReconfig;
     sync_place(g);
     for (int i = 0; i < g.nroster; ++i) {
-      const int ji = g.roster[i];
-      const DJob& j = c.jobs[ji];
-      if (j.phase == kRunning && j.slice == g.plan_slice[i]) continue;
-      set_phase(ji, (j.flags & kRunState) ? kCkpt : kQueued, 0.0);
+      if (!((move >> i) & 1u)) continue;
+      set_phase(g.roster[i], ((ran >> i) & 1u) ? kCkpt : kQueued, 0.0);
     }
     ++g.epoch;
     push_event(c.J + gi, c.now + pause, 2, kEvReconfigDone);
@@ -889,8 +903,7 @@ struct Engine {
         const int ji = g.roster[i];
         if (!(c.jobs[ji].flags & kHasEst)) cache_estimates(ji, c.jobs[ji].truth);
       }
-    bool all_est = true;
-    for (int i = 0; i < g.nroster; ++i) all_est = all_est && (c.jobs[g.roster[i]].flags & kHasEst);
+    const bool all_est = roster_flag_mask(g, kHasEst) == (1u << g.nroster) - 1u;
     if (all_est) reopt_and_apply(gi, true);
     else start_profiling_session(gi);
   }
@@ -1125,22 +1138,25 @@ struct Engine {
       return;
     }
     log_rec(kLogShrink, gi, -1, 0, pack_part(g.part), 0, 0);
-    double obj = 0;
-    for (int i = 0; i < g.nroster; ++i) {
-      const DJob& r = c.jobs[g.roster[i]];
-      obj += est_rate(r, r.slice);
-    }
-    g.objective = obj;
-    if (c.prm.drift_threshold > 0 && POL == MISO_B200_POLICY_MISO && c.prm.window_us > 0) {
-      for (int i = 0; i < g.nroster; ++i) {
-        const DJob& r = c.jobs[g.roster[i]];
-        const double est = est_rate(r, r.slice);
+    // lane i: roster entry i's estimated rate and drift test (loads in parallel); the objective
+    // is then summed in roster order, as the reference's loop adds it
+    const int n = g.nroster;
+    double my_est = 0.0;
+    bool drift = false;
+    if (lane_id() < n) {
+      const DJob& r = c.jobs[g.roster[lane_id()]];
+      my_est = est_rate(r, r.slice);
+      if (c.prm.drift_threshold > 0 && POL == MISO_B200_POLICY_MISO && c.prm.window_us > 0) {
         const double truth = true_rate(r, r.slice);
-        if (est > 0 && fabs(truth - est) / est > c.prm.drift_threshold) {
-          start_profiling_session(gi);
-          return;
-        }
+        drift = my_est > 0 && fabs(truth - my_est) / my_est > c.prm.drift_threshold;
       }
+    }
+    double obj = 0;
+    for (int i = 0; i < n; ++i) obj += __shfl_sync(0xffffffffu, my_est, i);
+    g.objective = obj;
+    if (__ballot_sync(0xffffffffu, drift)) {
+      start_profiling_session(gi);
+      return;
     }
     reopt_and_apply(gi, false);
   }
