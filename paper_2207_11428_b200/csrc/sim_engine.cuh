@@ -514,11 +514,11 @@ struct Engine {
   // ---- queue (std::set ordered by (arrival_us, entry_seq == idx)) -------------------------
   static __device__ void enqueue(int ji) {
     Ctx& c = g_sim_ctx;
-    const int64_t a = c.jobs[ji].arrival_us;
+    const int64_t a = c.arr_us[ji];  // (dense copy of arrival_us)
     int pos = c.qtail;
     while (pos > c.qhead) {  // sorted insert; arrivals append at the tail
       const int prev = c.queue[pos - 1];
-      const int64_t pa = c.jobs[prev].arrival_us;
+      const int64_t pa = c.arr_us[prev];
       if (pa < a || (pa == a && prev < ji)) break;
       __syncwarp();
       c.queue[pos] = prev;
@@ -561,10 +561,11 @@ struct Engine {
     const int ln = lane_id();  // the job's roster position, one lane per entry
     const unsigned hit = __ballot_sync(0xffffffffu, ln < g.nroster && g.roster[ln < 7 ? ln : 0] == ji);
     const int i = hit ? __ffs(hit) - 1 : g.nroster;
-    for (int k = i; k + 1 < g.nroster; ++k) {
-      const int v = g.roster[k + 1];
+    {  // close the gap: lane k moves entry k + 1 down (all reads before any write)
+      const bool mv = ln >= i && ln + 1 < g.nroster;
+      const int v = mv ? g.roster[ln + 1] : 0;
       __syncwarp();
-      g.roster[k] = v;
+      if (mv) g.roster[ln] = v;
       __syncwarp();
     }
     --g.nroster;
@@ -788,13 +789,17 @@ struct Engine {
                          c.prm.target_mae, c.w, e);
         }
       }
-      __syncwarp();  // reconverge before the column exchange
-      for (int i = 0; i < n; ++i) {
-        double ei[5];
+      __syncwarp();  // reconverge
+      // cache_estimates for every column: lane i stores its own column's estimates (no column
+      // exchange), then the spawns run in roster order (they read only their own job's row)
+      if (ln < n) {
+        DJob& j = c.jobs[g.roster[ln]];
 #pragma unroll
-        for (int k = 0; k < 5; ++k) ei[k] = __shfl_sync(0xffffffffu, e[k], i);
-        cache_estimates(g.roster[i], ei);
+        for (int k = 0; k < 5; ++k) j.est[k] = e[k];
+        j.flags |= kHasEst;
       }
+      __syncwarp();
+      for (int i = 0; i < n; ++i) spawn_instances(g.roster[i]);
     }
     reopt_and_apply(gi, true);
   }
