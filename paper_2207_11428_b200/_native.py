@@ -211,7 +211,7 @@ class Context:
             if obj is None:
                 obj = torch.empty(n, dtype=torch.float64, device=speeds.device)
             _check_device_args(speeds, offsets, cand, obj, n)
-            s =stream if stream is not None else torch.cuda.current_stream(speeds.device).cuda_stream
+            s = stream if stream is not None else torch.cuda.current_stream(speeds.device).cuda_stream
             _check(lib.miso_b200_optimize_batch(self._h, speeds.data_ptr(), offsets.data_ptr(), n,
                                                 cand.data_ptr(), obj.data_ptr(), s))
             return cand, obj
