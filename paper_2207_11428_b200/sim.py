@@ -179,12 +179,30 @@ class TraceBatch(list):
 
 class DeviceTraceBatch:
     """Traces resident on the device (generate_traces_device): equal-length traces as CUDA
-    tensors, accepted by simulate_batch / best_static_partition without a host round trip."""
+    tensors, accepted by simulate_batch / best_static_partition without a host round trip.
 
-    def __init__(self, seeds, arrival_s, duration_s, speeds5, mem_gb):
+    Stream order: the tensors are written on `stream` (the generator's; default: the current
+    stream), and so are the simulator's CSR views (offsets, uint8 memory demands, QoS), built
+    once here. `ready` is a CUDA event recorded after them on that stream; every consumer on
+    another stream waits for it (simulate_batch, static_candidates, to_host)."""
+
+    def __init__(self, seeds, arrival_s, duration_s, speeds5, mem_gb, stream=None, after=None):
+        import torch
         self.seeds = np.ascontiguousarray(seeds, np.uint64)
         self.arrival_s, self.duration_s, self.speeds5, self.mem_gb = arrival_s, duration_s, speeds5, mem_gb
         self.n, self.job_count = arrival_s.shape
+        dev = arrival_s.device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        with torch.cuda.stream(st):
+            if after is not None:  # a slice: the parent's tensors must be ready first
+                st.wait_event(after)
+            offs = torch.arange(self.n + 1, dtype=torch.int32, device=dev) * self.job_count
+            self._csr = (offs, self.arrival_s.reshape(-1), self.duration_s.reshape(-1),
+                         self.speeds5.reshape(-1, 5), self.mem_gb.reshape(-1).to(torch.uint8),
+                         torch.full((self.n * self.job_count,), -1, dtype=torch.int8, device=dev),
+                         None)
+            self.ready = torch.cuda.Event()
+            self.ready.record(st)
 
     def __len__(self):
         return self.n
@@ -194,18 +212,19 @@ class DeviceTraceBatch:
             raise TypeError("DeviceTraceBatch supports contiguous slices only")
         lo, hi, _ = i.indices(self.n)
         return DeviceTraceBatch(self.seeds[lo:hi], self.arrival_s[lo:hi], self.duration_s[lo:hi],
-                                self.speeds5[lo:hi], self.mem_gb[lo:hi])
+                                self.speeds5[lo:hi], self.mem_gb[lo:hi], after=self.ready)
 
     @property
     def csr(self):
+        return self._csr
+
+    def wait(self, stream=None):
+        """Make `stream` (default: the current one) wait until the batch's tensors are written."""
         import torch
-        dev = self.arrival_s.device
-        offs = torch.arange(self.n + 1, dtype=torch.int32, device=dev) * self.job_count
-        return (offs, self.arrival_s.reshape(-1), self.duration_s.reshape(-1),
-                self.speeds5.reshape(-1, 5), self.mem_gb.reshape(-1).to(torch.uint8),
-                torch.full((self.n * self.job_count,), -1, dtype=torch.int8, device=dev), None)
+        (stream if stream is not None else torch.cuda.current_stream(self.arrival_s.device)).wait_event(self.ready)
 
     def to_host(self) -> "TraceBatch":
+        self.wait()
         a, d = self.arrival_s.cpu().numpy(), self.duration_s.cpu().numpy()
         sp, mem = self.speeds5.cpu().numpy(), self.mem_gb.cpu().numpy()
         out = TraceBatch(Trace(a[i], d[i], sp[i], mem[i], None, int(self.seeds[i])) for i in range(self.n))
@@ -287,7 +306,7 @@ def generate_traces_device(ctx: Context, seeds, job_count: int = 100, lambda_s: 
                                                 max_duration_s, kind, sigma, fixed_s, lo_s, hi_s,
                                                 a.data_ptr(), d.data_ptr(), sp.data_ptr(),
                                                 mem.data_ptr(), st.cuda_stream))
-    return DeviceTraceBatch(np.ascontiguousarray(seeds, np.uint64), a, d, sp, mem)
+    return DeviceTraceBatch(np.ascontiguousarray(seeds, np.uint64), a, d, sp, mem, stream=st)
 
 
 @dataclass
@@ -323,6 +342,11 @@ def simulate_batch(ctx: Context, traces: Sequence[Trace], opts: SimOptions,
     import torch
     dev = torch.device("cuda", ctx.device)
     st_obj = stream if stream is not None else torch.cuda.current_stream(dev)
+    # stream order: the launch stream waits for the caller's stream (whatever produced the
+    # inputs there) and for device-resident traces' own producer stream
+    st_obj.wait_stream(torch.cuda.current_stream(dev))
+    if isinstance(traces, DeviceTraceBatch):
+        traces.wait(st_obj)
     S = len(traces) if task_trace is None else len(task_trace)
     offs, arr, dur, sp, mem, qos, inst = _csr(traces)
     if inst is not None and (np.asarray(inst) < 1).any():
@@ -487,6 +511,7 @@ def static_candidates(traces: Sequence[Trace], catalog=None):
     largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
     offs, _, _, _, mem, qos, _ = _csr(traces)
     if hasattr(mem, "cpu"):  # device-resident batch: the feasibility pass runs on host copies
+        traces.wait()
         offs, mem, qos = offs.cpu().numpy(), mem.cpu().numpy(), qos.cpu().numpy()
     # min_slice_for: the smallest kind with memory_gb >= mem and gpc >= gpc(qos); both tables
     # are non-decreasing in the kind index, so it is max(first kind with enough memory, qos)

@@ -276,3 +276,37 @@ def test_device_trace_batch_feeds_the_simulator(ctx):
     sb = m.best_static_partition(ctx, hb, cluster_size=16)
     assert [e for e, _ in sa] == [e for e, _ in sb]
     assert all(np.array_equal(x.view(np.uint64), y.view(np.uint64)) for (_, x), (_, y) in zip(sa, sb))
+
+
+def test_device_trace_batch_stream_order(ctx):
+    """Stream order of device-resident traces: traces generated on one stream behind a long
+    spin, then simulated at once on other streams (and a slice of them, and the chosen-only
+    static search) without any host synchronisation -- every launch waits for the generator,
+    so the results equal the host traces' bit for bit."""
+    import torch
+    import paper_2207_11428_b200 as m
+    seeds = list(range(24))
+    hb = m.generate_traces(seeds, 200, lambda_s=20.0)
+    o = m.SimOptions(policy="nopart", cluster_size=16)
+    want = m.simulate_batch(ctx, hb, o).metrics
+    gen, s1, s2 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(gen):
+        torch.cuda._sleep(50_000_000)  # ~25 ms: the generator finishes long after the launches
+    db = m.generate_traces_device(ctx, seeds, 200, lambda_s=20.0, stream=gen)
+    c2 = m.Context(0)
+    try:
+        r1 = m.simulate_batch(ctx, db, o, stream=s1, defer=True)
+        r2 = m.simulate_batch(c2, db[8:24], o, stream=s2, defer=True)
+        got1, got2 = r1().metrics, r2().metrics
+        assert got1.tobytes() == want.tobytes()
+        assert got2.tobytes() == want[8:24].tobytes()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(gen):
+            torch.cuda._sleep(50_000_000)
+        db2 = m.generate_traces_device(ctx, seeds, 200, lambda_s=20.0, stream=gen)
+        st = m.best_static_partition(c2, db2, cluster_size=16, stream=s2, chosen_only=True)
+        sh = m.best_static_partition(ctx, hb, cluster_size=16)
+        assert [e for e, _ in st] == [e for e, _ in sh]
+    finally:
+        c2.close()

@@ -29,10 +29,13 @@ def ev(stream):
     return e
 
 
-def batch(chosen_only, chunks=1):
+def batch(chosen_only, chunks=1, delay_ms=0.0):
     t0 = ev(torch.cuda.current_stream())
     for s in (s_a, s_b, s_c):
         s.wait_stream(torch.cuda.current_stream())
+    if delay_ms > 0:  # the static search (and its re-run) start delay_ms after miso
+        with torch.cuda.stream(s_b):
+            torch.cuda._sleep(int(delay_ms * 1.965e6))
     a0 = ev(s_a)
     p_nop = miso.simulate_batch(ctx_a, traces, miso.SimOptions(policy="nopart", cluster_size=100), stream=s_a, defer=True)
     a1 = ev(s_a)
@@ -96,6 +99,13 @@ def batch_probes_full(rest_waits=False):
 
 
 out = {}
+if len(sys.argv) > 1 and sys.argv[1] == "delay":  # static search started after a delay
+    for rep in range(2):
+        for d in (0, 80, 300):
+            batch(True, 1, d)
+            out[f"pruned_delay{d}_{rep}"] = batch(True, 1, d)
+    print(json.dumps(out))
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "probes":  # probes (full metrics) first, then the rest
     for rep in range(2):
         for w in (False, True):
