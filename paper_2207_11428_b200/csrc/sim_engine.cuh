@@ -162,6 +162,57 @@ __shared__ Ctx g_sim_ctx;
 // reopt_and_apply's m x 5 effective estimated speeds (the search's rows)
 __shared__ double g_sim_rows[35];
 
+// Asynchronous STP (the ASYNC kernels): the engine warp posts every change of a job's STP term
+// and the end of every processed event into this ring; a second warp of the block replays
+// them in order and computes the sequential STP sums, the series and the integral off the
+// engine's critical path. Single producer (engine lane 0), single consumer (helper).
+struct StpMsg {
+  unsigned long long head;  // job index (term change) | kind << 32
+  unsigned long long bits;  // the new term's bits (change) or the event time in us (event)
+};
+enum : int32_t { kStpChange = 0, kStpEvent = 1, kStpEnd = 2 };
+
+// The ring is a single-producer / single-consumer queue published by a block fence and volatile
+// index stores -- an ordering compute-sanitizer racecheck does not follow (it reports the
+// cross-warp accesses as hazards). MISO_SIM_STP_ATOMIC_RING=1 builds the same protocol with
+// every ring access a shared-memory atomic (racecheck-clean, slower).
+#ifndef MISO_SIM_STP_ATOMIC_RING
+#define MISO_SIM_STP_ATOMIC_RING 0
+#endif
+__device__ __forceinline__ uint32_t ring_ld(uint32_t* p) {
+  if constexpr (MISO_SIM_STP_ATOMIC_RING) return atomicAdd(p, 0u);
+  else return *reinterpret_cast<volatile uint32_t*>(p);
+}
+__device__ __forceinline__ void ring_st(uint32_t* p, uint32_t v) {
+  if constexpr (MISO_SIM_STP_ATOMIC_RING) atomicExch(p, v);
+  else *reinterpret_cast<volatile uint32_t*>(p) = v;
+}
+__device__ __forceinline__ unsigned long long ring_ld(unsigned long long* p) {
+  if constexpr (MISO_SIM_STP_ATOMIC_RING) return atomicAdd(p, 0ull);
+  else return *p;
+}
+__device__ __forceinline__ void ring_st(unsigned long long* p, unsigned long long v) {
+  if constexpr (MISO_SIM_STP_ATOMIC_RING) atomicExch(p, v);
+  else *p = v;
+}
+constexpr int kStpRing = 128;
+struct StpRing {
+  uint32_t tail;  // messages posted (engine lane 0 writes)
+  uint32_t head;  // messages consumed (helper lane 0 writes)
+  int quit;       // 1: the task was rejected before its event loop; 2: producer watchdog fired
+  StpMsg msg[kStpRing];
+};
+__shared__ StpRing g_stp_ring;
+
+// the engine and helper warps meet here twice: after the engine's init, and at the end. The two
+// warps reach it from different code, so it is the non-aligned barrier (barrier.sync without
+// .aligned: participating threads may execute different barrier instructions); each warp
+// reconverges first.
+__device__ __forceinline__ void stp_pair_barrier() {
+  __syncwarp();
+  asm volatile("barrier.sync 1, 64;" ::: "memory");
+}
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Single-writer update of a warp-uniform Ctx field (shared memory): every lane evaluates the
@@ -253,7 +304,7 @@ __device__ __forceinline__ int lut_index(const uint8_t* k) {
 // use the LOG = false instantiation, which carries no log calls at all. STP: the STP series and
 // integral are tracked (SimParams::track_stp; the best-static search's JCT-only candidate runs
 // use STP = false, which carries no STP bookkeeping).
-template <int POL, bool PRUNE, bool LOG, bool STP>
+template <int POL, bool PRUNE, bool LOG, bool STP, bool ASYNC = false>
 struct Engine {
 
   static __device__ __forceinline__ void sync_jst(int ji, const DJob& j) {
@@ -384,6 +435,9 @@ struct Engine {
     Ctx& c = g_sim_ctx;
     DJob& j = c.jobs[ji];
     advance_job(j);
+    // the job's current STP term (== rate_eff[ji], which every term change keeps in step)
+    const double old_term = (progressing(j.phase) && !(j.flags & kDone)) ? j.rate : 0.0;
+    (void)old_term;
     if constexpr (PRUNE) {
     if (c.prune && j.first_progress_us >= 0 && !(j.flags & kDone)) {  // retire the old-rate term
       LB_SET(c.lb_p, c.lb_p - (j.lbp));
@@ -401,7 +455,9 @@ struct Engine {
     }
     // the STP window's sums only need redoing from ji if the job's term actually changed
     const double re = (progressing(phase) && !(j.flags & kDone)) ? j.rate : 0.0;
-    if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
+    if constexpr (ASYNC) {  // the helper warp owns rate_eff: post the change
+      if (__double_as_longlong(re) != __double_as_longlong(old_term)) stp_post(kStpChange, ji, __double_as_longlong(re));
+    } else if (__double_as_longlong(re) != __double_as_longlong(c.rate_eff[ji])) {
       c.rate_eff[ji] = re;
       if (re != 0.0 && ji >= c.stp_hi) {  // the summed range grows: its new blocks need sums
         if constexpr (STP) {
@@ -446,15 +502,32 @@ struct Engine {
   // the chain restarts at the smallest index changed since the previous refresh.
   static __device__ void refresh_stp() {
     Ctx& c = g_sim_ctx;
-    if constexpr (!STP) return;
+    if constexpr (!STP || ASYNC) return;
     if (!c.stp_dirty) return;
     c.stp_dirty = false;
+    const int lo = c.stp_lo, hi = c.stp_hi;
+    const double s = stp_sum(c.stp_cmin, lo, hi);
+    c.stp_cmin = INT32_MAX;
+    if (s != c.stp_cur) {
+      c.stp_cur = s;
+      if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
+        c.stp_series[2 * c.stp_points] = s_from_us(c.now);
+        c.stp_series[2 * c.stp_points + 1] = s;
+      }
+      __syncwarp();
+      CTX_SET(c.stp_points, c.stp_points + 1);
+    }
+  }
+
+  // The window's sequential sum after changes at indices >= cmin: rate_eff[lo, hi) (zeros
+  // outside), restarting from the cached partial sum before cmin's block. (Called by all lanes
+  // of one warp; lane 0 updates the cache.)
+  static __device__ __forceinline__ double stp_sum(int cmin, int lo, int hi) {
+    Ctx& c = g_sim_ctx;
     const double* r = c.rate_eff;
     double* P = c.stp_prefix;  // P[q]: the sum through index 8q + 7, cached at block ends
-    const int lo = c.stp_lo, hi = c.stp_hi;
-    int i0 = c.stp_cmin > lo ? c.stp_cmin : lo;
+    int i0 = cmin > lo ? cmin : lo;
     if (i0 > hi) i0 = hi;  // changes at not-yet-arrived indices: the window's sum is unchanged
-    c.stp_cmin = INT32_MAX;
     // restart at i0's 8-aligned block from the cached sum before it: the block's terms below i0
     // are unchanged, so re-adding them reproduces the same partial sums (and jobs below lo are
     // done, contributing +0.0, so a start below lo is exact too)
@@ -498,18 +571,115 @@ struct Engine {
     for (int k = 0; k < 7; ++k)
       if (i + k < hi) s = s + t[k];
     __syncwarp();
-    if (hi <= lo) s = 0.0;
-    if (s != c.stp_cur) {
-      c.stp_cur = s;
-      if (c.stp_series && c.stp_points < c.stp_cap && lane_id() == 0) {
-        c.stp_series[2 * c.stp_points] = s_from_us(c.now);
-        c.stp_series[2 * c.stp_points + 1] = s;
+    return hi <= lo ? 0.0 : s;
+  }
+
+  // ---- asynchronous STP (ASYNC kernels) ----------------------------------------------------
+  // Engine side: one message into the ring, waiting only if the helper is a whole ring behind.
+  static __device__ __forceinline__ void stp_post(int32_t kind, int32_t idx, int64_t bits) {
+    // every lane of the converged engine warp executes the same stores (identical values at the
+    // same addresses): no divergent branch, no reconvergence (the atomic build: lane 0 alone)
+    if (!MISO_SIM_STP_ATOMIC_RING || lane_id() == 0) {
+      StpRing& R = g_stp_ring;
+      const uint32_t t = ring_ld(&R.tail);
+      if (t - ring_ld(&R.head) >= static_cast<uint32_t>(kStpRing)) {  // full: the helper is behind
+        uint32_t spins = 0;
+        while (t - ring_ld(&R.head) >= static_cast<uint32_t>(kStpRing)) {
+          __nanosleep(64);
+          if (++spins > (1u << 26)) {  // watchdog (never expected): flag it, do not hang
+            R.quit = 2;
+            break;
+          }
+        }
+      }
+      StpMsg& m = R.msg[t % kStpRing];
+      ring_st(&m.head, static_cast<unsigned long long>(static_cast<uint32_t>(idx)) |
+                           (static_cast<unsigned long long>(static_cast<uint32_t>(kind)) << 32));
+      ring_st(&m.bits, static_cast<unsigned long long>(bits));
+      __threadfence_block();
+      ring_st(&R.tail, t + 1);
+    }
+    if (MISO_SIM_STP_ATOMIC_RING) __syncwarp();
+  }
+
+  // Helper warp: replays the engine's messages in order -- term changes into rate_eff, and at
+  // each event's end the reference's integral step (with the sum after the previous event) and
+  // then refresh_stp (sim.hpp:227-232, 353-361), exactly the synchronous path's operations.
+  static __device__ void stp_helper() {
+    Ctx& c = g_sim_ctx;
+    StpRing& R = g_stp_ring;
+    const int lane = lane_id();
+    int hi = 0, cmin = INT32_MAX;
+    bool dirty = false;
+    double cur = 0.0, integ = 0.0;
+    int64_t last = 0, pts = 0;
+    uint32_t h = 0;
+    uint32_t idle = 0;
+    for (;;) {
+      const uint32_t t = __shfl_sync(0xffffffffu, lane == 0 ? ring_ld(&R.tail) : 0u, 0);  // one view
+      if (t == h) {
+        __nanosleep(32);
+        if (++idle > (1u << 28)) return;  // watchdog (never expected): the engine stopped posting
+        continue;
+      }
+      idle = 0;
+      __threadfence_block();
+      for (; h != t; ++h) {
+        StpMsg& slot = R.msg[h % kStpRing];
+        const unsigned long long mh = ring_ld(&slot.head);
+        const int64_t mbits = static_cast<int64_t>(ring_ld(&slot.bits));
+        const int32_t kind = static_cast<int32_t>(mh >> 32);
+        if (kind == kStpChange) {
+          const int ji = static_cast<int32_t>(mh & 0xffffffffu);
+          if (mbits != __double_as_longlong(c.rate_eff[ji])) {
+            if (lane == 0) c.rate_eff[ji] = __longlong_as_double(mbits);
+            __syncwarp();
+            if (mbits != 0 && ji >= hi) {  // the summed range grows: its new blocks need sums
+              cmin = hi < cmin ? hi : cmin;
+              hi = ji + 1;
+            }
+            cmin = ji < cmin ? ji : cmin;
+            dirty = true;
+          }
+        } else if (kind == kStpEvent) {
+          const int64_t te = mbits;
+          integ = integ + cur * s_from_us(te - last);
+          last = te;
+          if (dirty) {
+            dirty = false;
+            const double sum = stp_sum(cmin, 0, hi);
+            cmin = INT32_MAX;
+            if (sum != cur) {
+              cur = sum;
+              if (c.stp_series && pts < c.stp_cap && lane == 0) {
+                c.stp_series[2 * pts] = s_from_us(te);
+                c.stp_series[2 * pts + 1] = sum;
+              }
+              ++pts;
+            }
+          }
+        } else {  // kStpEnd
+          if (lane == 0) {
+            c.stp_integral = integ;
+            c.stp_points = pts;
+            c.stp_cur = cur;
+          }
+          __syncwarp();
+          return;
+        }
       }
       __syncwarp();
-      CTX_SET(c.stp_points, c.stp_points + 1);
+      if (lane == 0) ring_st(&R.head, h);
     }
   }
 
+  // the helper warp's whole life: wait for the engine's init, replay, meet the engine at the end
+  static __device__ void stp_helper_main() {
+    stp_pair_barrier();
+    if (g_stp_ring.quit == 1) return;  // the task was rejected: no event loop
+    stp_helper();
+    stp_pair_barrier();
+  }
 
   // ---- queue (std::set ordered by (arrival_us, entry_seq == idx)) -------------------------
   static __device__ void enqueue(int ji) {
@@ -1269,14 +1439,19 @@ struct Engine {
       const double base = j.base;
       if (fabs(j.consumed - base) > 1e-6 * base + 1e-9) fail(MISO_B200_SIM_INVARIANT);
     }
+    const double old_term = (progressing(j.phase) && !(j.flags & kDone)) ? j.rate : 0.0;
     j.remaining = 0;
     j.flags |= kDone;
     ++j.epoch;
     clear_slot(ji);
-    c.rate_eff[ji] = 0.0;
-    if constexpr (STP) {
-      c.stp_dirty = true;
-      CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+    if constexpr (ASYNC) {
+      if (__double_as_longlong(old_term) != 0) stp_post(kStpChange, ji, 0);
+    } else {
+      c.rate_eff[ji] = 0.0;
+      if constexpr (STP) {
+        c.stp_dirty = true;
+        CTX_SET(c.stp_cmin, ji < c.stp_cmin ? ji : c.stp_cmin);
+      }
     }
     sync_jst(ji, j);
     int stp_lo = c.stp_lo;
@@ -1438,6 +1613,11 @@ struct Engine {
         m.status = MISO_B200_SIM_BAD_INPUT;
         m.detail = bad;
         b.metrics[warp] = m;
+      }
+      if constexpr (ASYNC) {  // release the helper warp
+        if (lane == 0) g_stp_ring.quit = 1;
+        __syncwarp();
+        stp_pair_barrier();
       }
       return;
     }
@@ -1614,6 +1794,17 @@ struct Engine {
       for (int off = 16; off > 0; off >>= 1) lb_unstarted += __shfl_xor_sync(0xffffffffu, lb_unstarted, off);
       c.lb_unstarted = lb_unstarted;
     }
+    if constexpr (ASYNC) {  // the helper's state: an empty ring, rate_eff (zeroed above) and a
+                            // zeroed partial-sum cache (every term starts at 0.0)
+      for (int q = lane; q < (J + 7) / 8 + 1; q += 32) c.stp_prefix[q] = 0.0;
+      if (lane == 0) {
+        g_stp_ring.tail = 0;
+        g_stp_ring.head = 0;
+        g_stp_ring.quit = 0;
+      }
+      __syncwarp();
+      stp_pair_barrier();
+    }
     c.seq = static_cast<uint64_t>(JT);  // one arrival event per trace job (sim.hpp:219)
     bool bad_job = false;
     for (int i = lane; i < JT; i += 32) bad_job = bad_job || c.jobs[i].min_kind == 0xFF;
@@ -1635,13 +1826,14 @@ struct Engine {
       }
       clear_slot(slot);
       __syncwarp();
-      if constexpr (STP) {
+      if constexpr (STP && !ASYNC) {
         CTX_SET(c.stp_integral, c.stp_integral + (c.stp_cur * s_from_us(ev.t - c.stp_last)));
         c.stp_last = ev.t;
       }
       c.now = ev.t;
       dispatch(slot, static_cast<uint32_t>(ev.pk & 7));
       drain_queue();
+      if constexpr (ASYNC) stp_post(kStpEvent, 0, ev.t);  // the helper's integral step + refresh
       refresh_stp();
       __syncwarp();
     if constexpr (PRUNE) {
@@ -1665,6 +1857,11 @@ struct Engine {
     }
     }
     c.processed = processed;
+    if constexpr (ASYNC) {  // the helper finishes the STP; its results are in Ctx after this
+      stp_post(kStpEnd, 0, 0);
+      stp_pair_barrier();
+      if (g_stp_ring.quit == 2) c.status = MISO_B200_SIM_INVARIANT;
+    }
     // every pushed event is popped by the reference exactly once (live or stale), so its
     // max_events budget (sim.hpp:224, stale pops included) is exceeded iff the pushes exceed it
     CTX_SET(c.status, (c.status == 0 && c.seq > prm.max_events) ? MISO_B200_SIM_EVENT_BUDGET : c.status);

@@ -15,14 +15,29 @@
 #ifndef MISO_SIM_MIN_BLOCKS
 #define MISO_SIM_MIN_BLOCKS 32
 #endif
+// ASYNC (engine warp + STP helper warp per block): 8 two-warp blocks per SM keep the engine's
+// register budget of the one-warp dynamic kernels
+#ifndef MISO_SIM_MIN_BLOCKS_ASYNC
+#define MISO_SIM_MIN_BLOCKS_ASYNC 8
+#endif
 
 namespace miso_b200 {
 
-template <int POL, bool PRUNE, bool LOG, bool STP>
-__global__ void __launch_bounds__(32, (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE)
-                                          ? MISO_SIM_MIN_BLOCKS_DYN : MISO_SIM_MIN_BLOCKS)
+template <int POL, bool PRUNE, bool LOG, bool STP, bool ASYNC>
+__global__ void __launch_bounds__(ASYNC ? 64 : 32,
+                                  ASYNC ? MISO_SIM_MIN_BLOCKS_ASYNC
+                                        : ((POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE)
+                                               ? MISO_SIM_MIN_BLOCKS_DYN : MISO_SIM_MIN_BLOCKS))
 simulate_kernel(SimBatch b, SimParams prm, ModelW w) {
-  simk::Engine<POL, PRUNE, LOG, STP>::run(b, prm, w);
+  using E = simk::Engine<POL, PRUNE, LOG, STP, ASYNC>;
+  if constexpr (ASYNC) {
+    if (static_cast<int>(blockIdx.x) >= b.n_seeds) return;
+    if (threadIdx.x >= 32) {  // warp 1: the STP helper
+      E::stp_helper_main();
+      return;
+    }
+  }
+  E::run(b, prm, w);
 }
 
 // The engine uses ~2.5 KB of shared memory per block and lives on L1 hits (job records, event
@@ -38,12 +53,33 @@ inline int sim_carveout_env() {
   return v;
 }
 
-template <int POL, bool PRUNE, bool LOG, bool STP>
+// The asynchronous-STP variant (an STP helper warp beside each engine warp) for the dynamic
+// policies when the tasks fit the GPU in about one wave -- a latency-bound batch, where taking
+// the STP chain off the engine's critical path pays; a many-wave batch keeps one-warp blocks
+// (twice the resident tasks). MISO_B200_SIM_ASYNC_STP=0/1 forces it off/on.
+inline bool sim_async_stp(int n_tasks) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("MISO_B200_SIM_ASYNC_STP");
+    mode = e ? atoi(e) : -1;
+  }
+  if (mode >= 0) return mode != 0;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return n_tasks <= sms * MISO_SIM_MIN_BLOCKS_ASYNC;
+}
+
+template <int POL, bool PRUNE, bool LOG, bool STP, bool ASYNC = false>
 cudaError_t launch_sim_k(const SimBatch& b, const SimParams& p, const ModelW& w, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     attr_set = true;
-    auto kern = simulate_kernel<POL, PRUNE, LOG, STP>;
+    auto kern = simulate_kernel<POL, PRUNE, LOG, STP, ASYNC>;
     int pct = sim_carveout_env();
     if (pct == -3) {
       cudaFuncAttributes fa{};
@@ -51,7 +87,7 @@ cudaError_t launch_sim_k(const SimBatch& b, const SimParams& p, const ModelW& w,
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
       if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && smem_sm > 0 &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, 32, 0) == cudaSuccess) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, ASYNC ? 64 : 32, 0) == cudaSuccess) {
         const size_t need = size_t(blocks) * (fa.sharedSizeBytes + 1024);  // + per-block reserve
         pct = static_cast<int>(std::min<size_t>(100, (need * 100 + smem_sm - 1) / smem_sm));
       } else {
@@ -64,7 +100,8 @@ cudaError_t launch_sim_k(const SimBatch& b, const SimParams& p, const ModelW& w,
       if (e != cudaSuccess) return e;
     }
   }
-  simulate_kernel<POL, PRUNE, LOG, STP><<<b.n_seeds, 32, 0, s>>>(b, p, w);  // one warp (block) per task
+  // one block per task: the engine warp (and with ASYNC the STP helper warp)
+  simulate_kernel<POL, PRUNE, LOG, STP, ASYNC><<<b.n_seeds, ASYNC ? 64 : 32, 0, s>>>(b, p, w);
   return cudaGetLastError();
 }
 
@@ -78,6 +115,9 @@ cudaError_t launch_sim(const SimBatch& b, const SimParams& p, const ModelW& w, c
                          : launch_sim_k<POL, PRUNE, true, false>(b, p, w, s);
   } else {
     if (b.log) return cudaErrorInvalidValue;
+  }
+  if constexpr (!PRUNE && (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE)) {
+    if (p.track_stp && sim_async_stp(b.n_seeds)) return launch_sim_k<POL, PRUNE, false, true, true>(b, p, w, s);
   }
   return p.track_stp ? launch_sim_k<POL, PRUNE, false, true>(b, p, w, s)
                      : launch_sim_k<POL, PRUNE, false, false>(b, p, w, s);

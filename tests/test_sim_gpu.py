@@ -310,3 +310,20 @@ def test_device_trace_batch_stream_order(ctx):
         assert [e for e, _ in st] == [e for e, _ in sh]
     finally:
         c2.close()
+
+
+def test_async_stp_matches_sync():
+    """The asynchronous-STP kernels (an STP helper warp per task; the default for batches
+    that fit one wave) against the synchronous ones, forced per process with
+    MISO_B200_SIM_ASYNC_STP: miso and oracle metrics and STP series byte-identical
+    (tools/async_stp_check.py on 256 config-4 seeds)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    p = subprocess.run([sys.executable, str(root / "tools" / "async_stp_check.py"), "256"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stdout + p.stderr
+    res = json.loads(p.stdout.strip().splitlines()[-1])
+    assert all(res["identical"].values()), res

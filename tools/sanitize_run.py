@@ -58,5 +58,7 @@ single = [t for i, t in enumerate(traces) if i != 2]
 m.best_static_partition(ctx, single, cluster_size=4, chosen_only=True)  # pruned kernel
 db = m.generate_traces_device(ctx, np.arange(8, dtype=np.uint64), 50, lambda_s=10.0)
 m.simulate_batch(ctx, db, m.SimOptions(policy="miso", cluster_size=4, predictor="noisy"))
+# the asynchronous-STP kernels (no log; STP series): engine and helper warps
+m.simulate_batch(ctx, list(traces), m.SimOptions(policy="oracle", cluster_size=4), stp_cap=2000)
 torch.cuda.synchronize()
 print("sanitize run ok")
