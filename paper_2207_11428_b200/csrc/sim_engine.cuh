@@ -197,7 +197,7 @@ __device__ __forceinline__ void ring_st(unsigned long long* p, unsigned long lon
 }
 constexpr int kStpRing = 128;
 struct StpRing {
-  uint32_t tail;  // messages posted (engine lane 0 writes)
+  uint32_t tail;  // messages posted (the engine warp writes it)
   uint32_t head;  // messages consumed (helper lane 0 writes)
   int quit;       // 1: the task was rejected before its event loop; 2: producer watchdog fired
   StpMsg msg[kStpRing];
