@@ -703,14 +703,36 @@ class TrialRunner:
     only pruning: a candidate stops once it provably loses), the optsta re-run with the chosen
     partition, and miso (noisy predictor, rng_seed = seed). Three
     contexts (one simulation workspace each) on three streams: nopart and miso overlap the
-    static search and the optsta re-run that depends on it."""
+    static search and the optsta re-run that depends on it.
+
+    For batches that fit the GPU in about one wave (<= 8 seeds per SM, config 4) the miso
+    simulations run on their own SM partition (a green context of ~38% of the SMs, 56 of 148)
+    and the other sets on the rest, so the two never share an SM's instruction cache
+    (paper_2207_11428_b200/partition.py; 190 -> 179 ms per 1024-seed step on one box,
+    tools/green_c4.py). Larger batches (config 5: 8192 seeds) share the whole GPU, which
+    measured faster there. MISO_C4_GREEN_SMS=<k> sets the miso partition's SM count (0: off)."""
 
     def __init__(self, device):
         import torch
         import paper_2207_11428_b200 as miso
         self.miso = miso
+        self.device = device
         self.ctx = [miso.Context(device) for _ in range(3)]
         self.st = [torch.cuda.Stream() for _ in range(3)]
+        self.part, self.part_st, self.part_note = None, None, "shared GPU"
+        sms = torch.cuda.get_device_properties(device).multi_processor_count
+        self.sms = sms
+        k = int(os.environ.get("MISO_C4_GREEN_SMS", str(int(round(sms * 0.38 / 8)) * 8)))
+        if k > 0:
+            try:
+                from paper_2207_11428_b200.partition import SmPartition
+                self.part = SmPartition(device, k)
+                # miso on group 0; nopart and the static search (+ re-run) on group 1
+                self.part_st = (self.part.streams(1, 1)[0], self.part.streams(1, 1)[0],
+                                self.part.streams(0, 1)[0])
+                self.part_note = f"miso on {self.part.sms[0]} SMs, other sets on {self.part.sms[1]} SMs (green contexts)"
+            except RuntimeError as e:
+                self.part, self.part_note = None, f"shared GPU (no SM partition: {e})"
 
     def __call__(self, traces, pruned=True):
         """pruned: the chosen-only best-static search (config 4's default; config 5's 8192
@@ -721,6 +743,10 @@ class TrialRunner:
         if env is not None:
             pruned = env == "1"
         (ca, cb, cc), (sa, sb, sc) = self.ctx, self.st
+        self.last_note = "shared GPU"
+        if self.part is not None and len(traces) <= 8 * self.sms:
+            sa, sb, sc = self.part_st
+            self.last_note = self.part_note
         p_nop = miso.simulate_batch(ca, traces, miso.SimOptions(policy="nopart", cluster_size=100),
                                     stream=sa, defer=True)
         p_mis = miso.simulate_batch(cc, traces, miso.SimOptions(policy="miso", cluster_size=100,
@@ -738,6 +764,8 @@ class TrialRunner:
     def close(self):
         for c in self.ctx:
             c.close()
+        if self.part is not None:
+            self.part.close()
 
 
 def ref_trials(seeds):
@@ -806,7 +834,8 @@ def sec_c4(args, D, runner, seeds_per_rank=1024, steps=3):
            "data": "synthetic (generate_trace seeds, generated on the device)",
            "median_jct_norm": {"optsta": float(np.median(sta.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"])),
                                "miso": float(np.median(mis.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"]))},
-           "gpu_launches_per_step": "4 simulate_kernel + host-side upload/readback"}
+           "gpu_launches_per_step": "4 simulate_kernel + host-side upload/readback",
+           "placement": runner.last_note}
     cap = ncu_capture("sim_kernel_ncu.json")
     bound = {"bound": "latency (one warp walks one seed's sequential event chain)",
              "miso_ms": ms_miso, "miso_us_per_event_per_warp": us_ev,
@@ -1006,6 +1035,7 @@ def sec_c5(args, D, ctx, runner, steps=10):
         "trials": {"value": S / trial_s, "unit": "trials/s", "s": trial_s,
                    "seeds_in_flight_per_gpu": s_hi - s_lo,
                    "static_search": "chosen-only pruned" if pruned else "full",
+                   "placement": runner.last_note,
                    "device_trace_gen_s_rank0": gen_s},
         "median_jct_norm": {"optsta": float(np.median(r[:, 1] / r[:, 0])),
                             "miso": float(np.median(r[:, 2] / r[:, 0]))},

@@ -327,3 +327,32 @@ def test_async_stp_matches_sync():
     assert p.returncode == 0, p.stdout + p.stderr
     res = json.loads(p.stdout.strip().splitlines()[-1])
     assert all(res["identical"].values()), res
+
+
+def test_sm_partition_streams_same_results(ctx):
+    """paper_2207_11428_b200.partition.SmPartition (green contexts): simulations launched on
+    either SM group's streams -- miso on one, nopart and the chosen-only static search on the
+    other, concurrently -- give the bytes of the shared-GPU runs."""
+    import paper_2207_11428_b200 as m
+    from paper_2207_11428_b200.partition import SmPartition
+    tr = m.generate_traces_device(ctx, np.arange(48, dtype=np.uint64), 300, lambda_s=20.0)
+    om = m.SimOptions(policy="miso", cluster_size=16, predictor="noisy")
+    on = m.SimOptions(policy="nopart", cluster_size=16)
+    want_m = m.simulate_batch(ctx, tr, om).metrics
+    want_n = m.simulate_batch(ctx, tr, on).metrics
+    want_s = m.best_static_partition(ctx, tr, cluster_size=16, chosen_only=True)
+    part = SmPartition(0, 56)
+    c2, c3 = m.Context(0), m.Context(0)
+    try:
+        (s_m,), (s_n, s_s) = part.streams(0, 1), part.streams(1, 2)
+        assert part.sms[0] >= 8 and part.sms[1] >= 8
+        pm = m.simulate_batch(ctx, tr, om, stream=s_m, defer=True)
+        pn = m.simulate_batch(c2, tr, on, stream=s_n, defer=True)
+        st = m.best_static_partition(c3, tr, cluster_size=16, stream=s_s, chosen_only=True)
+        assert pm().metrics.tobytes() == want_m.tobytes()
+        assert pn().metrics.tobytes() == want_n.tobytes()
+        assert [e for e, _ in st] == [e for e, _ in want_s]
+    finally:
+        c2.close()
+        c3.close()
+        part.close()
