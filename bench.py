@@ -706,10 +706,11 @@ class TrialRunner:
     static search and the optsta re-run that depends on it.
 
     For batches that fit the GPU in about one wave (<= 8 seeds per SM, config 4) the miso
-    simulations run on their own SM partition (a green context of ~38% of the SMs, 56 of 148)
+    simulations run on their own SM partition (a green context of ~43% of the SMs, 64 of 148)
     and the other sets on the rest, so the two never share an SM's instruction cache
-    (paper_2207_11428_b200/partition.py; 190 -> 179 ms per 1024-seed step on one box,
-    tools/green_c4.py). Larger batches (config 5: 8192 seeds) share the whole GPU, which
+    (paper_2207_11428_b200/partition.py). On the partition the miso batch no longer fits one
+    wave of two-warp blocks, so the library picks the one-warp (synchronous STP) kernel there
+    (config 4: 5.37e3 -> 6.5e3 trials/s on one box). Larger batches (config 5: 8192 seeds) share the whole GPU, which
     measured faster there. MISO_C4_GREEN_SMS=<k> sets the miso partition's SM count (0: off)."""
 
     def __init__(self, device):
@@ -722,7 +723,7 @@ class TrialRunner:
         self.part, self.part_st, self.part_note = None, None, "shared GPU"
         sms = torch.cuda.get_device_properties(device).multi_processor_count
         self.sms = sms
-        k = int(os.environ.get("MISO_C4_GREEN_SMS", str(int(round(sms * 0.38 / 8)) * 8)))
+        k = int(os.environ.get("MISO_C4_GREEN_SMS", str(int(round(sms * 0.43 / 8)) * 8)))
         if k > 0:
             try:
                 from paper_2207_11428_b200.partition import SmPartition

@@ -1,6 +1,8 @@
 // sim_launch.cuh -- the simulator kernel and its launcher, included only by the per-policy TUs
 // (sim_pol_*.cu), each of which explicitly instantiates its policy.
 #pragma once
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -53,25 +55,56 @@ inline int sim_carveout_env() {
   return v;
 }
 
+// SMs the launch stream's kernels can use: the device's, or its green context's SM partition
+// (driver entry points looked up at run time, so the library links no libcuda).
+inline int sim_stream_sms(cudaStream_t stream) {
+  static int dev_sms = 0;
+  if (dev_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev_sms <= 0) dev_sms = 148;
+  }
+  using GetGreen = CUresult (*)(CUstream, CUgreenCtx*);
+  using GetRes = CUresult (*)(CUgreenCtx, CUdevResource*, CUdevResourceType);
+  static GetGreen get_green = nullptr;
+  static GetRes get_res = nullptr;
+  static bool looked = false;
+  if (!looked) {
+    looked = true;
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamGetGreenCtx", &f1, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuGreenCtxGetDevResource", &f2, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+      get_green = reinterpret_cast<GetGreen>(f1);
+      get_res = reinterpret_cast<GetRes>(f2);
+    }
+  }
+  if (get_green && stream) {
+    CUgreenCtx g = nullptr;
+    CUdevResource r{};
+    if (get_green(static_cast<CUstream>(stream), &g) == CUDA_SUCCESS && g &&
+        get_res(g, &r, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS && r.sm.smCount > 0)
+      return static_cast<int>(r.sm.smCount);
+  }
+  return dev_sms;
+}
+
 // The asynchronous-STP variant (an STP helper warp beside each engine warp) for the dynamic
-// policies when the tasks fit the GPU in about one wave -- a latency-bound batch, where taking
-// the STP chain off the engine's critical path pays; a many-wave batch keeps one-warp blocks
-// (twice the resident tasks). MISO_B200_SIM_ASYNC_STP=0/1 forces it off/on.
-inline bool sim_async_stp(int n_tasks) {
+// policies when the tasks fit the SMs the launch stream can use in about one wave -- a
+// latency-bound batch, where taking the STP chain off the engine's critical path pays; a
+// many-wave batch keeps one-warp blocks (twice the resident tasks). MISO_B200_SIM_ASYNC_STP=0/1
+// forces it off/on.
+inline bool sim_async_stp(int n_tasks, cudaStream_t stream) {
   static int mode = -2;
   if (mode == -2) {
     const char* e = getenv("MISO_B200_SIM_ASYNC_STP");
     mode = e ? atoi(e) : -1;
   }
   if (mode >= 0) return mode != 0;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return n_tasks <= sms * MISO_SIM_MIN_BLOCKS_ASYNC;
+  return n_tasks <= sim_stream_sms(stream) * MISO_SIM_MIN_BLOCKS_ASYNC;
 }
 
 template <int POL, bool PRUNE, bool LOG, bool STP, bool ASYNC = false>
@@ -117,7 +150,7 @@ cudaError_t launch_sim(const SimBatch& b, const SimParams& p, const ModelW& w, c
     if (b.log) return cudaErrorInvalidValue;
   }
   if constexpr (!PRUNE && (POL == MISO_B200_POLICY_MISO || POL == MISO_B200_POLICY_ORACLE)) {
-    if (p.track_stp && sim_async_stp(b.n_seeds)) return launch_sim_k<POL, PRUNE, false, true, true>(b, p, w, s);
+    if (p.track_stp && sim_async_stp(b.n_seeds, s)) return launch_sim_k<POL, PRUNE, false, true, true>(b, p, w, s);
   }
   return p.track_stp ? launch_sim_k<POL, PRUNE, false, true>(b, p, w, s)
                      : launch_sim_k<POL, PRUNE, false, false>(b, p, w, s);
