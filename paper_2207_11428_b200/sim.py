@@ -509,20 +509,32 @@ def static_candidates(traces: Sequence[Trace], catalog=None):
     cat = list(catalog if catalog is not None else DEFAULT_CATALOG)
     catc = np.asarray(cat, np.uint8).reshape(-1, 5)
     largest = np.array([max(k for k in range(5) if c[k] > 0) for c in catc])
+    assert list(GPC) == sorted(GPC) and list(MEM_GB) == sorted(MEM_GB)
     offs, _, _, _, mem, qos, _ = _csr(traces)
-    if hasattr(mem, "cpu"):  # device-resident batch: the feasibility pass runs on host copies
-        traces.wait()
-        offs, mem, qos = offs.cpu().numpy(), mem.cpu().numpy(), qos.cpu().numpy()
     # min_slice_for: the smallest kind with memory_gb >= mem and gpc >= gpc(qos); both tables
     # are non-decreasing in the kind index, so it is max(first kind with enough memory, qos)
-    mk = np.maximum(np.searchsorted(np.asarray(MEM_GB), np.asarray(mem, np.int64), side="left"),
-                    np.maximum(np.asarray(qos, np.int64), 0))
-    assert list(GPC) == sorted(GPC) and list(MEM_GB) == sorted(MEM_GB)
-    if len(mk) and mk.max() > 4:
-        j = int(np.argmax(mk > 4))
-        ti = int(np.searchsorted(offs, j, side="right") - 1)
-        raise ValueError(f"trace {ti}: a job fits no slice kind")
-    need = np.maximum.reduceat(mk, offs[:-1]) if len(traces) else np.zeros(0, np.int64)
+    if isinstance(traces, DeviceTraceBatch) and len(traces):
+        # device-resident, equal-length traces: the per-job pass runs on the device and only
+        # each trace's largest minimum kind (and the first unfittable job) comes back
+        import torch
+        traces.wait()
+        dev = mem.device
+        mk = torch.maximum(torch.searchsorted(torch.tensor(MEM_GB, dtype=torch.int64, device=dev),
+                                              mem.to(torch.int64), right=False),
+                           qos.to(torch.int64).clamp(min=0)).view(traces.n, traces.job_count)
+        need_t = mk.max(dim=1).values
+        need = need_t.cpu().numpy()
+        if len(need) and need.max() > 4:
+            ti = int(np.argmax(need > 4))
+            raise ValueError(f"trace {ti}: a job fits no slice kind")
+    else:
+        mk = np.maximum(np.searchsorted(np.asarray(MEM_GB), np.asarray(mem, np.int64), side="left"),
+                        np.maximum(np.asarray(qos, np.int64), 0))
+        if len(mk) and mk.max() > 4:
+            j = int(np.argmax(mk > 4))
+            ti = int(np.searchsorted(offs, j, side="right") - 1)
+            raise ValueError(f"trace {ti}: a job fits no slice kind")
+        need = np.maximum.reduceat(mk, offs[:-1]) if len(traces) else np.zeros(0, np.int64)
     feas = largest[None, :] >= need[:, None]                      # (traces, entries)
     return np.nonzero(feas)
 
@@ -597,12 +609,11 @@ def best_static_partition(ctx: Context, traces: Sequence[Trace], cluster_size: i
         # the candidates' only consumed output is avg_jct_s (sim.hpp:1053-1060): JCT-only runs
         table[ti_arr, e_arr] = res.metrics["avg_jct_s"]
     out = []
-    for ti in range(len(traces)):
-        row = table[ti]
-        chosen = int(np.argmin(row))  # first minimum == strict <, first wins (sim.hpp:1058)
-        if not row[chosen] < np.inf:
-            raise ValueError(f"trace {ti}: no static partition can host this trace")
-        out.append((chosen, row))
+    chosen = table.argmin(axis=1) if len(traces) else np.zeros(0, np.int64)  # first minimum
+    ok = table[np.arange(len(traces)), chosen] < np.inf  # == strict <, first wins (sim.hpp:1058)
+    if not ok.all():
+        raise ValueError(f"trace {int(np.argmin(ok))}: no static partition can host this trace")
+    out.extend(zip(chosen.tolist(), table))
     return out
 
 
