@@ -852,7 +852,9 @@ def sec_c4(args, D, runner, seeds_per_rank=1024, steps=3):
            "data": "synthetic (generate_trace seeds, generated on the device)",
            "median_jct_norm": {"optsta": float(np.median(sta.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"])),
                                "miso": float(np.median(mis.metrics["avg_jct_s"] / nop.metrics["avg_jct_s"]))},
-           "gpu_launches_per_step": "4 simulate_kernel + host-side upload/readback",
+           "gpu_launches_per_step": "5 of the library's kernels (nopart, the predictor draws and "
+                                    "miso, the pruned static search, the optsta re-run) + torch "
+                                    "helper ops (candidate feasibility, bound init) and uploads/readbacks",
            "placement": runner.last_note}
     cap = ncu_capture("sim_kernel_ncu.json")
     bound = {"bound": "latency (one warp walks one seed's sequential event chain)",
