@@ -23,6 +23,17 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         out[pol] = r.metrics.tobytes().hex()
         r2 = miso.simulate_batch(ctx, tr[:64], o, stp_cap=20000)
         out[pol + "_series"] = "".join(s.tobytes().hex() for s in r2.stp) + r2.metrics.tobytes().hex()
+    # multi-instance jobs (clones spawned mid-run) and a QoS class, smaller cluster
+    ht = miso.generate_traces(range(12), 120, lambda_s=20.0)
+    for i, t in enumerate(ht):
+        if i % 3 == 0:
+            t.instances = np.array([1] * 10 + [3] + [1] * 109, np.uint8)
+        if i % 4 == 1:
+            t.qos_kind = np.array([-1] * 50 + [2] + [-1] * 69, np.int8)
+    for pol in ("miso", "oracle"):
+        o = miso.SimOptions(policy=pol, cluster_size=8, predictor="noisy")
+        r = miso.simulate_batch(ctx, list(ht), o, stp_cap=5000)
+        out[pol + "_clones"] = r.metrics.tobytes().hex() + "".join(s.tobytes().hex() for s in r.stp)
     o = miso.SimOptions(policy="miso", cluster_size=100, predictor="noisy")
     ts = []
     for _ in range(3):
