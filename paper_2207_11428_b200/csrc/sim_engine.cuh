@@ -619,7 +619,11 @@ struct Engine {
       const uint32_t t = __shfl_sync(0xffffffffu, lane == 0 ? ring_ld(&R.tail) : 0u, 0);  // one view
       if (t == h) {
         __nanosleep(32);
-        if (++idle > (1u << 28)) return;  // watchdog (never expected): the engine stopped posting
+        if (++idle > (1u << 28)) {  // watchdog (never expected): the engine stopped posting
+          if (lane == 0) R.quit = 2;  // the engine reports the run as failed
+          __syncwarp();
+          return;
+        }
         continue;
       }
       idle = 0;
